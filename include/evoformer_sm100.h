@@ -1,0 +1,182 @@
+/*
+ * evoformer_sm100.h -- C ABI of libevoformer_sm100.so, the B200 (sm_100a)
+ * kernels behind the Evoformer hot path of the reference package `evotrain`
+ * (reference: /root/reference/pkg/src/evotrain, abbreviated src/).
+ *
+ * The reference boundary is a pure-Python operator API; each entry point
+ * below names the reference interface it replaces (file:line).  The Python
+ * host package `paper_2207_05477_b200` binds these through ctypes (see
+ * INTEGRATION.md for the binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *  - Every function returns EVO_OK (0) or an EVO_ERR_* code; the message of
+ *    the last failure on the calling thread is evo_last_error().
+ *  - The caller allocates every buffer (device pointers).  Workspaces are
+ *    sized with the matching *_workspace() query.  No host synchronisation;
+ *    all work is enqueued on `stream` (a cudaStream_t passed as void*).
+ *  - Storage dtype codes: EVO_F32 (fp32 parity mode) or EVO_BF16 (bf16
+ *    storage, fp32 math).  Parameters and their gradients are always fp32
+ *    (the fused-buffer regions of src/fusion.py:84-111); residual-stream
+ *    gradients are fp32.
+ *  - Row-major tensors.  "Tokens" are rows of [B, L] problems: the token
+ *    of (batch b, position l) is row b*tok_sb + l*tok_sl, which lets the
+ *    four attention variants (MSA row/column, triangle start/end) read one
+ *    token-major buffer without any transpose (src/model.py:320-398).
+ */
+#ifndef EVOFORMER_SM100_H
+#define EVOFORMER_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVO_OK 0
+#define EVO_ERR_ARG 1         /* shape/argument contract (DimensionError / ContractError) */
+#define EVO_ERR_CUDA 2        /* CUDA runtime / launch failure */
+#define EVO_ERR_UNSUPPORTED 3 /* no kernel for this shape/dtype/device */
+#define EVO_ERR_INTERNAL 4
+
+#define EVO_F32 0
+#define EVO_BF16 1
+
+/* Partial-sum rows used by every deterministic column reduction. */
+#define EVO_PARTIAL_BLOCKS 256
+
+/* ---- library ------------------------------------------------------------ */
+const char* evo_last_error(void);
+int evo_version(void);
+/* 0 if the current device is sm_100 (B200) and the kernels can run. */
+int evo_device_check(int* sm_major, int* sm_minor, int* num_sms);
+/* Kernel-launch counter (launches issued by this library on this thread). */
+int64_t evo_launch_count(void);
+
+/* ---- dense projections ----------------------------------------------------
+ * Replaces the np.matmul projections of src/attention.py:141,167,173,
+ * src/model.py:314,346-347,363-364,378.  Row-major, batched-strided:
+ *   C_b[M,N] = alpha * op(A_b)[M,K] . op(B_b)[K,N] + beta * C_b
+ * ab_dtype: EVO_F32 (true fp32, no TF32) or EVO_BF16; c_dtype: F32 or BF16.
+ * Routed to the hand-written tcgen05 GEMM when the shape is supported,
+ * else cuBLAS (plain library GEMM). */
+int evo_gemm(int64_t M, int64_t N, int64_t K,
+             const void* A, int64_t lda, int trans_a, int64_t stride_a,
+             const void* B, int64_t ldb, int trans_b, int64_t stride_b,
+             void* C, int64_t ldc, int64_t stride_c, int batch,
+             float alpha, float beta, int ab_dtype, int c_dtype, void* stream);
+
+/* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
+ * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */
+int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const float* beta,
+                      void* y, int y_dtype, float* mean, float* rstd,
+                      int64_t rows, int64_t C, float eps, void* stream);
+/* dx = dres + LN'(dy) (dres nullable; dx may alias dres), dgamma/dbeta
+ * written (accumulate=0) or added (accumulate=1).  ws: workspace bytes from
+ * evo_layernorm_bwd_workspace. */
+int64_t evo_layernorm_bwd_workspace(int64_t rows, int64_t C);
+int evo_layernorm_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype,
+                      const float* mean, const float* rstd, const float* gamma,
+                      const float* dres, float* dx, float* dgamma, float* dbeta,
+                      int accumulate, void* ws, int64_t rows, int64_t C, void* stream);
+
+/* ---- elementwise glue (src/tensor.py:244-331) ---------------------------- */
+/* out = res + y + bias (res nullable, bias nullable). */
+int evo_bias_residual(const void* res, int res_dtype, const void* y, int y_dtype,
+                      const float* bias, void* out, int out_dtype,
+                      int64_t rows, int64_t C, void* stream);
+/* y = relu(y + bias), in place. */
+int evo_bias_relu(void* y, int dtype, const float* bias, int64_t rows, int64_t C, void* stream);
+/* dh *= (h > 0) in place; db (+)= colsum(dh). */
+int evo_relu_bwd_colsum(void* dh, const void* h, int dtype, float* db, int accumulate,
+                        void* ws, int64_t rows, int64_t C, void* stream);
+/* out (+)= colsum(x) (x fp32 or bf16); optionally y = cast(x) to y_dtype. */
+int64_t evo_colsum_workspace(int64_t C);
+int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate,
+                    void* y, int y_dtype, void* ws, int64_t rows, int64_t C, void* stream);
+int evo_cast(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, void* stream);
+/* in-place y *= s (fp32) */
+int evo_scale_inplace(float* y, float s, int64_t n, void* stream);
+
+/* ---- gated attention core (src/attention.py:118-233) ---------------------
+ * qkvg: [tokens, 4*H*D] = x.[Wq|Wk|Wv|Wg] (row stride ld_qkvg).  Computes
+ *   logits = (q.k^T)/sqrt(D) + (mask-1)*1e9 + nb,  w = softmax(logits),
+ *   ctx = w.v,  gate = sigmoid(g + bg),  gated = ctx*gate
+ * in the reference's accumulation order (:151-161).  mask is fp32 {0,1}
+ * indexed b*mask_sb + l*mask_sl.  bias_t is nb transposed, [H, Lk, Lq]
+ * (bias_t[h,j,i] = nb[h,i,j]); nullable.  lse: [B, H, L, 2] fp32 = (row max,
+ * 1/row sum) of the logits -- kept apart because at a fully-masked row the
+ * logits sit at -1e9 where m + log(sum) is not representable.
+ * ctx/gate/gated: [tokens, H*D] storage dtype. */
+int evo_attn_fwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
+                 int64_t mask_sl, const float* bias_t, const float* bg,
+                 void* ctx, void* gate, void* gated, float* lse,
+                 int64_t B, int64_t L, int64_t H, int64_t D, int64_t tok_sb, int64_t tok_sl,
+                 int dtype, void* stream);
+/* Backward closure (src/attention.py:178-221) from d(gated):
+ * writes all four slots of dqkvg [tokens, 4*H*D] (dq, dk, dv, d(g pre-act)),
+ * dbias_t [H, Lk, Lq] = sum over batches of dlogits (nullable when no bias),
+ * dbg (+)= colsum of d(g pre-act). */
+int64_t evo_attn_bwd_workspace(int64_t B, int64_t L, int64_t H, int64_t D, int dtype);
+int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
+                 int64_t mask_sl, const float* bias_t, const void* ctx, const void* gate,
+                 const void* dgated, const float* lse, void* dqkvg, float* dbias_t,
+                 float* dbg, int accumulate, void* ws, size_t ws_bytes,
+                 int64_t B, int64_t L, int64_t H, int64_t D, int64_t tok_sb, int64_t tok_sl,
+                 int dtype, void* stream);
+
+/* ---- pair bias (src/model.py:312-317) ------------------------------------
+ * z: [R*R, C] pair tokens.  P[x,y,h] = LN(z[x,y]).w_bias[:,h]; written as
+ * bias_t[h,x,y] (transposed_layout=0, triangle end) or bias_t[h,y,x]
+ * (transposed_layout=1, MSA row / triangle start). */
+int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
+                      const float* w_bias, float* bias_t, float* mean, float* rstd,
+                      int64_t R, int64_t C, int64_t H, int transposed_layout, void* stream);
+int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H);
+/* dz += LN_bwd(dP . w_bias^T); dln_g, dln_b, dw_bias (+)= ... */
+int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
+                      const float* ln_g, const float* ln_b, const float* w_bias, const float* dbias_t,
+                      int transposed_layout, float* dz, float* dln_g, float* dln_b,
+                      float* dw_bias, int accumulate, void* ws,
+                      int64_t R, int64_t C, int64_t H, void* stream);
+
+/* ---- outer product mean (src/model.py:351-378) ---------------------------
+ * ab: [S*R, 2k] = LN(m).[Wl|Wr]; a = (ab[:, :k]+bl)*mask, c = (ab[:, k:]+br)*mask
+ * written as [S, R*k] each. */
+int evo_opm_proj(const void* ab, const float* bl, const float* br, const float* mask,
+                 void* a, void* c, int64_t SR, int64_t k, int dtype, void* stream);
+/* da, dc [S, R*k] -> d_ab [S*R, 2k] (masked), dbl/dbr (+)= colsums. */
+int evo_opm_proj_bwd(const void* da, const void* dc, const float* mask, void* d_ab,
+                     float* dbl, float* dbr, int accumulate, void* ws,
+                     int64_t SR, int64_t k, int dtype, void* stream);
+/* rec[i,j] = 1/(sum_s m[s,i] m[s,j] + 1e-3);  outn[i,j,p*k+q] = num[i*k+p, j*k+q]*rec[i,j] */
+int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* rec,
+                     void* outn, int out_dtype, int64_t S, int64_t R, int64_t k, void* stream);
+/* dnum[i*k+p, j*k+q] = doutn[i,j,p*k+q] * rec[i,j] */
+int evo_opm_norm_bwd(const void* doutn, int in_dtype, const float* rec, void* dnum,
+                     int out_dtype, int64_t R, int64_t k, void* stream);
+
+/* ---- loss (src/harness.py:313-320) ---------------------------------------
+ * loss = km*sum(msa^2) + kz*sum(pair^2);  dmsa = 2*km*msa, dpair = 2*kz*pair (fp32). */
+int64_t evo_sq_loss_workspace(void);
+int evo_sq_loss(const void* msa, int64_t n_m, const void* pair, int64_t n_z, int dtype,
+                float km, float kz, float* loss, float* dmsa, float* dpair, void* ws,
+                void* stream);
+
+/* ---- fused-buffer optimizer (src/fusion.py:150-233) ----------------------
+ * One fp64 sum-of-squares pass over the pooled grad region, then one pass of
+ * clip (scale = clip/norm if norm > clip) + Adam (bias-corrected) + EMA over
+ * all five regions, optionally writing a bf16 shadow of the params.
+ * Elementwise arithmetic is IEEE round-to-nearest in the reference's order,
+ * so the trajectory is bitwise the reference's. */
+int64_t evo_sumsq_workspace(void);
+int evo_sumsq_f64(const float* g, int64_t n, double* out, void* ws, void* stream);
+int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema,
+                      void* p_bf16, int64_t n, const double* sumsq, double clip,
+                      float lr, float b1, float omb1, float b2, float omb2, float eps,
+                      float bc1, float bc2, float decay, float omdecay, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVOFORMER_SM100_H */

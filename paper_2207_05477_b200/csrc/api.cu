@@ -1,0 +1,268 @@
+// Library plumbing, dense projections (GEMM routing) and elementwise glue.
+#include <cublas_v2.h>
+
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace evo {
+
+static thread_local std::string g_last_error;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+
+// ---------------------------------------------------------------------------
+// cuBLAS handle per (thread, device); a fixed workspace so the handle is
+// usable inside CUDA-graph capture.
+
+struct BlasState {
+  cublasHandle_t h = nullptr;
+  void* ws = nullptr;
+};
+
+static cublasHandle_t blas_handle(cudaStream_t s) {
+  static thread_local BlasState st[16];
+  int dev = 0;
+  EVO_CUDA(cudaGetDevice(&dev));
+  BlasState& b = st[dev & 15];
+  if (!b.h) {
+    if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasCreate failed");
+    const size_t ws = size_t(32) << 20;
+    EVO_CUDA(cudaMalloc(&b.ws, ws));
+    cublasSetWorkspace(b.h, b.ws, ws);
+    cublasSetMathMode(b.h, CUBLAS_DEFAULT_MATH);  // never TF32
+  }
+  cublasSetStream(b.h, s);
+  return b.h;
+}
+
+static cudaDataType_t cuda_dt(int d) {
+  if (d == EVO_F32) return CUDA_R_32F;
+  if (d == EVO_BF16) return CUDA_R_16BF;
+  throw Error(EVO_ERR_ARG, "bad dtype code");
+}
+
+// tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
+bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
+                 const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
+                 int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// elementwise kernels
+
+template <typename TR, typename TY, typename TO>
+__global__ void bias_residual_kernel(const TR* __restrict__ res, const TY* __restrict__ y,
+                                     const float* __restrict__ bias, TO* __restrict__ out,
+                                     int64_t n, int64_t C) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = to_f(y[i]);
+    if (bias) v = v + bias[i % C];
+    float r = res ? to_f(res[i]) : 0.f;
+    out[i] = from_f<TO>(res ? r + v : v);
+  }
+}
+
+template <typename T>
+__global__ void bias_relu_kernel(T* __restrict__ y, const float* __restrict__ bias, int64_t n, int64_t C) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = to_f(y[i]) + (bias ? bias[i % C] : 0.f);
+    y[i] = from_f<T>(fmaxf(v, 0.f));
+  }
+}
+
+template <typename TX, typename TY>
+__global__ void cast_kernel(const TX* __restrict__ x, TY* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = from_f<TY>(to_f(x[i]));
+}
+
+__global__ void scale_kernel(float* y, float s, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] *= s;
+}
+
+// colsum partials with optional cast-copy: block b handles rows b, b+G, ...
+template <typename TX, typename TY>
+__global__ void colsum_cast_kernel(const TX* __restrict__ x, TY* __restrict__ y,
+                                   float* __restrict__ partials, int64_t rows, int64_t C) {
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+      float v = to_f(x[r * C + c]);
+      acc += v;
+      if (y) y[r * C + c] = from_f<TY>(v);
+    }
+    partials[blockIdx.x * C + c] = acc;
+  }
+}
+
+template <typename T>
+__global__ void relu_bwd_colsum_kernel(T* __restrict__ dh, const T* __restrict__ h,
+                                       float* __restrict__ partials, int64_t rows, int64_t C) {
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+      int64_t i = r * C + c;
+      float v = to_f(h[i]) > 0.f ? to_f(dh[i]) : 0.f;
+      dh[i] = from_f<T>(v);
+      acc += v;
+    }
+    partials[blockIdx.x * C + c] = acc;
+  }
+}
+
+static unsigned ew_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (unsigned)(g < cap ? (g > 0 ? g : 1) : cap);
+}
+
+unsigned partial_grid(int64_t rows) {
+  int64_t g = rows < EVO_PARTIAL_BLOCKS ? rows : EVO_PARTIAL_BLOCKS;
+  return (unsigned)(g > 0 ? g : 1);
+}
+
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" {
+
+const char* evo_last_error(void) { return g_last_error.c_str(); }
+int evo_version(void) { return 1; }
+int64_t evo_launch_count(void) { return g_launches; }
+
+int evo_device_check(int* sm_major, int* sm_minor, int* nsm) {
+  EVO_API_BEGIN
+  int dev = 0, ma = 0, mi = 0, n = 0;
+  EVO_CUDA(cudaGetDevice(&dev));
+  EVO_CUDA(cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, dev));
+  EVO_CUDA(cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, dev));
+  EVO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  if (sm_major) *sm_major = ma;
+  if (sm_minor) *sm_minor = mi;
+  if (nsm) *nsm = n;
+  EVO_REQUIRE(ma == 10 && mi == 0, EVO_ERR_UNSUPPORTED,
+              "libevoformer_sm100 is built for sm_100a (B200); device is sm_" +
+                  std::to_string(ma) + std::to_string(mi));
+  EVO_API_END
+}
+
+int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
+             int64_t stride_a, const void* B, int64_t ldb, int trans_b, int64_t stride_b,
+             void* C, int64_t ldc, int64_t stride_c, int batch, float alpha, float beta,
+             int ab_dtype, int c_dtype, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 1, EVO_ERR_ARG, "gemm: bad extents");
+  if (M == 0 || N == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (gemm_tc_try(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, ldc, stride_c,
+                  batch, alpha, beta, ab_dtype, c_dtype, s))
+    return EVO_OK;
+  cublasHandle_t h = blas_handle(s);
+  // row-major C = op(A) op(B)  <=>  column-major C^T = op(B)^T op(A)^T
+  cublasOperation_t ob = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasOperation_t oa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasStatus_t st;
+  if (batch == 1)
+    st = cublasGemmEx(h, ob, oa, (int)N, (int)M, (int)K, &alpha, B, cuda_dt(ab_dtype), (int)ldb, A,
+                      cuda_dt(ab_dtype), (int)lda, &beta, C, cuda_dt(c_dtype), (int)ldc,
+                      CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  else
+    st = cublasGemmStridedBatchedEx(h, ob, oa, (int)N, (int)M, (int)K, &alpha, B, cuda_dt(ab_dtype),
+                                    (int)ldb, stride_b, A, cuda_dt(ab_dtype), (int)lda, stride_a,
+                                    &beta, C, cuda_dt(c_dtype), (int)ldc, stride_c, batch,
+                                    CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  EVO_REQUIRE(st == CUBLAS_STATUS_SUCCESS, EVO_ERR_CUDA,
+              "cublasGemmEx failed with status " + std::to_string((int)st));
+  EVO_API_END
+}
+
+int evo_bias_residual(const void* res, int res_dtype, const void* y, int y_dtype, const float* bias,
+                      void* out, int out_dtype, int64_t rows, int64_t C, void* stream) {
+  EVO_API_BEGIN
+  int64_t n = rows * C;
+  if (n == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = ew_grid(n);
+  EVO_DISPATCH_T(res_dtype, TR, EVO_DISPATCH_T(y_dtype, TY, EVO_DISPATCH_T(out_dtype, TO, {
+    bias_residual_kernel<TR, TY, TO><<<g, 256, 0, s>>>((const TR*)res, (const TY*)y, bias, (TO*)out, n, C);
+  })));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_bias_relu(void* y, int dtype, const float* bias, int64_t rows, int64_t C, void* stream) {
+  EVO_API_BEGIN
+  int64_t n = rows * C;
+  if (n == 0) return EVO_OK;
+  EVO_DISPATCH_T(dtype, T, {
+    bias_relu_kernel<T><<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>((T*)y, bias, n, C);
+  });
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int64_t evo_colsum_workspace(int64_t C) { return (int64_t)EVO_PARTIAL_BLOCKS * C * 4; }
+
+int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate, void* y, int y_dtype,
+                    void* ws, int64_t rows, int64_t C, void* stream) {
+  EVO_API_BEGIN
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = partial_grid(rows);
+  int bs = C >= 256 ? 256 : (int)((C + 31) / 32 * 32);
+  EVO_DISPATCH_T(x_dtype, TX, EVO_DISPATCH_T(y_dtype, TY, {
+    colsum_cast_kernel<TX, TY><<<g, bs, 0, s>>>((const TX*)x, (TY*)y, (float*)ws, rows, C);
+  }));
+  EVO_LAUNCH_CHECK();
+  finalize_partials((const float*)ws, g, C, out, accumulate, s);
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_relu_bwd_colsum(void* dh, const void* h, int dtype, float* db, int accumulate, void* ws,
+                        int64_t rows, int64_t C, void* stream) {
+  EVO_API_BEGIN
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = partial_grid(rows);
+  int bs = C >= 256 ? 256 : (int)((C + 31) / 32 * 32);
+  EVO_DISPATCH_T(dtype, T, {
+    relu_bwd_colsum_kernel<T><<<g, bs, 0, s>>>((T*)dh, (const T*)h, (float*)ws, rows, C);
+  });
+  EVO_LAUNCH_CHECK();
+  finalize_partials((const float*)ws, g, C, db, accumulate, s);
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_cast(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, void* stream) {
+  EVO_API_BEGIN
+  if (n == 0) return EVO_OK;
+  EVO_DISPATCH_T(x_dtype, TX, EVO_DISPATCH_T(y_dtype, TY, {
+    cast_kernel<TX, TY><<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>((const TX*)x, (TY*)y, n);
+  }));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_scale_inplace(float* y, float s_, int64_t n, void* stream) {
+  EVO_API_BEGIN
+  if (n == 0) return EVO_OK;
+  scale_kernel<<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>(y, s_, n);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// Pair-bias projection for MSA-row and triangle attention (src/model.py:312-317):
+//   nb[h, i, j] = LN(z)[i, j, :] . w_bias[:, h]
+// One warp per pair token: LayerNorm in registers, the H-wide projection as
+// warp reductions, written straight into the transposed bias layout the
+// attention kernels read (bias_t[h, key, query]).  Bandwidth-bound: reads
+// the pair once (R*R*C storage bytes), writes H*R*R fp32.
+//
+// Backward fuses dP -> dLN -> LayerNorm backward -> dz (+=) with the
+// w_bias / LN-affine gradient partials in one pass over the pair.
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace evo {
+
+constexpr int PB_WARPS = 8;
+constexpr int PB_HMAX = 16;
+
+template <typename T, int NPL>
+__global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
+    const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
+    const float* __restrict__ w, float* __restrict__ bias_t, float* __restrict__ mean,
+    float* __restrict__ rstd, int64_t R, int C, int H, int transposed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)PB_WARPS + (threadIdx.x >> 5);
+  if (t >= R * R) return;
+  float v[NPL];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    int c = lane + 32 * k;
+    v[k] = c < C ? to_f(z[t * C + c]) : 0.f;
+    s += v[k];
+  }
+  const float mu = warp_sum(s) / (float)C;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    int c = lane + 32 * k;
+    float d = c < C ? v[k] - mu : 0.f;
+    q += d * d;
+  }
+  const float inv = 1.0f / sqrtf(warp_sum(q) / (float)C + 1e-5f);
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    int c = lane + 32 * k;
+    v[k] = c < C ? (v[k] - mu) * inv * g[c] + b[c] : 0.f;
+  }
+  const int64_t x = t / R, y = t % R;
+  float mine = 0.f;
+#pragma unroll
+  for (int h = 0; h < PB_HMAX; ++h) {
+    if (h < H) {
+      float p = 0.f;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) {
+        int c = lane + 32 * k;
+        if (c < C) p = fmaf(v[k], w[c * H + h], p);
+      }
+      p = warp_sum(p);
+      if (lane == h) mine = p;
+    }
+  }
+  if (lane < H) {
+    int64_t o = transposed ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+    bias_t[o] = mine;
+  }
+  if (lane == 0) {
+    mean[t] = mu;
+    rstd[t] = inv;
+  }
+}
+
+template <typename T, int NPL>
+__global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
+    const T* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
+    const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
+    const float* __restrict__ dbias_t, int transposed, float* __restrict__ dz,
+    float* __restrict__ partials, int64_t R, int C, int H) {
+  extern __shared__ float sm[];  // [PB_WARPS][C*H + 2C]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int W = C * H + 2 * C;
+  float dw[NPL][PB_HMAX], dg[NPL], db[NPL];
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    dg[k] = db[k] = 0.f;
+#pragma unroll
+    for (int h = 0; h < PB_HMAX; ++h) dw[k][h] = 0.f;
+  }
+  for (int64_t t = blockIdx.x * (int64_t)PB_WARPS + warp; t < R * R;
+       t += (int64_t)gridDim.x * PB_WARPS) {
+    const int64_t x = t / R, y = t % R;
+    float dp = 0.f;
+    if (lane < H) {
+      int64_t o = transposed ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+      dp = dbias_t[o];
+    }
+    float dP[PB_HMAX];
+#pragma unroll
+    for (int h = 0; h < PB_HMAX; ++h) dP[h] = __shfl_sync(0xffffffffu, dp, h);
+    const float mu = mean[t], inv = rstd[t];
+    float xh[NPL], dxh[NPL];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      int c = lane + 32 * k;
+      if (c < C) {
+        xh[k] = (to_f(z[t * C + c]) - mu) * inv;
+        const float zl = xh[k] * g[c] + bln[c];
+        float dzl = 0.f;
+#pragma unroll
+        for (int h = 0; h < PB_HMAX; ++h) {
+          if (h < H) {
+            dzl = fmaf(dP[h], w[c * H + h], dzl);
+            dw[k][h] = fmaf(zl, dP[h], dw[k][h]);
+          }
+        }
+        dg[k] += dzl * xh[k];
+        db[k] += dzl;
+        dxh[k] = dzl * g[c];
+      } else {
+        xh[k] = dxh[k] = 0.f;
+      }
+      s1 += dxh[k];
+      s2 += dxh[k] * xh[k];
+    }
+    const float m1 = warp_sum(s1) / (float)C, m2 = warp_sum(s2) / (float)C;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      int c = lane + 32 * k;
+      if (c < C) dz[t * C + c] += inv * (dxh[k] - m1 - xh[k] * m2);
+    }
+  }
+  float* mine = sm + warp * W;
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    int c = lane + 32 * k;
+    if (c < C) {
+#pragma unroll
+      for (int h = 0; h < PB_HMAX; ++h)
+        if (h < H) mine[c * H + h] = dw[k][h];
+      mine[C * H + c] = dg[k];
+      mine[C * H + C + c] = db[k];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    float acc = 0.f;
+    for (int ww = 0; ww < PB_WARPS; ++ww) acc += sm[ww * W + c];
+    partials[(int64_t)blockIdx.x * W + c] = acc;
+  }
+}
+
+#define PB_NPL_DISPATCH(C, NPL, ...)                                          \
+  do {                                                                        \
+    if ((C) <= 32) { constexpr int NPL = 1; __VA_ARGS__; }                    \
+    else if ((C) <= 64) { constexpr int NPL = 2; __VA_ARGS__; }               \
+    else if ((C) <= 128) { constexpr int NPL = 4; __VA_ARGS__; }              \
+    else if ((C) <= 256) { constexpr int NPL = 8; __VA_ARGS__; }              \
+    else throw Error(EVO_ERR_UNSUPPORTED, "pair_bias: C > 256");              \
+  } while (0)
+
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" {
+
+int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
+                      const float* w_bias, float* bias_t, float* mean, float* rstd, int64_t R,
+                      int64_t C, int64_t H, int transposed_layout, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
+  if (R == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned grid = cdiv(R * R, PB_WARPS);
+  PB_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(dtype, T, {
+    pair_bias_fwd_kernel<T, NPL><<<grid, PB_WARPS * 32, 0, s>>>(
+        (const T*)z, ln_g, ln_b, w_bias, bias_t, mean, rstd, R, (int)C, (int)H, transposed_layout);
+  }));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H) {
+  return (int64_t)EVO_PARTIAL_BLOCKS * (C * H + 2 * C) * 4;
+}
+
+int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
+                      const float* ln_g, const float* ln_b, const float* w_bias,
+                      const float* dbias_t, int transposed_layout, float* dz, float* dln_g,
+                      float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t R,
+                      int64_t C, int64_t H, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
+  EVO_REQUIRE(ws != nullptr, EVO_ERR_ARG, "pair_bias_bwd: workspace required");
+  if (R == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t want = (R * R + PB_WARPS - 1) / PB_WARPS;
+  unsigned grid = (unsigned)(want < EVO_PARTIAL_BLOCKS ? want : EVO_PARTIAL_BLOCKS);
+  const int64_t W = C * H + 2 * C;
+  size_t smem = (size_t)PB_WARPS * W * sizeof(float);
+  float* part = (float*)ws;
+  PB_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(dtype, T, {
+    auto k = pair_bias_bwd_kernel<T, NPL>;
+    if (smem > 48 * 1024)
+      EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, PB_WARPS * 32, smem, s>>>((const T*)z, mean, rstd, ln_g, ln_b, w_bias, dbias_t,
+                                         transposed_layout, dz, part, R, (int)C, (int)H);
+  }));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  finalize_partials(part, grid, C * H, dw_bias, accumulate, s, W);
+  finalize_partials(part + C * H, grid, C, dln_g, accumulate, s, W);
+  finalize_partials(part + C * H + C, grid, C, dln_b, accumulate, s, W);
+  EVO_API_END
+}
+
+}  // extern "C"

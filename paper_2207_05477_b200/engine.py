@@ -1,0 +1,394 @@
+"""Evoformer block engine: forward and hand-written backward per module,
+on the sm_100a kernels.
+
+Mirrors the reference block (src/model.py:300-445) module by module; the
+backward of each module is written out the way the reference's fused-op
+closure is (src/attention.py:178-221) instead of going through a tape.
+Parameter gradients are written straight into the pooled grad region of
+the ``FusionEngine`` (tensor fusion, src/fusion.py) -- nothing is copied.
+
+Data layout in HBM (B=1 as in the reference features):
+  msa  [S*R, c_m]   token (s, r) -> row s*R + r      (storage dtype)
+  pair [R*R, c_z]   token (i, j) -> row i*R + j      (storage dtype)
+  residual-stream gradients d_msa / d_pair: same shapes, fp32
+The four attention variants read the same token-major buffers through
+(batch, position) strides, so MSA-column and triangle-ending attention need
+no transposes (the reference transposes, src/model.py:335-340, 388-397).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .fusion import FusionEngine
+from .model import ModelConfig
+
+F32 = torch.float32
+
+
+@dataclass
+class Variant:
+    """Attention geometry: problems are (batch b, position l); token row of
+    (b, l) is b*sb + l*sl; mask element is mask[b*msb + l*msl]."""
+
+    name: str
+    B: int
+    L: int
+    sb: int
+    sl: int
+    msb: int
+    msl: int
+    mask: str          # "msa" or "pair"
+    bias: bool         # pair-derived bias present
+    transposed: bool   # bias_t layout flag for evo_pair_bias_fwd
+
+
+def variants(cfg: ModelConfig) -> dict:
+    S, R = cfg.n_seq, cfg.n_res
+    return {
+        # src/model.py:320-328: batch s, keys r, mask msa[s, r]
+        "row_attn": Variant("row_attn", S, R, R, 1, R, 1, "msa", True, True),
+        # src/model.py:331-341: batch r, keys s, mask msa_t[r, s] = msa[s, r]
+        "col_attn": Variant("col_attn", R, S, 1, R, 1, R, "msa", False, False),
+        # src/model.py:381-398 (start): batch i, keys j, mask pair[i, j]
+        "tri_start": Variant("tri_start", R, R, R, 1, R, 1, "pair", True, True),
+        # (end): batch j of pair^T, keys i: token (a, b) = pair row b*R + a
+        "tri_end": Variant("tri_end", R, R, 1, R, 1, R, "pair", True, False),
+    }
+
+
+class DeviceFeatures:
+    """Features resident in HBM (fp32): msa_feat [S*R, F], pair_feat [R*R, F],
+    msa_mask [S*R], pair_mask [R*R]."""
+
+    def __init__(self, feats, device, cfg: ModelConfig):
+        S, R, F = cfg.n_seq, cfg.n_res, cfg.feat_dim
+
+        def up(a, shape):
+            return torch.as_tensor(np.ascontiguousarray(a, np.float32)).reshape(shape).to(device)
+
+        self.msa_feat = up(feats.msa_feat, (S * R, F))
+        self.pair_feat = up(feats.pair_feat, (R * R, F))
+        self.msa_mask = up(feats.msa_mask, (S * R,))
+        self.pair_mask = up(feats.pair_mask, (R * R,))
+
+    def copy_from_host(self, host):
+        """In-place refresh from pinned host tensors (keeps device pointers
+        stable for CUDA-graph replay)."""
+        for k in ("msa_feat", "pair_feat", "msa_mask", "pair_mask"):
+            getattr(self, k).copy_(getattr(host, k), non_blocking=True)
+
+
+class BlockEngine:
+    def __init__(self, cfg: ModelConfig, store: FusionEngine, act_dtype=torch.bfloat16):
+        cfg.validate()
+        self.cfg = cfg
+        self.st = store
+        self.dt = act_dtype
+        self.var = variants(cfg)
+
+    # -- parameter access ---------------------------------------------------------
+
+    def P(self, name):
+        return self.st.param(name)
+
+    def G(self, name):
+        return self.st.grad(name)
+
+    def W(self, name, rows):
+        """Projection weight in the storage dtype as a [rows, cols] matrix."""
+        w = self.st.weight(name)
+        return w.view(rows, -1)
+
+    def Gm(self, name, rows):
+        return self.st.grad(name).view(rows, -1)
+
+    def mask(self, feats: DeviceFeatures, which: str):
+        return feats.msa_mask if which == "msa" else feats.pair_mask
+
+    # -- gated attention module (LN -> [pair bias] -> fused attention -> residual)
+
+    def attn_fwd(self, x, prefix, v: Variant, feats, pair=None):
+        cfg, dt = self.cfg, self.dt
+        T, C = x.shape
+        H = cfg.heads
+        D = C // H
+        HD = H * D
+        xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
+        nb = pmu = prs = None
+        if v.bias:
+            z = pair if pair is not None else x
+            nb, pmu, prs = ops.pair_bias_fwd(z, self.P(f"{prefix}.bias_ln_g"),
+                                             self.P(f"{prefix}.bias_ln_b"),
+                                             self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.transposed)
+        qkvg = torch.empty((T, 4 * HD), dtype=dt, device=x.device)
+        for s, f in enumerate(("wq", "wk", "wv", "wg")):
+            ops.gemm(xl, self.W(f"{prefix}.attn.{f}", C), qkvg[:, s * HD:(s + 1) * HD])
+        mask = self.mask(feats, v.mask)
+        ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, v.msb, v.msl, nb,
+                                             self.P(f"{prefix}.attn.bg"), v.B, v.L, H, D, v.sb, v.sl)
+        y = torch.empty((T, C), dtype=dt, device=x.device)
+        ops.gemm(gated, self.W(f"{prefix}.attn.wo", HD), y)
+        out = torch.empty((T, C), dtype=dt, device=x.device)
+        ops.bias_residual(x, y, self.P(f"{prefix}.attn.bo"), out)
+        saved = dict(x=x, xl=xl, mu=mu, rs=rs, qkvg=qkvg, ctx=ctx, gate=gate, gated=gated, lse=lse,
+                     nb=nb, pmu=pmu, prs=prs, pair=pair if pair is not None else x)
+        return out, saved
+
+    def attn_bwd(self, d, sv, prefix, v: Variant, feats, dpair=None):
+        """``d`` (fp32 [T, C]) is d(out) on entry and d(x) on exit.  The
+        pair-bias gradient is added into ``dpair`` (or ``d`` for triangle
+        attention, whose bias comes from its own input)."""
+        cfg, dt = self.cfg, self.dt
+        T, C = d.shape
+        H = cfg.heads
+        D = C // H
+        HD = H * D
+        d_act = torch.empty((T, C), dtype=dt, device=d.device)
+        ops.colsum_cast(d, self.G(f"{prefix}.attn.bo"), y=d_act)
+        ops.gemm(sv["gated"], d_act, self.Gm(f"{prefix}.attn.wo", HD), ta=True)
+        dgated = torch.empty((T, HD), dtype=dt, device=d.device)
+        ops.gemm(d_act, self.W(f"{prefix}.attn.wo", HD), dgated, tb=True)
+        del d_act
+        mask = self.mask(feats, v.mask)
+        dqkvg, dnb = ops.attn_bwd(sv["qkvg"], mask, v.msb, v.msl, sv["nb"], sv["ctx"], sv["gate"],
+                                  dgated, sv["lse"], self.G(f"{prefix}.attn.bg"), v.B, v.L, H, D,
+                                  v.sb, v.sl, want_dbias=v.bias)
+        del dgated
+        xl = sv["xl"]
+        for s, f in enumerate(("wq", "wk", "wv", "wg")):
+            ops.gemm(xl, dqkvg[:, s * HD:(s + 1) * HD], self.Gm(f"{prefix}.attn.{f}", C), ta=True)
+        dxl = torch.empty((T, C), dtype=F32, device=d.device)
+        for s, f in enumerate(("wq", "wk", "wv", "wg")):
+            ops.gemm(dqkvg[:, s * HD:(s + 1) * HD], self.W(f"{prefix}.attn.{f}", C), dxl, tb=True,
+                     beta=0.0 if s == 0 else 1.0)
+        del dqkvg
+        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d, d,
+                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+        if v.bias:
+            target = dpair if dpair is not None else d
+            ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
+                              self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
+                              v.transposed, target, self.G(f"{prefix}.bias_ln_g"),
+                              self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
+                              cfg.n_res, H)
+
+    # -- transition (src/model.py:344-348) ------------------------------------------
+
+    def trans_fwd(self, x, prefix):
+        dt = self.dt
+        T, C = x.shape
+        xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
+        w1 = self.W(f"{prefix}.w1", C)
+        h = torch.empty((T, w1.shape[1]), dtype=dt, device=x.device)
+        ops.gemm(xl, w1, h)
+        ops.bias_relu_(h, self.P(f"{prefix}.b1"))
+        y = torch.empty((T, C), dtype=dt, device=x.device)
+        ops.gemm(h, self.W(f"{prefix}.w2", w1.shape[1]), y)
+        out = torch.empty((T, C), dtype=dt, device=x.device)
+        ops.bias_residual(x, y, self.P(f"{prefix}.b2"), out)
+        return out, dict(x=x, xl=xl, mu=mu, rs=rs, h=h)
+
+    def trans_bwd(self, d, sv, prefix):
+        dt = self.dt
+        T, C = d.shape
+        h = sv["h"]
+        F = h.shape[1]
+        d_act = torch.empty((T, C), dtype=dt, device=d.device)
+        ops.colsum_cast(d, self.G(f"{prefix}.b2"), y=d_act)
+        ops.gemm(h, d_act, self.Gm(f"{prefix}.w2", F), ta=True)
+        dh = torch.empty((T, F), dtype=dt, device=d.device)
+        ops.gemm(d_act, self.W(f"{prefix}.w2", F), dh, tb=True)
+        del d_act
+        ops.relu_bwd_colsum_(dh, h, self.G(f"{prefix}.b1"))
+        ops.gemm(sv["xl"], dh, self.Gm(f"{prefix}.w1", C), ta=True)
+        dxl = torch.empty((T, C), dtype=F32, device=d.device)
+        ops.gemm(dh, self.W(f"{prefix}.w1", C), dxl, tb=True)
+        del dh
+        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d, d,
+                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+
+    # -- outer product mean (src/model.py:351-378) -----------------------------------
+
+    def opm_fwd(self, msa_in, prefix, feats, pair_res=None):
+        """Returns pair_res + OPM(msa_in) (or OPM alone when pair_res is None)."""
+        cfg, dt = self.cfg, self.dt
+        S, R, k = cfg.n_seq, cfg.n_res, cfg.opm_dim
+        SR, Cm = msa_in.shape
+        xl, mu, rs = ops.layernorm(msa_in, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
+        ab = torch.empty((SR, 2 * k), dtype=dt, device=msa_in.device)
+        ops.gemm(xl, self.W(f"{prefix}.w_left", Cm), ab[:, :k])
+        ops.gemm(xl, self.W(f"{prefix}.w_right", Cm), ab[:, k:])
+        a, c = ops.opm_proj(ab, self.P(f"{prefix}.b_left"), self.P(f"{prefix}.b_right"),
+                            feats.msa_mask, k)
+        del ab
+        num = torch.empty((R * k, R * k), dtype=dt, device=msa_in.device)
+        ops.gemm(a.view(S, R * k), c.view(S, R * k), num, ta=True)
+        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt)
+        del num
+        y = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
+        ops.gemm(outn, self.W(f"{prefix}.w_out", k * k), y)
+        out = torch.empty_like(y)
+        ops.bias_residual(pair_res, y, self.P(f"{prefix}.b_out"), out)
+        return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
+
+    def opm_bwd_core(self, d, sv, prefix, feats):
+        """d(pair_mid) (fp32) -> dxl (fp32 [S*R, c_m]); the LayerNorm backward is
+        applied later by opm_ln_bwd so it can accumulate into d(msa_in)."""
+        cfg, dt = self.cfg, self.dt
+        S, R, k = cfg.n_seq, cfg.n_res, cfg.opm_dim
+        RR, Cz = d.shape
+        SR, Cm = sv["x"].shape
+        d_act = torch.empty((RR, Cz), dtype=dt, device=d.device)
+        ops.colsum_cast(d, self.G(f"{prefix}.b_out"), y=d_act)
+        ops.gemm(sv["outn"], d_act, self.Gm(f"{prefix}.w_out", k * k), ta=True)
+        doutn = torch.empty((RR, k * k), dtype=dt, device=d.device)
+        ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
+        del d_act
+        dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt)
+        del doutn
+        a2, c2 = sv["a"].view(S, R * k), sv["c"].view(S, R * k)
+        da = torch.empty((S, R * k), dtype=dt, device=d.device)
+        dc = torch.empty((S, R * k), dtype=dt, device=d.device)
+        ops.gemm(c2, dnum, da, tb=True)
+        ops.gemm(a2, dnum, dc)
+        del dnum
+        d_ab = ops.opm_proj_bwd(da, dc, feats.msa_mask, self.G(f"{prefix}.b_left"),
+                                self.G(f"{prefix}.b_right"), k)
+        xl = sv["xl"]
+        ops.gemm(xl, d_ab[:, :k], self.Gm(f"{prefix}.w_left", Cm), ta=True)
+        ops.gemm(xl, d_ab[:, k:], self.Gm(f"{prefix}.w_right", Cm), ta=True)
+        dxl = torch.empty((SR, Cm), dtype=F32, device=d.device)
+        ops.gemm(d_ab[:, :k], self.W(f"{prefix}.w_left", Cm), dxl, tb=True)
+        ops.gemm(d_ab[:, k:], self.W(f"{prefix}.w_right", Cm), dxl, tb=True, beta=1.0)
+        return dxl
+
+    def opm_ln_bwd(self, dxl, sv, prefix, d_msa):
+        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d_msa, d_msa,
+                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+
+    # -- branches (the split used by branch parallelism, src/harness.py:447-486) ----
+
+    def msa_branch_fwd(self, i, msa_in, pair_in, feats):
+        p = f"block{i}"
+        msa, s1 = self.attn_fwd(msa_in, f"{p}.row_attn", self.var["row_attn"], feats, pair=pair_in)
+        msa, s2 = self.attn_fwd(msa, f"{p}.col_attn", self.var["col_attn"], feats)
+        msa, s3 = self.trans_fwd(msa, f"{p}.msa_trans")
+        return msa, (s1, s2, s3)
+
+    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats):
+        """d_msa: d(msa_out) -> d(msa_in) in place; the pair-bias path adds
+        d(pair_in) into d_pair_acc."""
+        p = f"block{i}"
+        s1, s2, s3 = saved
+        self.trans_bwd(d_msa, s3, f"{p}.msa_trans")
+        self.attn_bwd(d_msa, s2, f"{p}.col_attn", self.var["col_attn"], feats)
+        self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc)
+
+    def pair_branch_fwd(self, i, pair_mid, feats):
+        p = f"block{i}"
+        pair, s1 = self.attn_fwd(pair_mid, f"{p}.tri_start", self.var["tri_start"], feats)
+        pair, s2 = self.attn_fwd(pair, f"{p}.tri_end", self.var["tri_end"], feats)
+        pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
+        return pair, (s1, s2, s3)
+
+    def pair_branch_bwd(self, i, d_pair, saved, feats):
+        """d(pair_out) -> d(pair_mid) in place."""
+        p = f"block{i}"
+        s1, s2, s3 = saved
+        self.trans_bwd(d_pair, s3, f"{p}.pair_trans")
+        self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats)
+        self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats)
+
+    # -- whole block (src/model.py:431-445) -------------------------------------------
+
+    def block_fwd(self, i, msa_in, pair_in, feats):
+        msa, sm = self.msa_branch_fwd(i, msa_in, pair_in, feats)
+        pair_mid, so = self.opm_fwd(msa_in, f"block{i}.opm", feats, pair_res=pair_in)
+        pair, sp = self.pair_branch_fwd(i, pair_mid, feats)
+        return msa, pair, (sm, so, sp)
+
+    def block_bwd(self, i, d_msa, d_pair, saved, feats):
+        """In place: (d msa_out, d pair_out) -> (d msa_in, d pair_in)."""
+        sm, so, sp = saved
+        self.pair_branch_bwd(i, d_pair, sp, feats)            # d_pair = d(pair_mid)
+        dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats)
+        self.msa_branch_bwd(i, d_msa, d_pair, sm, feats)      # d_pair += bias path
+        self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)      # d_msa += OPM path
+
+    # -- embedding, recycling, loss (src/model.py:448-478, src/harness.py:313-320) ----
+
+    def embed_fwd(self, feats: DeviceFeatures, prev=None):
+        cfg, dt = self.cfg, self.dt
+        S, R = cfg.n_seq, cfg.n_res
+        dev = feats.msa_feat.device
+        ym = torch.empty((S * R, cfg.c_m), dtype=F32, device=dev)
+        ops.gemm(feats.msa_feat, self.P("msa_embed.w"), ym)
+        msa = torch.empty((S * R, cfg.c_m), dtype=dt, device=dev)
+        ops.bias_residual(None, ym, self.P("msa_embed.b"), msa)
+        yz = torch.empty((R * R, cfg.c_z), dtype=F32, device=dev)
+        ops.gemm(feats.pair_feat, self.P("pair_embed.w"), yz)
+        pair = torch.empty((R * R, cfg.c_z), dtype=dt, device=dev)
+        ops.bias_residual(None, yz, self.P("pair_embed.b"), pair)
+        rec = None
+        if prev is not None:
+            pm, pz = prev[0][:R].contiguous(), prev[1]
+            fb, m1, r1 = ops.layernorm(pm, self.P("recycle_m.g"), self.P("recycle_m.b"), F32)
+            ops.bias_residual(msa[:R], fb, None, msa[:R])
+            fz, m2, r2 = ops.layernorm(pz, self.P("recycle_z.g"), self.P("recycle_z.b"), F32)
+            ops.bias_residual(pair, fz, None, pair)
+            rec = (pm, m1, r1, pz, m2, r2)
+        return msa, pair, rec
+
+    def embed_bwd(self, d_msa, d_pair, feats: DeviceFeatures, rec):
+        ops.gemm(feats.msa_feat, d_msa, self.G("msa_embed.w"), ta=True)
+        ops.colsum_cast(d_msa, self.G("msa_embed.b"))
+        ops.gemm(feats.pair_feat, d_pair, self.G("pair_embed.w"), ta=True)
+        ops.colsum_cast(d_pair, self.G("pair_embed.b"))
+        if rec is not None:
+            R = self.cfg.n_res
+            pm, m1, r1, pz, m2, r2 = rec
+            scratch = torch.empty_like(d_msa[:R])
+            ops.layernorm_bwd(pm, d_msa[:R], m1, r1, self.P("recycle_m.g"), None, scratch,
+                              self.G("recycle_m.g"), self.G("recycle_m.b"))
+            scratch = torch.empty_like(d_pair)
+            ops.layernorm_bwd(pz, d_pair, m2, r2, self.P("recycle_z.g"), None, scratch,
+                              self.G("recycle_z.g"), self.G("recycle_z.b"))
+
+    def loss(self, msa, pair):
+        cfg = self.cfg
+        km = float(np.float32(1.0 / (cfg.n_seq * cfg.n_res * cfg.c_m)))
+        kz = float(np.float32(1.0 / (cfg.n_res * cfg.n_res * cfg.c_z)))
+        return ops.sq_loss(msa, pair, km, kz)
+
+    # -- whole model ---------------------------------------------------------------------
+
+    def forward_only(self, feats, prev=None):
+        msa, pair, _ = self.embed_fwd(feats, prev)
+        for i in range(self.cfg.n_blocks):
+            msa, pair, _ = self.block_fwd(i, msa, pair, feats)
+        return msa, pair
+
+    def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1):
+        """``_serial_grads`` (src/harness.py:327-352): n-1 untaped recycling
+        passes, one differentiated pass; grads land in the pooled region.
+        Returns (loss device tensor [1], (msa, pair))."""
+        self.st.zero_grads()
+        prev = None
+        for _ in range(max(0, n_cycles - 1)):
+            prev = self.forward_only(feats, prev)
+        msa, pair, rec = self.embed_fwd(feats, prev)
+        saved = []
+        for i in range(self.cfg.n_blocks):
+            msa, pair, sv = self.block_fwd(i, msa, pair, feats)
+            saved.append(sv)
+        loss, d_msa, d_pair = self.loss(msa, pair)
+        for i in reversed(range(self.cfg.n_blocks)):
+            self.block_bwd(i, d_msa, d_pair, saved[i], feats)
+            saved[i] = None
+        self.embed_bwd(d_msa, d_pair, feats, rec)
+        return loss, (msa, pair)

@@ -1,0 +1,221 @@
+"""Tensor-level wrappers over the C ABI.  PyTorch provides device memory and
+the current stream; every byte of arithmetic runs in libevoformer_sm100.so.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import BF16, F32, call
+
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+def dcode(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}") from None
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, ta: bool = False, tb: bool = False,
+         alpha: float = 1.0, beta: float = 0.0):
+    """c = alpha * op(a) @ op(b) + beta * c for row-major 2-D (possibly
+    column-sliced) views with unit inner stride."""
+    for t in (a, b, c):
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("gemm operands must be 2-D with unit inner stride")
+    M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
+    Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
+    if K != Kb or tuple(c.shape) != (M, N):
+        raise ValueError(f"gemm shape mismatch: op(a)={M}x{K} op(b)={Kb}x{N} c={tuple(c.shape)}")
+    if a.dtype != b.dtype:
+        raise TypeError("gemm: a and b must share a dtype")
+    call("evo_gemm", M, N, K, ptr(a), a.stride(0), int(ta), 0, ptr(b), b.stride(0), int(tb), 0,
+         ptr(c), c.stride(0), 0, 1, alpha, beta, dcode(a), dcode(c), stream())
+
+
+# ---------------------------------------------------------------------------
+# LayerNorm / glue
+
+
+def layernorm(x: torch.Tensor, g: torch.Tensor, b: torch.Tensor, out_dtype, eps: float = 1e-5):
+    rows, C = x.shape
+    y = torch.empty((rows, C), dtype=out_dtype, device=x.device)
+    mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+    call("evo_layernorm_fwd", ptr(x), dcode(x), ptr(g), ptr(b), ptr(y), dcode(y), ptr(mean),
+         ptr(rstd), rows, C, eps, stream())
+    return y, mean, rstd
+
+
+def layernorm_bwd(x, dy, mean, rstd, g, dres, dx, dgamma, dbeta, accumulate=False):
+    rows, C = x.shape
+    ws = _ws(_lib.load().evo_layernorm_bwd_workspace(rows, C), x.device)
+    call("evo_layernorm_bwd", ptr(x), dcode(x), ptr(dy), dcode(dy), ptr(mean), ptr(rstd), ptr(g),
+         ptr(dres), ptr(dx), ptr(dgamma), ptr(dbeta), int(accumulate), ptr(ws), rows, C, stream())
+
+
+def bias_residual(res, y, bias, out):
+    rows, C = y.shape
+    call("evo_bias_residual", ptr(res), dcode(res) if res is not None else F32, ptr(y), dcode(y),
+         ptr(bias), ptr(out), dcode(out), rows, C, stream())
+    return out
+
+
+def bias_relu_(y, bias):
+    rows, C = y.shape
+    call("evo_bias_relu", ptr(y), dcode(y), ptr(bias), rows, C, stream())
+
+
+def relu_bwd_colsum_(dh, h, db, accumulate=False):
+    rows, C = dh.shape
+    ws = _ws(_lib.load().evo_colsum_workspace(C), dh.device)
+    call("evo_relu_bwd_colsum", ptr(dh), ptr(h), dcode(dh), ptr(db), int(accumulate), ptr(ws),
+         rows, C, stream())
+
+
+def colsum_cast(x, out, y=None, accumulate=False):
+    rows, C = x.shape
+    ws = _ws(_lib.load().evo_colsum_workspace(C), x.device)
+    call("evo_colsum_cast", ptr(x), dcode(x), ptr(out), int(accumulate), ptr(y),
+         dcode(y) if y is not None else F32, ptr(ws), rows, C, stream())
+
+
+def cast(x, y):
+    call("evo_cast", ptr(x), dcode(x), ptr(y), dcode(y), x.numel(), stream())
+    return y
+
+
+# ---------------------------------------------------------------------------
+# attention core
+
+
+def attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl):
+    T = qkvg.shape[0]
+    dev, dt = qkvg.device, qkvg.dtype
+    ctx = torch.empty((T, H * D), dtype=dt, device=dev)
+    gate = torch.empty_like(ctx)
+    gated = torch.empty_like(ctx)
+    lse = torch.empty((B, H, L, 2), dtype=torch.float32, device=dev)
+    call("evo_attn_fwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(bias_t), ptr(bg),
+         ptr(ctx), ptr(gate), ptr(gated), ptr(lse), B, L, H, D, sb, sl, dcode(qkvg), stream())
+    return ctx, gate, gated, lse
+
+
+def attn_bwd(qkvg, mask, msb, msl, bias_t, ctx, gate, dgated, lse, dbg, B, L, H, D, sb, sl,
+             want_dbias: bool, accumulate=False):
+    dev, dt = qkvg.device, qkvg.dtype
+    dqkvg = torch.empty_like(qkvg)
+    dbias_t = torch.empty((H, L, L), dtype=torch.float32, device=dev) if want_dbias else None
+    nbytes = _lib.load().evo_attn_bwd_workspace(B, L, H, D, dcode(qkvg))
+    ws = _ws(nbytes, dev)
+    call("evo_attn_bwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(bias_t), ptr(ctx),
+         ptr(gate), ptr(dgated), ptr(lse), ptr(dqkvg), ptr(dbias_t), ptr(dbg), int(accumulate),
+         ptr(ws), ws.numel(), B, L, H, D, sb, sl, dcode(qkvg), stream())
+    return dqkvg, dbias_t
+
+
+# ---------------------------------------------------------------------------
+# pair bias
+
+
+def pair_bias_fwd(z, g, b, w, R, H, transposed):
+    C = z.shape[1]
+    dev = z.device
+    bias_t = torch.empty((H, R, R), dtype=torch.float32, device=dev)
+    mean = torch.empty(R * R, dtype=torch.float32, device=dev)
+    rstd = torch.empty(R * R, dtype=torch.float32, device=dev)
+    call("evo_pair_bias_fwd", ptr(z), dcode(z), ptr(g), ptr(b), ptr(w), ptr(bias_t), ptr(mean),
+         ptr(rstd), R, C, H, int(transposed), stream())
+    return bias_t, mean, rstd
+
+
+def pair_bias_bwd(z, mean, rstd, g, b, w, dbias_t, transposed, dz, dg, db, dw, R, H,
+                  accumulate=False):
+    C = z.shape[1]
+    ws = _ws(_lib.load().evo_pair_bias_bwd_workspace(C, H), z.device)
+    call("evo_pair_bias_bwd", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
+         ptr(dbias_t), int(transposed), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
+         ptr(ws), R, C, H, stream())
+
+
+# ---------------------------------------------------------------------------
+# outer product mean
+
+
+def opm_proj(ab, bl, br, mask_flat, k):
+    SR = ab.shape[0]
+    a = torch.empty((SR, k), dtype=ab.dtype, device=ab.device)
+    c = torch.empty_like(a)
+    call("evo_opm_proj", ptr(ab), ptr(bl), ptr(br), ptr(mask_flat), ptr(a), ptr(c), SR, k,
+         dcode(ab), stream())
+    return a, c
+
+
+def opm_proj_bwd(da, dc, mask_flat, dbl, dbr, k, accumulate=False):
+    SR = mask_flat.numel()
+    d_ab = torch.empty((SR, 2 * k), dtype=da.dtype, device=da.device)
+    ws = _ws(_lib.load().evo_colsum_workspace(2 * k), da.device)
+    call("evo_opm_proj_bwd", ptr(da), ptr(dc), ptr(mask_flat), ptr(d_ab), ptr(dbl), ptr(dbr),
+         int(accumulate), ptr(ws), SR, k, dcode(da), stream())
+    return d_ab
+
+
+def opm_norm_fwd(num, mask, S, R, k, out_dtype):
+    dev = num.device
+    rec = torch.empty(R * R, dtype=torch.float32, device=dev)
+    outn = torch.empty((R * R, k * k), dtype=out_dtype, device=dev)
+    call("evo_opm_norm_fwd", ptr(num), dcode(num), ptr(mask), ptr(rec), ptr(outn), dcode(outn),
+         S, R, k, stream())
+    return rec, outn
+
+
+def opm_norm_bwd(doutn, rec, R, k, out_dtype):
+    dnum = torch.empty((R * k, R * k), dtype=out_dtype, device=doutn.device)
+    call("evo_opm_norm_bwd", ptr(doutn), dcode(doutn), ptr(rec), ptr(dnum), dcode(dnum), R, k,
+         stream())
+    return dnum
+
+
+# ---------------------------------------------------------------------------
+# loss and optimizer
+
+
+def sq_loss(msa, pair, km, kz):
+    dev = msa.device
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    dmsa = torch.empty(msa.shape, dtype=torch.float32, device=dev)
+    dpair = torch.empty(pair.shape, dtype=torch.float32, device=dev)
+    ws = _ws(_lib.load().evo_sq_loss_workspace(), dev)
+    call("evo_sq_loss", ptr(msa), msa.numel(), ptr(pair), pair.numel(), dcode(msa), km, kz,
+         ptr(loss), ptr(dmsa), ptr(dpair), ptr(ws), stream())
+    return loss, dmsa, dpair
+
+
+def sumsq_f64(g, out):
+    ws = _ws(_lib.load().evo_sumsq_workspace(), g.device)
+    call("evo_sumsq_f64", ptr(g), g.numel(), ptr(out), ptr(ws), stream())
+
+
+def adam_clip_ema(p, g, m, v, ema, p_bf16, sumsq, clip, lr, b1, omb1, b2, omb2, eps, bc1, bc2,
+                  decay, omdecay):
+    call("evo_adam_clip_ema", ptr(p), ptr(g), ptr(m), ptr(v), ptr(ema), ptr(p_bf16), p.numel(),
+         ptr(sumsq), clip, lr, b1, omb1, b2, omb2, eps, bc1, bc2, decay, omdecay, stream())

@@ -1,0 +1,147 @@
+"""Training-step orchestration (src/trainer.py) on the GPU engine.
+
+One step: draw recycles (or pin them), build the step's synthetic features
+(src/trainer.py:98-101, src/model.py:274-288), copy them host->device, run
+forward + hand-written backward with gradients landing in the pooled grad
+region, then the fused optimizer tail (clip + Adam + EMA).  The whole
+device-side step can be captured into one CUDA graph (``capture()``): the
+feature buffers keep fixed device addresses and are refreshed in place.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import BlockEngine, DeviceFeatures
+from .errors import ContractError, TrainingAborted
+from .fusion import FusionEngine, OptimConfig
+from .model import (ModelConfig, draw_num_recycles, flatten_params, init_params,
+                    make_features, step_feature_seed)
+
+
+@dataclass
+class ExecutionPlan:
+    """src/trainer.py:37-79 (single-worker part; BP/DP in parallel.py)."""
+
+    dp: int = 1
+    bp: int = 1
+    dap: int = 1
+    fuse_ops: bool = True
+    fuse_tensors: bool = True
+    recompute: tuple = ()
+    act_dtype: str = "bf16"
+    chunk: int = 0
+    seed: int = 32
+    steps: int = 10
+    fixed_recycles: int = 0  # >0 pins n_recycles (throughput runs use 1)
+
+    def validate(self):
+        if self.dp < 1 or self.bp not in (1, 2) or self.dap != 1:
+            raise ContractError("supported grids: dp>=1, bp in {1,2}, dap=1")
+        if self.act_dtype not in ("f32", "bf16"):
+            raise ContractError(f"act_dtype must be f32 or bf16, got {self.act_dtype!r}")
+        if self.chunk < 0:
+            raise ContractError("chunk must be >= 0")
+
+    @property
+    def torch_dtype(self):
+        return torch.bfloat16 if self.act_dtype == "bf16" else torch.float32
+
+
+class PinnedFeatures:
+    """Host staging of one step's features in pinned memory."""
+
+    def __init__(self, cfg: ModelConfig):
+        S, R, F = cfg.n_seq, cfg.n_res, cfg.feat_dim
+        self.msa_feat = torch.empty((S * R, F), dtype=torch.float32).pin_memory()
+        self.pair_feat = torch.empty((R * R, F), dtype=torch.float32).pin_memory()
+        self.msa_mask = torch.empty((S * R,), dtype=torch.float32).pin_memory()
+        self.pair_mask = torch.empty((R * R,), dtype=torch.float32).pin_memory()
+
+    def fill(self, feats):
+        for k in ("msa_feat", "pair_feat", "msa_mask", "pair_mask"):
+            getattr(self, k).copy_(torch.from_numpy(
+                np.ascontiguousarray(getattr(feats, k), np.float32).reshape(getattr(self, k).shape)))
+
+    @property
+    def nbytes(self) -> int:
+        return sum(getattr(self, k).numel() * 4 for k in ("msa_feat", "pair_feat", "msa_mask", "pair_mask"))
+
+
+@dataclass
+class Trainer:
+    cfg: ModelConfig
+    plan: ExecutionPlan
+    store: FusionEngine
+    engine: BlockEngine
+    feats: DeviceFeatures
+    host: PinnedFeatures
+    history: list = field(default_factory=list)
+    graph: object = None
+    graph_loss: object = None
+
+    @classmethod
+    def create(cls, cfg: ModelConfig, plan: ExecutionPlan, optim: OptimConfig = None,
+               device="cuda", params: dict = None):
+        plan.validate()
+        cfg.validate()
+        params = params if params is not None else init_params(cfg, plan.seed)
+        named = [(n, params[n]) for n, _ in flatten_params(cfg)]
+        store = FusionEngine(named, optim or OptimConfig(), device=device,
+                             shadow_dtype=plan.torch_dtype)
+        engine = BlockEngine(cfg, store, plan.torch_dtype)
+        f0 = make_features(cfg, step_feature_seed(plan.seed, 0))
+        feats = DeviceFeatures(f0, device, cfg)
+        host = PinnedFeatures(cfg)
+        return cls(cfg, plan, store, engine, feats, host)
+
+    def n_recycles(self, step: int) -> int:
+        if self.plan.fixed_recycles:
+            return self.plan.fixed_recycles
+        return draw_num_recycles(self.plan.seed, step)
+
+    def stage_features(self, step: int, feats=None):
+        """Host-side feature generation for ``step`` into pinned memory."""
+        feats = feats or make_features(self.cfg, step_feature_seed(self.plan.seed, step))
+        self.host.fill(feats)
+
+    def device_step(self, n_cycles: int):
+        """H2D of the staged features, fwd+bwd, optimizer; returns the
+        device loss tensor (no host sync)."""
+        self.feats.copy_from_host(self.host)
+        loss, _ = self.engine.forward_backward(self.feats, n_cycles)
+        self.store.grad_sync(None)
+        self.store.step()
+        return loss
+
+    def capture(self, n_cycles: int = 1, warmup: int = 2):
+        """Capture ``device_step`` into a CUDA graph (after eager warm-up)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.device_step(n_cycles)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.graph_loss = self.device_step(n_cycles)
+        self.graph = g
+        return g
+
+    def train_step(self, step: int):
+        """src/trainer.py:192-247 (serial): returns (loss, metrics)."""
+        n_rec = self.n_recycles(step)
+        self.stage_features(step)
+        loss_t = self.device_step(n_rec)
+        loss = float(loss_t.item())
+        if not math.isfinite(loss):
+            raise TrainingAborted(step, f"non-finite loss {loss!r}")
+        grad_norm = float(np.sqrt(self.store.sumsq.item()))
+        metrics = {"step": step, "loss": loss, "grad_norm": grad_norm, "n_recycles": n_rec,
+                   "launches": dict(self.store.launches.counts)}
+        self.history.append(metrics)
+        return loss, metrics
