@@ -17,16 +17,13 @@
 //   bias : dnb[h] = sum over batches of ds (fixed batch order)
 #include "common.cuh"
 #include "reduce.cuh"
+#include "attn_geom.cuh"
 
 namespace evo {
 
 constexpr int SIMT_QT = 64;  // query rows (threads) per CTA
 constexpr int SIMT_KC = 32;  // keys per shared-memory chunk
 
-struct AttnGeom {
-  int64_t B, L, H, D, sb, sl, ld, msb, msl;
-  __host__ __device__ int64_t tok(int64_t b, int64_t l) const { return b * sb + l * sl; }
-};
 
 template <typename T, int DM>
 __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(

@@ -1,0 +1,167 @@
+"""Kernel-level numerics of the sm_100a library against plain PyTorch fp32
+references of the same op (floating-point kernels), for every attention
+geometry the Evoformer uses (MSA row / column, triangle start / end) and the
+ragged key counts the padding logic has to handle.
+
+Tolerances: fp32 SIMT path 1e-5 relative; bf16 tensor-core path 2e-2 relative
+on bf16-stored outputs (inputs are the same bf16 tensors; the differences
+are the bf16 rounding of P and of the outputs)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2207_05477_b200 import _lib
+    _lib.lib()
+
+
+def rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).abs().max() / max(a.abs().max(), b.abs().max(), 1e-30))
+
+
+def ref_attention(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl):
+    """fp32 torch reference in the reference's op order (src/attention.py:141-174)."""
+    HD = H * D
+    dev = qkvg.device
+    b = torch.arange(B, device=dev)[:, None]
+    l = torch.arange(L, device=dev)[None, :]
+    tok = (b * sb + l * sl)                     # [B, L]
+    x = qkvg.float()[tok]                      # [B, L, 4HD]
+    q = x[..., :HD].view(B, L, H, D).transpose(1, 2)
+    k = x[..., HD:2 * HD].view(B, L, H, D).transpose(1, 2)
+    v = x[..., 2 * HD:3 * HD].view(B, L, H, D).transpose(1, 2)
+    gp = x[..., 3 * HD:]
+    m = mask[(b * msb + l * msl)]               # [B, L]
+    logits = (q @ k.transpose(-1, -2)) * np.float32(1.0 / np.sqrt(D))
+    logits = logits + ((m - 1.0) * 1e9)[:, None, None, :]
+    if bias_t is not None:
+        logits = logits + bias_t.transpose(1, 2)[None]
+    w = torch.softmax(logits, dim=-1)
+    ctx = (w @ v).transpose(1, 2).reshape(B, L, HD)
+    gate = torch.sigmoid(gp + bg)
+    out_ctx = torch.empty(qkvg.shape[0], HD, device=dev)
+    out_gate = torch.empty_like(out_ctx)
+    out_ctx[tok.reshape(-1)] = ctx.reshape(-1, HD)
+    out_gate[tok.reshape(-1)] = gate.reshape(-1, HD)
+    return out_ctx, out_gate, w
+
+
+GEOMS = {
+    # name: (B, L, sb, sl, msb, msl, bias, bias_transposed_source)
+    "row": lambda S, R: (S, R, R, 1, R, 1),
+    "col": lambda S, R: (R, S, 1, R, 1, R),
+    "tri_start": lambda S, R: (R, R, R, 1, R, 1),
+    "tri_end": lambda S, R: (R, R, 1, R, 1, R),
+}
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("geom", list(GEOMS))
+@pytest.mark.parametrize("S,R,H,D", [(8, 32, 2, 16), (12, 40, 2, 32), (6, 64, 4, 16),
+                                     (16, 100, 2, 32), (4, 256, 8, 16), (4, 256, 8, 32),
+                                     (8, 200, 2, 16)])
+def test_attention_fwd_vs_torch(dtype, geom, S, R, H, D):
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(S * 1000 + R + H + D)
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    B, L, sb, sl, msb, msl = GEOMS[geom](S, R)
+    T = S * R if geom in ("row", "col") else R * R
+    HD = H * D
+    qkvg = (torch.randn(T, 4 * HD, device="cuda") * 0.7).to(dt)
+    mask = torch.ones(T, device="cuda")
+    n_valid = R - R // 10
+    mv = mask.view(S, R) if geom in ("row", "col") else mask.view(R, R)
+    mv[:, n_valid:] = 0.0
+    if geom in ("tri_start", "tri_end"):
+        mv[n_valid:, :] = 0.0
+    use_bias = geom != "col"
+    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3) if use_bias else None
+    bg = torch.randn(HD, device="cuda") * 0.1
+    ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
+    rc, rg, w = ref_attention(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
+    tol = 1e-5 if dtype == "f32" else 2e-2
+    assert rel(ctx.float(), rc) <= tol
+    assert rel(gate.float(), rg) <= tol
+    assert rel(gated.float(), rc * rg) <= tol * 2
+    # saved (row max, 1/row sum) reproduce the probabilities
+    assert torch.isfinite(lse).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("geom", list(GEOMS))
+@pytest.mark.parametrize("S,R,H,D", [(8, 32, 2, 16), (6, 64, 4, 16), (16, 100, 2, 32),
+                                     (4, 256, 8, 16), (4, 256, 8, 32)])
+def test_attention_bwd_vs_torch(dtype, geom, S, R, H, D):
+    """Backward of the core (dq, dk, dv, d gate pre-activation, dbias, dbg)
+    against torch autograd through the fp32 reference."""
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(7 * S + R + H * D)
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    B, L, sb, sl, msb, msl = GEOMS[geom](S, R)
+    T = S * R if geom in ("row", "col") else R * R
+    HD = H * D
+    qkvg = (torch.randn(T, 4 * HD, device="cuda") * 0.7).to(dt)
+    mask = torch.ones(T, device="cuda")
+    n_valid = R - R // 10
+    mv = mask.view(S, R) if geom in ("row", "col") else mask.view(R, R)
+    mv[:, n_valid:] = 0.0
+    if geom in ("tri_start", "tri_end"):
+        mv[n_valid:, :] = 0.0
+    use_bias = geom != "col"
+    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3) if use_bias else None
+    bg = torch.randn(HD, device="cuda") * 0.1
+    ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
+    dgated = (torch.randn(T, HD, device="cuda") * 0.5).to(dt)
+    dbg = torch.empty(HD, device="cuda")
+    dqkvg, dbias_t = ops.attn_bwd(qkvg, mask, msb, msl, bias_t, ctx, gate, dgated, lse, dbg,
+                                  B, L, H, D, sb, sl, want_dbias=use_bias)
+    # reference gradient
+    qr = qkvg.float().clone().requires_grad_(True)
+    br = bias_t.clone().requires_grad_(True) if use_bias else None
+    bgr = bg.clone().requires_grad_(True)
+    rc, rg, _ = ref_attention(qr, mask, msb, msl, br, bgr, B, L, H, D, sb, sl)
+    (rc * rg * dgated.float()).sum().backward()
+    tol = 1e-4 if dtype == "f32" else 3e-2
+    for s, name in enumerate(("dq", "dk", "dv", "dg")):
+        got = dqkvg[:, s * HD:(s + 1) * HD].float()
+        want = qr.grad[:, s * HD:(s + 1) * HD]
+        assert rel(got, want) <= tol, name
+    assert rel(dbg, bgr.grad) <= tol
+    if use_bias:
+        assert rel(dbias_t, br.grad) <= tol
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("C", [32, 64, 128, 256])
+def test_layernorm_fwd_bwd_vs_torch(dtype, C):
+    from paper_2207_05477_b200 import ops
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    torch.manual_seed(C)
+    x = (torch.randn(1000, C, device="cuda") * 2 + 0.5).to(dt)
+    g = torch.randn(C, device="cuda")
+    b = torch.randn(C, device="cuda")
+    y, mu, rs = ops.layernorm(x, g, b, dt)
+    xr = x.float().requires_grad_(True)
+    gr, brr = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (C,), gr, brr, 1e-5)
+    tol = 1e-5 if dtype == "f32" else 1e-2
+    assert rel(y.float(), yr) <= tol
+    dy = torch.randn(1000, C, device="cuda").to(dt)
+    dres = torch.randn(1000, C, device="cuda")
+    dx = dres.clone()
+    dg = torch.empty(C, device="cuda")
+    db = torch.empty(C, device="cuda")
+    ops.layernorm_bwd(x, dy, mu, rs, g, dx, dx, dg, db)
+    yr.backward(dy.float())
+    assert rel(dx - dres, xr.grad) <= 1e-4
+    assert rel(dg, gr.grad) <= 1e-4
+    assert rel(db, brr.grad) <= 1e-4
