@@ -207,7 +207,7 @@ def kernel_candidates(trainer):
     D = cz // H
     qkvg = (torch.randn(R * R, 4 * cz, device=dev) * 0.5).to(dt)
     mask = torch.ones(R * R, device=dev)
-    bias = torch.randn(H, R, R, device=dev) * 0.1
+    bias = (torch.randn(H, R, R, device=dev) * 0.1).to(dt)
     bg = torch.zeros(cz, device=dev)
     fl = R * H * 4 * R * R * D
     t = timeit(lambda: ops.attn_fwd(qkvg, mask, R, 1, bias, bg, R, R, H, D, R, 1))

@@ -103,40 +103,42 @@ int evo_scale_inplace(float* y, float s, int64_t n, void* stream);
  *   logits = (q.k^T)/sqrt(D) + (mask-1)*1e9 + nb,  w = softmax(logits),
  *   ctx = w.v,  gate = sigmoid(g + bg),  gated = ctx*gate
  * in the reference's accumulation order (:151-161).  mask is fp32 {0,1}
- * indexed b*mask_sb + l*mask_sl.  bias_t is nb transposed, [H, Lk, Lq]
- * (bias_t[h,j,i] = nb[h,i,j]); nullable.  lse: [B, H, L, 2] fp32 = (row max,
- * 1/row sum) of the logits -- kept apart because at a fully-masked row the
+ * indexed b*mask_sb + l*mask_sl.  nb: [H, L, L] (query, key) in the storage
+ * dtype -- bf16 in bf16 mode, as the reference rounds op outputs
+ * (src/tensor.py:102-108); nullable.  lse: [B, H, L, 2] fp32 = (row max of
+ * logits*log2(e), 1/row sum) -- kept apart because at a fully-masked row the
  * logits sit at -1e9 where m + log(sum) is not representable.
  * ctx/gate/gated: [tokens, H*D] storage dtype. */
 int evo_attn_fwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
-                 int64_t mask_sl, const float* bias_t, const float* bg,
+                 int64_t mask_sl, const void* nb, const float* bg,
                  void* ctx, void* gate, void* gated, float* lse,
                  int64_t B, int64_t L, int64_t H, int64_t D, int64_t tok_sb, int64_t tok_sl,
                  int dtype, void* stream);
 /* Backward closure (src/attention.py:178-221) from d(gated):
  * writes all four slots of dqkvg [tokens, 4*H*D] (dq, dk, dv, d(g pre-act)),
- * dbias_t [H, Lk, Lq] = sum over batches of dlogits (nullable when no bias),
- * dbg (+)= colsum of d(g pre-act). */
+ * dnb [H, L, L] fp32 = sum over batches of dlogits (:219-220; nullable when
+ * there is no bias), dbg (+)= colsum of d(g pre-act).  Deterministic. */
 int64_t evo_attn_bwd_workspace(int64_t B, int64_t L, int64_t H, int64_t D, int dtype);
 int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
-                 int64_t mask_sl, const float* bias_t, const void* ctx, const void* gate,
-                 const void* dgated, const float* lse, void* dqkvg, float* dbias_t,
+                 int64_t mask_sl, const void* nb, const void* ctx, const void* gate,
+                 const void* dgated, const float* lse, void* dqkvg, float* dnb,
                  float* dbg, int accumulate, void* ws, size_t ws_bytes,
                  int64_t B, int64_t L, int64_t H, int64_t D, int64_t tok_sb, int64_t tok_sl,
                  int dtype, void* stream);
 
 /* ---- pair bias (src/model.py:312-317) ------------------------------------
- * z: [R*R, C] pair tokens.  P[x,y,h] = LN(z[x,y]).w_bias[:,h]; written as
- * bias_t[h,x,y] (transposed_layout=0, triangle end) or bias_t[h,y,x]
- * (transposed_layout=1, MSA row / triangle start). */
+ * z: [R*R, C] pair tokens.  P[x,y,h] = LN(z[x,y]).w_bias[:,h]; written to
+ * nb (storage dtype) as nb[h,x,y] (swap_xy=0: MSA row / triangle start) or
+ * nb[h,y,x] (swap_xy=1: triangle end, whose rows are the pair's columns). */
 int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
-                      const float* w_bias, float* bias_t, float* mean, float* rstd,
-                      int64_t R, int64_t C, int64_t H, int transposed_layout, void* stream);
+                      const float* w_bias, void* nb, float* mean, float* rstd,
+                      int64_t R, int64_t C, int64_t H, int swap_xy, void* stream);
 int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H);
-/* dz += LN_bwd(dP . w_bias^T); dln_g, dln_b, dw_bias (+)= ... */
+/* dz += LN_bwd(dP . w_bias^T) with dP read from dnb (fp32, same swap_xy);
+ * dln_g, dln_b, dw_bias (+)= ... */
 int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
-                      const float* ln_g, const float* ln_b, const float* w_bias, const float* dbias_t,
-                      int transposed_layout, float* dz, float* dln_g, float* dln_b,
+                      const float* ln_g, const float* ln_b, const float* w_bias, const float* dnb,
+                      int swap_xy, float* dz, float* dln_g, float* dln_b,
                       float* dw_bias, int accumulate, void* ws,
                       int64_t R, int64_t C, int64_t H, void* stream);
 

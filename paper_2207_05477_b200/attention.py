@@ -75,7 +75,7 @@ class _GatedAttention(torch.autograd.Function):
         qkvg = torch.empty((T, 4 * HD), dtype=dt, device=x.device)
         ops.gemm(x2, wcat, qkvg)
         maskf = mask.reshape(b * s, r).to(torch.float32).contiguous()
-        bias_t = nb.transpose(1, 2).contiguous().float() if nb is not None else None
+        bias_t = nb.to(dt).contiguous() if nb is not None else None
         bgf = bg.reshape(-1).float().contiguous()
         c_, g_, gd, lse = ops.attn_fwd(qkvg, maskf, r, 1, bias_t, bgf, b * s, r, H, D, r, 1)
         wo2 = wo.reshape(HD, C).to(dt).contiguous()
@@ -112,7 +112,7 @@ class _GatedAttention(torch.autograd.Function):
         dx = torch.empty((T, C), dtype=torch.float32, device=dev)
         ops.gemm(dqkvg, wcat, dx, tb=True)
         dws = [dwcat[:, i * HD:(i + 1) * HD].reshape(C, H, D) for i in range(4)]
-        dnb = dbias_t.transpose(1, 2).contiguous() if ctx.has_bias else None
+        dnb = dbias_t if ctx.has_bias else None
         return (dx.view(b, s, r, C), None, dnb, *dws, dbg.view(H, D), dwo.view(H, D, C), dbo, None)
 
 

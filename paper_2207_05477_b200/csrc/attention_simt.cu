@@ -23,11 +23,12 @@ namespace evo {
 
 constexpr int SIMT_QT = 64;  // query rows (threads) per CTA
 constexpr int SIMT_KC = 32;  // keys per shared-memory chunk
+constexpr float LOG2E = 1.4426950408889634f;
 
 
 template <typename T, int DM>
 __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(
-    const T* __restrict__ qkvg, const float* __restrict__ mask, const float* __restrict__ bias_t,
+    const T* __restrict__ qkvg, const float* __restrict__ mask, const T* __restrict__ nb,
     const float* __restrict__ bg, T* __restrict__ ctx, T* __restrict__ gate, T* __restrict__ gated,
     float* __restrict__ lse, AttnGeom g, float scale) {
   __shared__ float Ks[SIMT_KC][DM];
@@ -70,9 +71,10 @@ __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(
         float d = 0.f;
 #pragma unroll
         for (int k = 0; k < DM; ++k) d = fmaf(q[k], Ks[jj][k], d);
-        float v = d * scale;
+        float v = __fmul_rn(d, scale);
         v = v + Mb[jj];
-        if (bias_t) v = v + bias_t[(h * g.L + j0 + jj) * g.L + i];
+        if (nb) v = v + to_f(nb[(h * g.L + i) * g.L + j0 + jj]);
+        v = __fmul_rn(v, LOG2E);  // softmax in the log2 domain (shared with the tcgen05 path)
         s[jj] = v;
         cmax = fmaxf(cmax, v);
       } else {
@@ -80,14 +82,14 @@ __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(
       }
     }
     const float mn = fmaxf(m, cmax);
-    const float alpha = expf(m - mn);  // m=-inf on the first chunk -> 0
+    const float alpha = exp2f(m - mn);  // m=-inf on the first chunk -> 0
     l *= alpha;
 #pragma unroll
     for (int k = 0; k < DM; ++k) acc[k] *= alpha;
 #pragma unroll
     for (int jj = 0; jj < SIMT_KC; ++jj) {
       if (jj < nk) {
-        float p = expf(s[jj] - mn);
+        float p = exp2f(s[jj] - mn);
         l += p;
 #pragma unroll
         for (int k = 0; k < DM; ++k) acc[k] = fmaf(p, Vs[jj][k], acc[k]);
@@ -144,7 +146,7 @@ __global__ void attn_bwd_prep_kernel(const T* __restrict__ ctx, const T* __restr
 // thread per query row: ds, dq; stash p and ds transposed [B,H,Lk,Lq]
 template <typename T, int DM>
 __global__ void __launch_bounds__(SIMT_QT) attn_bwd_rows_kernel(
-    const T* __restrict__ qkvg, const float* __restrict__ mask, const float* __restrict__ bias_t,
+    const T* __restrict__ qkvg, const float* __restrict__ mask, const T* __restrict__ nb,
     const float* __restrict__ lse, const float* __restrict__ dctx_ws, const float* __restrict__ Dvec,
     float* __restrict__ Pt, float* __restrict__ dSt, T* __restrict__ dqkvg, AttnGeom g, float scale) {
   __shared__ float Ks[SIMT_KC][DM];
@@ -192,10 +194,10 @@ __global__ void __launch_bounds__(SIMT_QT) attn_bwd_rows_kernel(
         d = fmaf(q[k], Ks[jj][k], d);
         dp = fmaf(dc[k], Vs[jj][k], dp);
       }
-      float s = d * scale;
+      float s = __fmul_rn(d, scale);
       s = s + Mb[jj];
-      if (bias_t) s = s + bias_t[(h * g.L + j0 + jj) * g.L + i];
-      float p = expf(s - ls) * rl;
+      if (nb) s = s + to_f(nb[(h * g.L + i) * g.L + j0 + jj]);
+      float p = exp2f(__fmul_rn(s, LOG2E) - ls) * rl;
       float ds = p * (dp - Dv);
       const int64_t o = (bh * g.L + j0 + jj) * g.L + i;
       Pt[o] = p;
@@ -263,15 +265,17 @@ __global__ void __launch_bounds__(SIMT_QT) attn_bwd_cols_kernel(
   }
 }
 
-// dbias_t[h, j, i] (+)= sum_b dSt[b, h, j, i]  (fixed batch order)
-__global__ void attn_bwd_bias_kernel(const float* __restrict__ dSt, float* __restrict__ dbias_t,
+// dnb[h, i, j] (+)= sum_b dSt[b, h, j, i]  (fixed batch order)
+__global__ void attn_bwd_bias_kernel(const float* __restrict__ dSt, float* __restrict__ dnb,
                                      int64_t B, int64_t H, int64_t L, int accumulate) {
   const int64_t n = H * L * L;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e % L, i = (e / L) % L, h = e / (L * L);
+    const int64_t src = (h * L + j) * L + i;
     float acc = 0.f;
-    for (int64_t b = 0; b < B; ++b) acc += dSt[b * n + e];
-    dbias_t[e] = accumulate ? dbias_t[e] + acc : acc;
+    for (int64_t b = 0; b < B; ++b) acc += dSt[b * n + src];
+    dnb[e] = accumulate ? dnb[e] + acc : acc;
   }
 }
 
@@ -296,12 +300,12 @@ __global__ void colsum_strided_kernel(const T* __restrict__ x, int64_t ld, int64
   } while (0)
 
 // tcgen05 path (attention_tc.cu); returns false when the shape is not covered.
-bool attn_fwd_tc_try(const void* qkvg, const float* mask, const float* bias_t, const float* bg,
+bool attn_fwd_tc_try(const void* qkvg, const float* mask, const void* nb, const float* bg,
                      void* ctx, void* gate, void* gated, float* lse, const AttnGeom& g, int dtype,
                      cudaStream_t s);
-bool attn_bwd_tc_try(const void* qkvg, const float* mask, const float* bias_t, const void* ctx,
+bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const void* ctx,
                      const void* gate, const void* dgated, const float* lse, void* dqkvg,
-                     float* dbias_t, float* dbg, int accumulate, void* ws, size_t ws_bytes,
+                     float* dnb, float* dbg, int accumulate, void* ws, size_t ws_bytes,
                      const AttnGeom& g, int dtype, cudaStream_t s);
 int64_t attn_bwd_tc_workspace(const AttnGeom& g, int dtype);
 
@@ -327,17 +331,17 @@ using namespace evo;
 extern "C" {
 
 int evo_attn_fwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
-                 int64_t mask_sl, const float* bias_t, const float* bg, void* ctx, void* gate,
+                 int64_t mask_sl, const void* nb, const float* bg, void* ctx, void* gate,
                  void* gated, float* lse, int64_t B, int64_t L, int64_t H, int64_t D,
                  int64_t tok_sb, int64_t tok_sl, int dtype, void* stream) {
   EVO_API_BEGIN
   AttnGeom g = make_geom(B, L, H, D, tok_sb, tok_sl, ld_qkvg, mask_sb, mask_sl);
   cudaStream_t s = (cudaStream_t)stream;
-  if (attn_fwd_tc_try(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
+  if (attn_fwd_tc_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
   const float scale = (float)(1.0 / sqrt((double)D));
   dim3 grid(cdiv(L, SIMT_QT), (unsigned)H, (unsigned)B);
   ATTN_DM_DISPATCH(D, DM, EVO_DISPATCH_T(dtype, T, {
-    attn_fwd_simt_kernel<T, DM><<<grid, SIMT_QT, 0, s>>>((const T*)qkvg, mask, bias_t, bg, (T*)ctx,
+    attn_fwd_simt_kernel<T, DM><<<grid, SIMT_QT, 0, s>>>((const T*)qkvg, mask, (const T*)nb, bg, (T*)ctx,
                                                          (T*)gate, (T*)gated, lse, g, scale);
   }));
   EVO_LAUNCH_CHECK();
@@ -353,14 +357,14 @@ int64_t evo_attn_bwd_workspace(int64_t B, int64_t L, int64_t H, int64_t D, int d
 }
 
 int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t mask_sb,
-                 int64_t mask_sl, const float* bias_t, const void* ctx, const void* gate,
-                 const void* dgated, const float* lse, void* dqkvg, float* dbias_t, float* dbg,
+                 int64_t mask_sl, const void* nb, const void* ctx, const void* gate,
+                 const void* dgated, const float* lse, void* dqkvg, float* dnb, float* dbg,
                  int accumulate, void* ws, size_t ws_bytes, int64_t B, int64_t L, int64_t H,
                  int64_t D, int64_t tok_sb, int64_t tok_sl, int dtype, void* stream) {
   EVO_API_BEGIN
   AttnGeom g = make_geom(B, L, H, D, tok_sb, tok_sl, ld_qkvg, mask_sb, mask_sl);
   cudaStream_t s = (cudaStream_t)stream;
-  if (attn_bwd_tc_try(qkvg, mask, bias_t, ctx, gate, dgated, lse, dqkvg, dbias_t, dbg, accumulate,
+  if (attn_bwd_tc_try(qkvg, mask, nb, ctx, gate, dgated, lse, dqkvg, dnb, dbg, accumulate,
                       ws, ws_bytes, g, dtype, s))
     return EVO_OK;
   EVO_REQUIRE((int64_t)ws_bytes >= simt_ws_bytes(g), EVO_ERR_ARG, "attn_bwd: workspace too small");
@@ -379,7 +383,7 @@ int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t m
         (const T*)ctx, (const T*)gate, (const T*)dgated, (T*)dqkvg, dctx_ws, Dvec, g);
     EVO_LAUNCH_CHECK();
     ATTN_DM_DISPATCH(D, DM, {
-      attn_bwd_rows_kernel<T, DM><<<grid, SIMT_QT, 0, s>>>((const T*)qkvg, mask, bias_t, lse,
+      attn_bwd_rows_kernel<T, DM><<<grid, SIMT_QT, 0, s>>>((const T*)qkvg, mask, (const T*)nb, lse,
                                                            dctx_ws, Dvec, Pt, dSt, (T*)dqkvg, g, scale);
       EVO_LAUNCH_CHECK();
       attn_bwd_cols_kernel<T, DM><<<grid, SIMT_QT, 0, s>>>((const T*)qkvg, dctx_ws, Pt, dSt,
@@ -392,8 +396,8 @@ int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t m
     EVO_LAUNCH_CHECK();
     finalize_partials(partials, pg, H * D, dbg, accumulate, s);
   });
-  if (dbias_t) {
-    attn_bwd_bias_kernel<<<cdiv(H * L * L, 256), 256, 0, s>>>(dSt, dbias_t, B, H, L, accumulate);
+  if (dnb) {
+    attn_bwd_bias_kernel<<<cdiv(H * L * L, 256), 256, 0, s>>>(dSt, dnb, B, H, L, accumulate);
     EVO_LAUNCH_CHECK();
   }
   count_launch(5);

@@ -1,22 +1,32 @@
 // Gated attention core on the 5th-generation tensor cores (tcgen05 + TMEM),
-// bf16 storage / fp32 accumulation (src/attention.py:118-174, fused op).
+// bf16 storage / fp32 accumulation (src/attention.py:118-233, fused op).
 //
-// One CTA per (query tile of 128 rows, head h, batch b); 8 warps.
+// Forward -- one CTA per (query tile of 128 rows, head h, batch b), 8 warps:
 //   1. Q [128 x D], K, V [Lp x D] staged into shared memory as UMMA core
-//      matrices with 16-byte cp.async (token-major qkvg rows, any
-//      (batch, position) strides -> the four Evoformer variants);
-//   2. S = Q K^T on the tensor core into TMEM (one elected thread issues
-//      D/16 tcgen05.mma of 128 x Lp x 16, completion via tcgen05.commit ->
-//      mbarrier);
+//      matrices with 16-byte cp.async straight from the token-major qkvg
+//      rows (any (batch, position) strides -> all four Evoformer variants);
+//   2. S = Q K^T on the tensor core into TMEM (one thread issues D/16
+//      tcgen05.mma 128 x Lp x 16; tcgen05.commit -> mbarrier);
 //   3. softmax from TMEM: the two warps sharing a TMEM lane quarter split the
-//      columns; pass 1 forms logits = S*c^-1/2 + (mask-1)*1e9 + nb in the
-//      reference's order and writes them back to TMEM, pass 2 exponentiates,
-//      sums and writes P (bf16) into shared memory as the A operand;
-//   4. O = P V on the tensor core, accumulated into TMEM columns aliasing S;
+//      key range; pass 1 forms logits = S*c^-1/2 + (mask-1)*1e9 + nb in the
+//      reference's order (src/attention.py:151-156), scales them by log2(e)
+//      and writes them back to TMEM; pass 2 exponentiates (ex2), sums and
+//      writes P (bf16) into shared memory as the next A operand;
+//   4. O = P V on the tensor core into TMEM columns aliasing S;
 //   5. epilogue: ctx = O / rowsum, gate = sigmoid(g + bg), gated = ctx*gate,
-//      and (row max, 1/rowsum) for the backward.
-// The whole key range (Lp <= 256) is resident, so the softmax is exact
-// two-pass rather than online.
+//      (row max, 1/rowsum) kept for the backward.
+//
+// Backward -- one CTA per (batch group, head, query tile), 16 warps, looping
+// over the batches of its group with double-buffered cp.async staging:
+//   per 64-key sub-chunk: S = Q K^T and dP = dO V^T on the tensor core,
+//   P = exp2(logits*log2e - m) / l and dS = P (dP - D) from TMEM, the bias
+//   gradient accumulated in TMEM across the whole batch group (deterministic,
+//   no atomics), P / dS written to shared memory;
+//   per 128-key chunk: dQ += dS K, dK = dS^T Q, dV = P^T dO on the tensor
+//   core (MN-major operand descriptors read the same shared tiles
+//   transposed), drained to HBM.
+// Query tile 1 (keys seen from queries 128..255) writes its dK/dV partial to
+// a workspace that a small combine kernel adds in (two addends, exact order).
 #include "common.cuh"
 #include "reduce.cuh"
 #include "attn_geom.cuh"
@@ -24,16 +34,53 @@
 
 namespace evo {
 
-
 namespace {
 
 using bf16 = __nv_bfloat16;
 constexpr float LOG2E = 1.4426950408889634f;
 
+__device__ __forceinline__ void st_zero16(void* p) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+__device__ __forceinline__ void bf16x8_to_f(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float2 t = __bfloat1622float2(h[k]);
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+
+// load N bias values nb_row[c0 .. c0+N) (bf16) as floats; zero beyond L
+template <int N>
+__device__ __forceinline__ void load_bias(const bf16* nb_row, int c0, int L, bool vec_ok, float* f) {
+  if (nb_row == nullptr) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) f[e] = 0.f;
+    return;
+  }
+  if (vec_ok && c0 + N <= L) {
+#pragma unroll
+    for (int k = 0; k < N / 8; ++k) {
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(nb_row + c0) + k);
+      bf16x8_to_f(u, f + 8 * k);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) f[e] = (c0 + e < L) ? __bfloat162float(nb_row[c0 + e]) : 0.f;
+  }
+}
+
 template <int LP>
 struct TmemCols {
   static constexpr int value = LP <= 32 ? 32 : (LP <= 64 ? 64 : (LP <= 128 ? 128 : 256));
 };
+
+// ============================================================================
+// forward
+// ============================================================================
 
 template <int D, int LP>
 struct FwdSmem {
@@ -48,13 +95,9 @@ struct FwdSmem {
   static constexpr int total = slot + 8;
 };
 
-__device__ __forceinline__ void st_zero16(void* p) {
-  *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
-}
-
 template <int D, int LP>
 __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
-    const bf16* __restrict__ qkvg, const float* __restrict__ mask, const float* __restrict__ bias_t,
+    const bf16* __restrict__ qkvg, const float* __restrict__ mask, const bf16* __restrict__ nb,
     const float* __restrict__ bg, bf16* __restrict__ ctx, bf16* __restrict__ gate,
     bf16* __restrict__ gated, float* __restrict__ lse, AttnGeom g, float scale) {
   using SM = FwdSmem<D, LP>;
@@ -79,7 +122,6 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   if (warp == 0) tc::tmem_alloc<TCOLS>(slot);
   if (tid == 32) tc::mbar_init(bar, 1);
 
-  // ---- stage Q, K, V (core-matrix layout) and the key mask bias ----
   for (int e = tid; e < 128 * DC; e += 256) {
     const int r = e / DC, c = e % DC;
     bf16* dst = sQ + ((r >> 3) * DC + c) * 64 + (r & 7) * 8;
@@ -120,8 +162,6 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     }
     tc::mma_commit(bar);
   }
-  tc::mbar_wait(bar, 0);
-  tc::fence_after();
 
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane;
@@ -130,24 +170,39 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
   constexpr int HALF = LP / 2;
   constexpr int NCH = HALF / 32;
-  const float* brow = (bias_t != nullptr && valid) ? bias_t + (size_t)h * L * L + i : nullptr;
+  const bf16* nbrow = (nb != nullptr && valid) ? nb + ((size_t)h * L + i) * L : nullptr;
+  const bool vec_ok = (L % 8) == 0;
 
-  // ---- pass 1: logits (reference order) + row max, logits back to TMEM ----
+  // prefetch the first bias chunk while the MMA runs
+  float bias_nx[32];
+  load_bias<32>(nbrow, half * HALF, L, vec_ok, bias_nx);
+  tc::mbar_wait(bar, 0);
+  tc::fence_after();
+
+  // ---- pass 1: logits (reference order), log2 domain, row max ----
   float mx = -INFINITY;
 #pragma unroll 1
   for (int ch = 0; ch < NCH; ++ch) {
     const int c0 = half * HALF + ch * 32;
-    float v[32];
+    float v[32], bias[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) bias[e] = bias_nx[e];
     tc::tmem_ld32(tl + c0, v);
+    if (ch + 1 < NCH) load_bias<32>(nbrow, c0 + 32, L, vec_ok, bias_nx);
     tc::wait_ld();
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      const int j = c0 + e;
-      float x = v[e] * scale;
-      x = x + sMb[j];
-      if (brow != nullptr && j < L) x = x + brow[(size_t)j * L];
-      v[e] = x;
-      mx = fmaxf(mx, x);
+    for (int e = 0; e < 32; e += 4) {
+      const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
+      const float mb[4] = {mb4.x, mb4.y, mb4.z, mb4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float x = __fmul_rn(v[e + u], scale);
+        x = x + mb[u];
+        x = x + bias[e + u];
+        x = __fmul_rn(x, LOG2E);
+        v[e + u] = x;
+        mx = fmaxf(mx, x);
+      }
     }
     tc::tmem_st32(tl + c0, v);
   }
@@ -156,7 +211,7 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   __syncthreads();
   const float m = fmaxf(sEx[row], sEx[128 + row]);
 
-  // ---- pass 2: P = exp(logits - m) -> bf16 A operand; row sums ----
+  // ---- pass 2: P = exp2(logits - m) -> bf16 A operand; row sums ----
   float sum = 0.f;
 #pragma unroll 1
   for (int ch = 0; ch < NCH; ++ch) {
@@ -167,8 +222,8 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     uint32_t pk[16];
 #pragma unroll
     for (int e = 0; e < 32; e += 2) {
-      const float p0 = tc::ex2((v[e] - m) * LOG2E);
-      const float p1 = tc::ex2((v[e + 1] - m) * LOG2E);
+      const float p0 = tc::ex2(v[e] - m);
+      const float p1 = tc::ex2(v[e + 1] - m);
       sum += p0 + p1;
       pk[e / 2] = tc::pack_bf16(p0, p1);
     }
@@ -240,6 +295,413 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   if (warp == 0) tc::tmem_dealloc<TCOLS>(tbase);
 }
 
+// ============================================================================
+// backward
+// ============================================================================
+
+template <int D, int LP>
+struct BwdSmem {
+  static constexpr int STAGE = 2 * 128 * D * 2 + 2 * LP * D * 2 + LP * 4;  // Q, dO, K, V, Mb
+  static constexpr int q = 0;                        // + stage offset
+  static constexpr int o = 128 * D * 2;
+  static constexpr int k = o + 128 * D * 2;
+  static constexpr int v = k + LP * D * 2;
+  static constexpr int mb = v + LP * D * 2;
+  static constexpr int p = 2 * STAGE;                // [128 x 128] bf16
+  static constexpr int ds = p + 128 * 128 * 2;
+  static constexpr int bar = ds + 128 * 128 * 2;
+  static constexpr int slot = bar + 16;
+  static constexpr int total = slot + 16;
+};
+
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]));
+}
+__device__ __forceinline__ void tmem_zero(uint32_t taddr) {
+  float z[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) z[e] = 0.f;
+  tmem_st16(taddr, z);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int D, int LP>
+__device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const bf16* dctx,
+                                          const float* mask, const AttnGeom& g, int64_t b,
+                                          int64_t h, int q0, int tid) {
+  using SM = BwdSmem<D, LP>;
+  constexpr int DC = D / 8;
+  const int L = (int)g.L;
+  const int64_t HD = g.H * D;
+  bf16* sQ = reinterpret_cast<bf16*>(st + SM::q);
+  bf16* sO = reinterpret_cast<bf16*>(st + SM::o);
+  bf16* sK = reinterpret_cast<bf16*>(st + SM::k);
+  bf16* sV = reinterpret_cast<bf16*>(st + SM::v);
+  float* sMb = reinterpret_cast<float*>(st + SM::mb);
+  for (int e = tid; e < 128 * DC; e += 512) {
+    const int r = e / DC, c = e % DC;
+    const int off = ((r >> 3) * DC + c) * 64 + (r & 7) * 8;
+    if (q0 + r < L) {
+      const int64_t t = g.tok(b, q0 + r);
+      tc::cp_async16(sQ + off, qkvg + t * g.ld + h * D + c * 8);
+      tc::cp_async16(sO + off, dctx + t * HD + h * D + c * 8);
+    } else {
+      st_zero16(sQ + off);
+      st_zero16(sO + off);
+    }
+  }
+  for (int e = tid; e < LP * DC; e += 512) {
+    const int j = e / DC, c = e % DC;
+    const int off = ((j >> 3) * DC + c) * 64 + (j & 7) * 8;
+    if (j < L) {
+      const bf16* src = qkvg + g.tok(b, j) * g.ld + HD + h * D + c * 8;
+      tc::cp_async16(sK + off, src);
+      tc::cp_async16(sV + off, src + HD);
+    } else {
+      st_zero16(sK + off);
+      st_zero16(sV + off);
+    }
+  }
+  for (int j = tid; j < LP; j += 512)
+    sMb[j] = j < L ? (mask[b * g.msb + (int64_t)j * g.msl] - 1.0f) * 1e9f : -INFINITY;
+}
+
+template <int D, int LP, bool BIAS>
+__global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
+    const bf16* __restrict__ qkvg, const bf16* __restrict__ dctx, const float* __restrict__ mask,
+    const bf16* __restrict__ nb, const float* __restrict__ lse, const float* __restrict__ Dvec,
+    bf16* __restrict__ dqkvg, bf16* __restrict__ kvpart, float* __restrict__ dnb_part,
+    AttnGeom g, float scale, int NG) {
+  using SM = BwdSmem<D, LP>;
+  constexpr int DC = D / 8;
+  constexpr int NKC = LP / 128;
+  constexpr uint32_t C_S = 0, C_DP = 64, C_DQ = 128, C_DK = 128 + D, C_DV = 128 + 2 * D, C_DB = 256;
+  extern __shared__ __align__(128) uint8_t smem[];
+  bf16* sP = reinterpret_cast<bf16*>(smem + SM::p);
+  bf16* sdS = reinterpret_cast<bf16*>(smem + SM::ds);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + SM::slot);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = blockIdx.x;
+  const int64_t h = blockIdx.y;
+  const int qt = blockIdx.z;
+  const int q0 = qt * 128;
+  const int L = (int)g.L;
+  const int64_t HD = g.H * D;
+  const int64_t b_lo = (g.B * grp) / NG, b_hi = (g.B * (grp + 1)) / NG;
+
+  const int quarter = warp & 3, cg = warp >> 2;  // TMEM lane quarter, column group
+  const int row = quarter * 32 + lane;
+  const int i = q0 + row;
+  const bool valid = i < L;
+  const bool vec_ok = (L % 8) == 0;
+  const bf16* nbrow = (BIAS && valid) ? nb + ((size_t)h * L + i) * L : nullptr;
+
+  if (warp == 0) tc::tmem_alloc<512>(slot);
+  if (tid == 32) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *slot;
+  const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
+  if (BIAS) {
+#pragma unroll
+    for (int c = 0; c < LP / 4; c += 16) tmem_zero(tl + C_DB + cg * (LP / 4) + c);
+  }
+  uint32_t ph0 = 0, ph1 = 0;
+
+  if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mask, g, b_lo, h, q0, tid);
+  cp_async_commit();
+
+  for (int64_t b = b_lo; b < b_hi; ++b) {
+    const int buf = (int)((b - b_lo) & 1);
+    uint8_t* st = smem + buf * SM::STAGE;
+    cp_async_wait0();
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (b + 1 < b_hi) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mask, g, b + 1, h, q0, tid);
+    cp_async_commit();
+    const bf16* sQ = reinterpret_cast<const bf16*>(st + SM::q);
+    const bf16* sO = reinterpret_cast<const bf16*>(st + SM::o);
+    const bf16* sK = reinterpret_cast<const bf16*>(st + SM::k);
+    const bf16* sV = reinterpret_cast<const bf16*>(st + SM::v);
+    const float* sMb = reinterpret_cast<const float*>(st + SM::mb);
+    const int64_t bh = b * g.H + h;
+    const float m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
+    const float rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
+    const float Dv = valid ? Dvec[bh * L + i] : 0.f;
+
+#pragma unroll 1
+    for (int kc = 0; kc < NKC; ++kc) {
+#pragma unroll 1
+      for (int sub = 0; sub < 2; ++sub) {
+        const int koff = kc * 128 + sub * 64;
+        if (tid == 0) {
+          const uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t aq = tc::sdesc(tc::smem_u32(sQ) + k * 256, 128, DC * 128);
+            const uint64_t ao = tc::sdesc(tc::smem_u32(sO) + k * 256, 128, DC * 128);
+            const uint64_t bk = tc::sdesc(tc::smem_u32(sK) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
+            const uint64_t bv = tc::sdesc(tc::smem_u32(sV) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
+            tc::mma_bf16_ss(tbase + C_S, aq, bk, idesc, k > 0 ? 1u : 0u);
+            tc::mma_bf16_ss(tbase + C_DP, ao, bv, idesc, k > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&bar[0]);
+        }
+        const int c0 = koff + cg * 16;  // this thread's 16 key columns
+        float bias[16];
+        load_bias<16>(nbrow, c0, L, vec_ok, bias);
+        tc::mbar_wait(&bar[0], ph0);
+        ph0 ^= 1;
+        tc::fence_after();
+        float s[16], dp[16], acc[16];
+        tc::tmem_ld16(tl + C_S + cg * 16, s);
+        tc::tmem_ld16(tl + C_DP + cg * 16, dp);
+        if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
+        tc::wait_ld();
+        uint32_t pp[8], pd[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
+          const float mb[4] = {mb4.x, mb4.y, mb4.z, mb4.w};
+          float pv[4], dv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float x = __fmul_rn(s[e + u], scale);
+            x = x + mb[u];
+            x = x + bias[e + u];
+            const float p = tc::ex2(__fmul_rn(x, LOG2E) - m2) * rl;
+            const float d = p * (dp[e + u] - Dv);
+            pv[u] = p;
+            dv[u] = d;
+            if (BIAS) acc[e + u] += d;
+          }
+          pp[e / 2] = tc::pack_bf16(pv[0], pv[1]);
+          pp[e / 2 + 1] = tc::pack_bf16(pv[2], pv[3]);
+          pd[e / 2] = tc::pack_bf16(dv[0], dv[1]);
+          pd[e / 2 + 1] = tc::pack_bf16(dv[2], dv[3]);
+        }
+        if (BIAS) tmem_st16(tl + C_DB + c0, acc);
+        // P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B
+        const int kcol = sub * 64 + cg * 16;
+#pragma unroll
+        for (int qd = 0; qd < 2; ++qd) {
+          const int off = ((row >> 3) * 16 + (kcol >> 3) + qd) * 64 + (row & 7) * 8;
+          *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
+          *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
+        }
+        if (BIAS) tc::wait_st();
+        tc::fence_proxy_async();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+      }
+      // ---- dQ += dS Kc ; dK = dS^T Q ; dV = P^T dO  (chunk of 128 keys) ----
+      if (tid == 0) {
+        const uint32_t id_q = tc::idesc_bf16(128, D, false, true);
+        const uint32_t id_kv = tc::idesc_bf16(128, D, true, true);
+        const uint32_t kbase = tc::smem_u32(sK) + (kc * 16) * DC * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t a = tc::sdesc(tc::smem_u32(sdS) + k * 256, 128, 16 * 128);
+          const uint64_t bb = tc::sdesc(kbase + k * 2 * DC * 128, DC * 128, 128);
+          tc::mma_bf16_ss(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t a_ds = tc::sdesc(tc::smem_u32(sdS) + k * 2 * 16 * 128, 16 * 128, 128);
+          const uint64_t a_p = tc::sdesc(tc::smem_u32(sP) + k * 2 * 16 * 128, 16 * 128, 128);
+          const uint64_t b_q = tc::sdesc(tc::smem_u32(sQ) + k * 2 * DC * 128, DC * 128, 128);
+          const uint64_t b_o = tc::sdesc(tc::smem_u32(sO) + k * 2 * DC * 128, DC * 128, 128);
+          tc::mma_bf16_ss(tbase + C_DK, a_ds, b_q, id_kv, k > 0 ? 1u : 0u);
+          tc::mma_bf16_ss(tbase + C_DV, a_p, b_o, id_kv, k > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&bar[1]);
+      }
+      tc::mbar_wait(&bar[1], ph1);
+      ph1 ^= 1;
+      tc::fence_after();
+      // drain dK / dV of this chunk: lanes = keys, cg -> (dK|dV, column half)
+      {
+        const int key = kc * 128 + row;
+        const int region = cg >> 1, chalf = cg & 1;
+        constexpr int DH = D / 2;
+        float vv[DH];
+        const uint32_t col = (region ? C_DV : C_DK) + chalf * DH;
+        if constexpr (DH == 16) tc::tmem_ld16(tl + col, vv);
+        else tc::tmem_ld8(tl + col, vv);
+        tc::wait_ld();
+        if (key < L) {
+          const float sc = region ? 1.0f : scale;
+          uint32_t pk[DH / 2];
+#pragma unroll
+          for (int e = 0; e < DH; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * sc, vv[e + 1] * sc);
+          const int64_t t = g.tok(b, key);
+          bf16* dst = (qt == 0) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
+                                : kvpart + t * 2 * HD + region * HD + h * D + chalf * DH;
+#pragma unroll
+          for (int k = 0; k < DH / 8; ++k)
+            reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        }
+      }
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+    }
+    // ---- drain dQ ----
+    {
+      constexpr int DQ = D / 4;
+      float vv[8];
+      if constexpr (DQ == 8) {
+        tc::tmem_ld8(tl + C_DQ + cg * DQ, vv);
+      } else {
+        float v4[4];
+        tmem_ld4(tl + C_DQ + cg * DQ, v4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) vv[e] = v4[e];
+      }
+      tc::wait_ld();
+      if (valid) {
+        const int64_t t = g.tok(b, i);
+        bf16* dst = dqkvg + t * g.ld + h * D + cg * DQ;
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < DQ; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * scale, vv[e + 1] * scale);
+        if constexpr (DQ == 8)
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        else
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pk[0], pk[1]);
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  // ---- bias-gradient partial of this batch group ----
+  if (BIAS) {
+    constexpr int PER = LP / 4;
+#pragma unroll 1
+    for (int c = 0; c < PER; c += 16) {
+      float vv[16];
+      tc::tmem_ld16(tl + C_DB + cg * PER + c, vv);
+      tc::wait_ld();
+      if (valid) {
+        float* dst = dnb_part + (((size_t)grp * g.H + h) * L + i) * L + cg * PER + c;
+        const int j0 = cg * PER + c;
+        if (vec_ok && j0 + 16 <= L) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            reinterpret_cast<float4*>(dst)[k] = make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (j0 + e < L) dst[e] = vv[e];
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+// thread per (b, h, l): dctx = dgated*gate (bf16), d(g) = dgated*ctx*gate*(1-gate), Dvec
+__global__ void attn_bwd_prep_tc_kernel(const bf16* __restrict__ ctx, const bf16* __restrict__ gate,
+                                        const bf16* __restrict__ dgated, bf16* __restrict__ dqkvg,
+                                        bf16* __restrict__ dctx, float* __restrict__ Dvec, AttnGeom g) {
+  const int64_t n = g.B * g.H * g.L;
+  const int64_t HD = g.H * g.D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = e % g.L, h = (e / g.L) % g.H, b = e / (g.L * g.H);
+    const int64_t t = g.tok(b, l);
+    float dsum = 0.f;
+    for (int k = 0; k < g.D; k += 8) {
+      const int64_t c = t * HD + h * g.D + k;
+      float dg[8], gv[8], cv[8];
+      bf16x8_to_f(*reinterpret_cast<const uint4*>(dgated + c), dg);
+      bf16x8_to_f(*reinterpret_cast<const uint4*>(gate + c), gv);
+      bf16x8_to_f(*reinterpret_cast<const uint4*>(ctx + c), cv);
+      uint32_t pc[4], pg[4];
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const float d0 = dg[u] * gv[u], d1 = dg[u + 1] * gv[u + 1];
+        const float g0 = dg[u] * cv[u] * gv[u] * (1.0f - gv[u]);
+        const float g1 = dg[u + 1] * cv[u + 1] * gv[u + 1] * (1.0f - gv[u + 1]);
+        // D uses the bf16-rounded dO the MMAs see
+        const __nv_bfloat162 dq = __floats2bfloat162_rn(d0, d1);
+        dsum += __bfloat162float(dq.x) * cv[u] + __bfloat162float(dq.y) * cv[u + 1];
+        pc[u / 2] = *reinterpret_cast<const uint32_t*>(&dq);
+        pg[u / 2] = tc::pack_bf16(g0, g1);
+      }
+      *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+      *reinterpret_cast<uint4*>(dqkvg + t * g.ld + 3 * HD + h * g.D + k) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+    }
+    Dvec[e] = dsum;
+  }
+}
+
+// dqkvg[:, HD:3HD] += kvpart   (query tile 1's dK/dV partial)
+__global__ void attn_kv_combine_kernel(bf16* __restrict__ dqkvg, const bf16* __restrict__ kvpart,
+                                       int64_t T, int64_t ld, int64_t HD) {
+  const int64_t per_row = 2 * HD / 8;
+  const int64_t n = T * per_row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / per_row, c = (e % per_row) * 8;
+    uint4* d = reinterpret_cast<uint4*>(dqkvg + t * ld + HD + c);
+    const uint4 p = *reinterpret_cast<const uint4*>(kvpart + t * 2 * HD + c);
+    float a[8], bq[8];
+    bf16x8_to_f(*d, a);
+    bf16x8_to_f(p, bq);
+    uint32_t o[4];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) o[u / 2] = tc::pack_bf16(a[u] + bq[u], a[u + 1] + bq[u + 1]);
+    *d = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// dnb[e] (+)= sum over batch groups of the partials (fixed group order)
+__global__ void attn_dnb_reduce_kernel(const float* __restrict__ part, float* __restrict__ dnb,
+                                       int64_t n, int NG, int accumulate) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int gi = 0; gi < NG; ++gi) acc += part[gi * n + e];
+    dnb[e] = accumulate ? dnb[e] + acc : acc;
+  }
+}
+
+template <typename T>
+__global__ void colsum_slice_kernel(const T* __restrict__ x, int64_t ld, int64_t off,
+                                    float* __restrict__ partials, int64_t rows, int64_t C) {
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) acc += to_f(x[r * ld + off + c]);
+    partials[blockIdx.x * C + c] = acc;
+  }
+}
+
 bool tc_disabled() {
   static int v = -1;
   if (v < 0) {
@@ -250,7 +712,7 @@ bool tc_disabled() {
 }
 
 template <int D, int LP>
-void launch_fwd(const void* qkvg, const float* mask, const float* bias_t, const float* bg, void* ctx,
+void launch_fwd(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
                 void* gate, void* gated, float* lse, const AttnGeom& g, cudaStream_t s) {
   using SM = FwdSmem<D, LP>;
   auto k = attn_fwd_tc_kernel<D, LP>;
@@ -261,25 +723,90 @@ void launch_fwd(const void* qkvg, const float* mask, const float* bias_t, const 
   }
   dim3 grid(cdiv(g.L, 128), (unsigned)g.H, (unsigned)g.B);
   const float scale = (float)(1.0 / sqrt((double)D));
-  k<<<grid, 256, SM::total, s>>>((const bf16*)qkvg, mask, bias_t, bg, (bf16*)ctx, (bf16*)gate,
-                                 (bf16*)gated, lse, g, scale);
+  k<<<grid, 256, SM::total, s>>>((const bf16*)qkvg, mask, (const bf16*)nb, bg, (bf16*)ctx,
+                                 (bf16*)gate, (bf16*)gated, lse, g, scale);
   EVO_LAUNCH_CHECK();
   count_launch(1);
 }
 
 template <int D>
-void launch_fwd_lp(const void* qkvg, const float* mask, const float* bias_t, const float* bg,
-                   void* ctx, void* gate, void* gated, float* lse, const AttnGeom& g, cudaStream_t s) {
+void launch_fwd_lp(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
+                   void* gate, void* gated, float* lse, const AttnGeom& g, cudaStream_t s) {
   const int64_t L = g.L;
-  if (L <= 64) launch_fwd<D, 64>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
-  else if (L <= 128) launch_fwd<D, 128>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
-  else if (L <= 192) launch_fwd<D, 192>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
-  else launch_fwd<D, 256>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
+  if (L <= 64) launch_fwd<D, 64>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
+  else if (L <= 128) launch_fwd<D, 128>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
+  else if (L <= 192) launch_fwd<D, 192>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
+  else launch_fwd<D, 256>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
+}
+
+struct BwdPlan {
+  int NQT, NG, LP;
+  int64_t off_dctx, off_dvec, off_kv, off_part, off_cols, total;
+};
+
+BwdPlan bwd_plan(const AttnGeom& g) {
+  BwdPlan p{};
+  p.LP = g.L <= 128 ? 128 : 256;
+  p.NQT = (int)((g.L + 127) / 128);
+  int per = (int)(g.H * p.NQT);
+  int ng = num_sms() / (per > 0 ? per : 1);
+  if (ng < 1) ng = 1;
+  if (ng > g.B) ng = (int)g.B;
+  p.NG = ng;
+  const int64_t T = g.B * g.L;  // tokens covered by the problem set
+  const int64_t HD = g.H * g.D;
+  auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+  p.off_dctx = 0;
+  p.off_dvec = p.off_dctx + al(T * HD * 2);
+  p.off_kv = p.off_dvec + al(g.B * g.H * g.L * 4);
+  p.off_part = p.off_kv + (p.NQT > 1 ? al(T * 2 * HD * 2) : 0);
+  p.off_cols = p.off_part + al((int64_t)p.NG * g.H * g.L * g.L * 4);
+  p.total = p.off_cols + al((int64_t)EVO_PARTIAL_BLOCKS * HD * 4);
+  return p;
+}
+
+bool bwd_supported(const AttnGeom& g, int dtype) {
+  if (tc_disabled() || dtype != EVO_BF16) return false;
+  if (!(g.D == 16 || g.D == 32) || g.L > 256 || g.L < 65) return false;
+  if ((g.ld % 8) != 0) return false;
+  return true;
+}
+
+template <int D, int LP, bool BIAS>
+void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const void* nb,
+                const float* lse, const float* Dvec, void* dqkvg, bf16* kvpart, float* part,
+                const AttnGeom& g, const BwdPlan& p, cudaStream_t s) {
+  using SM = BwdSmem<D, LP>;
+  auto k = attn_bwd_tc_kernel<D, LP, BIAS>;
+  static bool attr = false;
+  if (!attr) {
+    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::total));
+    attr = true;
+  }
+  dim3 grid((unsigned)p.NG, (unsigned)g.H, (unsigned)p.NQT);
+  const float scale = (float)(1.0 / sqrt((double)D));
+  k<<<grid, 512, SM::total, s>>>((const bf16*)qkvg, dctx, mask, (const bf16*)nb, lse, Dvec,
+                                 (bf16*)dqkvg, kvpart, part, g, scale, p.NG);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+}
+
+template <int D>
+void launch_bwd_d(bool bias, int LP, const void* qkvg, const bf16* dctx, const float* mask,
+                  const void* nb, const float* lse, const float* Dvec, void* dqkvg, bf16* kvpart,
+                  float* part, const AttnGeom& g, const BwdPlan& p, cudaStream_t s) {
+  if (LP == 128) {
+    if (bias) launch_bwd<D, 128, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    else launch_bwd<D, 128, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+  } else {
+    if (bias) launch_bwd<D, 256, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    else launch_bwd<D, 256, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+  }
 }
 
 }  // namespace
 
-bool attn_fwd_tc_try(const void* qkvg, const float* mask, const float* bias_t, const float* bg,
+bool attn_fwd_tc_try(const void* qkvg, const float* mask, const void* nb, const float* bg,
                      void* ctx, void* gate, void* gated, float* lse, const AttnGeom& g, int dtype,
                      cudaStream_t s) {
   if (tc_disabled() || dtype != EVO_BF16) return false;
@@ -287,17 +814,58 @@ bool attn_fwd_tc_try(const void* qkvg, const float* mask, const float* bias_t, c
   if ((g.ld % 8) != 0 || (((uintptr_t)qkvg) & 15) != 0) return false;
   if (((uintptr_t)ctx | (uintptr_t)gate | (uintptr_t)gated) & 15) return false;
   if (g.D == 16)
-    launch_fwd_lp<16>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
+    launch_fwd_lp<16>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
   else
-    launch_fwd_lp<32>(qkvg, mask, bias_t, bg, ctx, gate, gated, lse, g, s);
+    launch_fwd_lp<32>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
   return true;
 }
 
-bool attn_bwd_tc_try(const void*, const float*, const float*, const void*, const void*, const void*,
-                     const float*, void*, float*, float*, int, void*, size_t, const AttnGeom&, int,
-                     cudaStream_t) {
-  return false;
+int64_t attn_bwd_tc_workspace(const AttnGeom& g, int dtype) {
+  if (!bwd_supported(g, dtype)) return 0;
+  return bwd_plan(g).total;
 }
-int64_t attn_bwd_tc_workspace(const AttnGeom&, int) { return 0; }
+
+bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const void* ctx,
+                     const void* gate, const void* dgated, const float* lse, void* dqkvg,
+                     float* dnb, float* dbg, int accumulate, void* ws, size_t ws_bytes,
+                     const AttnGeom& g, int dtype, cudaStream_t s) {
+  if (!bwd_supported(g, dtype)) return false;
+  if (((uintptr_t)qkvg | (uintptr_t)dqkvg | (uintptr_t)ctx | (uintptr_t)gate | (uintptr_t)dgated) & 15)
+    return false;
+  const BwdPlan p = bwd_plan(g);
+  EVO_REQUIRE((int64_t)ws_bytes >= p.total, EVO_ERR_ARG, "attn_bwd: workspace too small");
+  uint8_t* w = (uint8_t*)ws;
+  bf16* dctx = (bf16*)(w + p.off_dctx);
+  float* Dvec = (float*)(w + p.off_dvec);
+  bf16* kvpart = (bf16*)(w + p.off_kv);
+  float* part = (float*)(w + p.off_part);
+  float* cols = (float*)(w + p.off_cols);
+  const int64_t nbhl = g.B * g.H * g.L;
+  attn_bwd_prep_tc_kernel<<<cdiv(nbhl, 256), 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
+                                                           (const bf16*)dgated, (bf16*)dqkvg, dctx,
+                                                           Dvec, g);
+  EVO_LAUNCH_CHECK();
+  const bool bias = nb != nullptr && dnb != nullptr;
+  if (g.D == 16)
+    launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+  else
+    launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+  const int64_t T = g.B * g.L, HD = g.H * g.D;
+  if (p.NQT > 1) {
+    attn_kv_combine_kernel<<<cdiv(T * 2 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, kvpart, T, g.ld, HD);
+    EVO_LAUNCH_CHECK();
+  }
+  if (bias) {
+    const int64_t n = g.H * g.L * g.L;
+    attn_dnb_reduce_kernel<<<cdiv(n, 256), 256, 0, s>>>(part, dnb, n, p.NG, accumulate);
+    EVO_LAUNCH_CHECK();
+  }
+  const unsigned pg = partial_grid(T);
+  colsum_slice_kernel<bf16><<<pg, 256, 0, s>>>((const bf16*)dqkvg, g.ld, 3 * HD, cols, T, HD);
+  EVO_LAUNCH_CHECK();
+  finalize_partials(cols, pg, HD, dbg, accumulate, s);
+  count_launch(3 + (p.NQT > 1) + bias);
+  return true;
+}
 
 }  // namespace evo

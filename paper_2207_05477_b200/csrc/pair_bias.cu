@@ -2,7 +2,7 @@
 //   nb[h, i, j] = LN(z)[i, j, :] . w_bias[:, h]
 // One warp per pair token: LayerNorm in registers, the H-wide projection as
 // warp reductions, written straight into the transposed bias layout the
-// attention kernels read (bias_t[h, key, query]).  Bandwidth-bound: reads
+// attention kernels read (nb[h, query, key], storage dtype).  Bandwidth-bound: reads
 // the pair once (R*R*C storage bytes), writes H*R*R fp32.
 //
 // Backward fuses dP -> dLN -> LayerNorm backward -> dz (+=) with the
@@ -18,8 +18,8 @@ constexpr int PB_HMAX = 16;
 template <typename T, int NPL>
 __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
-    const float* __restrict__ w, float* __restrict__ bias_t, float* __restrict__ mean,
-    float* __restrict__ rstd, int64_t R, int C, int H, int transposed) {
+    const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
+    float* __restrict__ rstd, int64_t R, int C, int H, int swap_xy) {
   const int lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x * (int64_t)PB_WARPS + (threadIdx.x >> 5);
   if (t >= R * R) return;
@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
     }
   }
   if (lane < H) {
-    int64_t o = transposed ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
-    bias_t[o] = mine;
+    int64_t o = swap_xy ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+    nb[o] = from_f<T>(mine);
   }
   if (lane == 0) {
     mean[t] = mu;
@@ -74,7 +74,7 @@ template <typename T, int NPL>
 __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
     const T* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
-    const float* __restrict__ dbias_t, int transposed, float* __restrict__ dz,
+    const float* __restrict__ dnb, int swap_xy, float* __restrict__ dz,
     float* __restrict__ partials, int64_t R, int C, int H) {
   extern __shared__ float sm[];  // [PB_WARPS][C*H + 2C]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
     const int64_t x = t / R, y = t % R;
     float dp = 0.f;
     if (lane < H) {
-      int64_t o = transposed ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
-      dp = dbias_t[o];
+      int64_t o = swap_xy ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+      dp = dnb[o];
     }
     float dP[PB_HMAX];
 #pragma unroll
@@ -166,8 +166,8 @@ using namespace evo;
 extern "C" {
 
 int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
-                      const float* w_bias, float* bias_t, float* mean, float* rstd, int64_t R,
-                      int64_t C, int64_t H, int transposed_layout, void* stream) {
+                      const float* w_bias, void* nb, float* mean, float* rstd, int64_t R,
+                      int64_t C, int64_t H, int swap_xy, void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
   if (R == 0) return EVO_OK;
@@ -175,7 +175,7 @@ int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* 
   unsigned grid = cdiv(R * R, PB_WARPS);
   PB_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(dtype, T, {
     pair_bias_fwd_kernel<T, NPL><<<grid, PB_WARPS * 32, 0, s>>>(
-        (const T*)z, ln_g, ln_b, w_bias, bias_t, mean, rstd, R, (int)C, (int)H, transposed_layout);
+        (const T*)z, ln_g, ln_b, w_bias, (T*)nb, mean, rstd, R, (int)C, (int)H, swap_xy);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);
@@ -188,7 +188,7 @@ int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H) {
 
 int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
                       const float* ln_g, const float* ln_b, const float* w_bias,
-                      const float* dbias_t, int transposed_layout, float* dz, float* dln_g,
+                      const float* dnb, int swap_xy, float* dz, float* dln_g,
                       float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t R,
                       int64_t C, int64_t H, void* stream) {
   EVO_API_BEGIN
@@ -205,8 +205,8 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
     auto k = pair_bias_bwd_kernel<T, NPL>;
     if (smem > 48 * 1024)
       EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, PB_WARPS * 32, smem, s>>>((const T*)z, mean, rstd, ln_g, ln_b, w_bias, dbias_t,
-                                         transposed_layout, dz, part, R, (int)C, (int)H);
+    k<<<grid, PB_WARPS * 32, smem, s>>>((const T*)z, mean, rstd, ln_g, ln_b, w_bias, dnb,
+                                         swap_xy, dz, part, R, (int)C, (int)H);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);

@@ -44,20 +44,20 @@ class Variant:
     msl: int
     mask: str          # "msa" or "pair"
     bias: bool         # pair-derived bias present
-    transposed: bool   # bias_t layout flag for evo_pair_bias_fwd
+    swap_xy: bool      # nb[h, i, j] = P[j, i, h] (triangle end) instead of P[i, j, h]
 
 
 def variants(cfg: ModelConfig) -> dict:
     S, R = cfg.n_seq, cfg.n_res
     return {
         # src/model.py:320-328: batch s, keys r, mask msa[s, r]
-        "row_attn": Variant("row_attn", S, R, R, 1, R, 1, "msa", True, True),
+        "row_attn": Variant("row_attn", S, R, R, 1, R, 1, "msa", True, False),
         # src/model.py:331-341: batch r, keys s, mask msa_t[r, s] = msa[s, r]
         "col_attn": Variant("col_attn", R, S, 1, R, 1, R, "msa", False, False),
         # src/model.py:381-398 (start): batch i, keys j, mask pair[i, j]
-        "tri_start": Variant("tri_start", R, R, R, 1, R, 1, "pair", True, True),
+        "tri_start": Variant("tri_start", R, R, R, 1, R, 1, "pair", True, False),
         # (end): batch j of pair^T, keys i: token (a, b) = pair row b*R + a
-        "tri_end": Variant("tri_end", R, R, 1, R, 1, R, "pair", True, False),
+        "tri_end": Variant("tri_end", R, R, 1, R, 1, R, "pair", True, True),
     }
 
 
@@ -124,7 +124,7 @@ class BlockEngine:
             z = pair if pair is not None else x
             nb, pmu, prs = ops.pair_bias_fwd(z, self.P(f"{prefix}.bias_ln_g"),
                                              self.P(f"{prefix}.bias_ln_b"),
-                                             self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.transposed)
+                                             self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.swap_xy)
         qkvg = torch.empty((T, 4 * HD), dtype=dt, device=x.device)
         for s, f in enumerate(("wq", "wk", "wv", "wg")):
             ops.gemm(xl, self.W(f"{prefix}.attn.{f}", C), qkvg[:, s * HD:(s + 1) * HD])
@@ -173,7 +173,7 @@ class BlockEngine:
             target = dpair if dpair is not None else d
             ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
                               self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
-                              v.transposed, target, self.G(f"{prefix}.bias_ln_g"),
+                              v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
                               self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
                               cfg.n_res, H)
 

@@ -108,52 +108,57 @@ def cast(x, y):
 # attention core
 
 
-def attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl):
+def attn_fwd(qkvg, mask, msb, msl, nb, bg, B, L, H, D, sb, sl):
+    """nb: [H, L, L] (query, key) in qkvg's dtype, or None."""
     T = qkvg.shape[0]
     dev, dt = qkvg.device, qkvg.dtype
+    if nb is not None and nb.dtype != dt:
+        raise TypeError("attention bias must be stored in the activation dtype")
     ctx = torch.empty((T, H * D), dtype=dt, device=dev)
     gate = torch.empty_like(ctx)
     gated = torch.empty_like(ctx)
     lse = torch.empty((B, H, L, 2), dtype=torch.float32, device=dev)
-    call("evo_attn_fwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(bias_t), ptr(bg),
+    call("evo_attn_fwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(nb), ptr(bg),
          ptr(ctx), ptr(gate), ptr(gated), ptr(lse), B, L, H, D, sb, sl, dcode(qkvg), stream())
     return ctx, gate, gated, lse
 
 
-def attn_bwd(qkvg, mask, msb, msl, bias_t, ctx, gate, dgated, lse, dbg, B, L, H, D, sb, sl,
+def attn_bwd(qkvg, mask, msb, msl, nb, ctx, gate, dgated, lse, dbg, B, L, H, D, sb, sl,
              want_dbias: bool, accumulate=False):
-    dev, dt = qkvg.device, qkvg.dtype
+    """Returns (dqkvg, dnb [H, L, L] fp32 or None)."""
+    dev = qkvg.device
     dqkvg = torch.empty_like(qkvg)
-    dbias_t = torch.empty((H, L, L), dtype=torch.float32, device=dev) if want_dbias else None
+    dnb = torch.empty((H, L, L), dtype=torch.float32, device=dev) if want_dbias else None
     nbytes = _lib.load().evo_attn_bwd_workspace(B, L, H, D, dcode(qkvg))
     ws = _ws(nbytes, dev)
-    call("evo_attn_bwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(bias_t), ptr(ctx),
-         ptr(gate), ptr(dgated), ptr(lse), ptr(dqkvg), ptr(dbias_t), ptr(dbg), int(accumulate),
+    call("evo_attn_bwd", ptr(qkvg), qkvg.stride(0), ptr(mask), msb, msl, ptr(nb), ptr(ctx),
+         ptr(gate), ptr(dgated), ptr(lse), ptr(dqkvg), ptr(dnb), ptr(dbg), int(accumulate),
          ptr(ws), ws.numel(), B, L, H, D, sb, sl, dcode(qkvg), stream())
-    return dqkvg, dbias_t
+    return dqkvg, dnb
 
 
 # ---------------------------------------------------------------------------
 # pair bias
 
 
-def pair_bias_fwd(z, g, b, w, R, H, transposed):
+def pair_bias_fwd(z, g, b, w, R, H, swap_xy):
+    """nb [H, R, R] (query, key) in z's dtype; swap_xy for triangle-end."""
     C = z.shape[1]
     dev = z.device
-    bias_t = torch.empty((H, R, R), dtype=torch.float32, device=dev)
+    nb = torch.empty((H, R, R), dtype=z.dtype, device=dev)
     mean = torch.empty(R * R, dtype=torch.float32, device=dev)
     rstd = torch.empty(R * R, dtype=torch.float32, device=dev)
-    call("evo_pair_bias_fwd", ptr(z), dcode(z), ptr(g), ptr(b), ptr(w), ptr(bias_t), ptr(mean),
-         ptr(rstd), R, C, H, int(transposed), stream())
-    return bias_t, mean, rstd
+    call("evo_pair_bias_fwd", ptr(z), dcode(z), ptr(g), ptr(b), ptr(w), ptr(nb), ptr(mean),
+         ptr(rstd), R, C, H, int(swap_xy), stream())
+    return nb, mean, rstd
 
 
-def pair_bias_bwd(z, mean, rstd, g, b, w, dbias_t, transposed, dz, dg, db, dw, R, H,
+def pair_bias_bwd(z, mean, rstd, g, b, w, dnb, swap_xy, dz, dg, db, dw, R, H,
                   accumulate=False):
     C = z.shape[1]
     ws = _ws(_lib.load().evo_pair_bias_bwd_workspace(C, H), z.device)
     call("evo_pair_bias_bwd", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
-         ptr(dbias_t), int(transposed), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
+         ptr(dnb), int(swap_xy), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
          ptr(ws), R, C, H, stream())
 
 

@@ -44,7 +44,7 @@ def ref_attention(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl):
     logits = (q @ k.transpose(-1, -2)) * np.float32(1.0 / np.sqrt(D))
     logits = logits + ((m - 1.0) * 1e9)[:, None, None, :]
     if bias_t is not None:
-        logits = logits + bias_t.transpose(1, 2)[None]
+        logits = logits + bias_t.float()[None]
     w = torch.softmax(logits, dim=-1)
     ctx = (w @ v).transpose(1, 2).reshape(B, L, HD)
     gate = torch.sigmoid(gp + bg)
@@ -84,7 +84,7 @@ def test_attention_fwd_vs_torch(dtype, geom, S, R, H, D):
     if geom in ("tri_start", "tri_end"):
         mv[n_valid:, :] = 0.0
     use_bias = geom != "col"
-    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3) if use_bias else None
+    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3).to(dt) if use_bias else None
     bg = torch.randn(HD, device="cuda") * 0.1
     ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
     rc, rg, w = ref_attention(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
@@ -117,7 +117,7 @@ def test_attention_bwd_vs_torch(dtype, geom, S, R, H, D):
     if geom in ("tri_start", "tri_end"):
         mv[n_valid:, :] = 0.0
     use_bias = geom != "col"
-    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3) if use_bias else None
+    bias_t = (torch.randn(H, L, L, device="cuda") * 0.3).to(dt) if use_bias else None
     bg = torch.randn(HD, device="cuda") * 0.1
     ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, msb, msl, bias_t, bg, B, L, H, D, sb, sl)
     dgated = (torch.randn(T, HD, device="cuda") * 0.5).to(dt)
@@ -126,7 +126,7 @@ def test_attention_bwd_vs_torch(dtype, geom, S, R, H, D):
                                   B, L, H, D, sb, sl, want_dbias=use_bias)
     # reference gradient
     qr = qkvg.float().clone().requires_grad_(True)
-    br = bias_t.clone().requires_grad_(True) if use_bias else None
+    br = bias_t.float().clone().requires_grad_(True) if use_bias else None
     bgr = bg.clone().requires_grad_(True)
     rc, rg, _ = ref_attention(qr, mask, msb, msl, br, bgr, B, L, H, D, sb, sl)
     (rc * rg * dgated.float()).sum().backward()
