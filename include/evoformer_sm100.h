@@ -79,6 +79,14 @@ int evo_layernorm_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype,
                       const float* mean, const float* rstd, const float* gamma,
                       const float* dres, float* dx, float* dgamma, float* dbeta,
                       int accumulate, void* ws, int64_t rows, int64_t C, void* stream);
+/* As evo_layernorm_bwd, also emitting a bf16 copy of dx (nullable) and the
+ * column sums of dx (nullable) -- the next module's output-bias gradient and
+ * GEMM operand come out of the same pass.  Power-of-two C in [32, 1024]. */
+int evo_layernorm_bwd_ex(const void* x, int x_dtype, const void* dy, int dy_dtype,
+                         const float* mean, const float* rstd, const float* gamma,
+                         const float* dres, float* dx, void* dx_bf16, float* dxsum,
+                         float* dgamma, float* dbeta, int accumulate, void* ws,
+                         int64_t rows, int64_t C, void* stream);
 
 /* ---- elementwise glue (src/tensor.py:244-331) ---------------------------- */
 /* out = res + y + bias (res nullable, bias nullable). */

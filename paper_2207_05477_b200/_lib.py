@@ -32,6 +32,8 @@ SIGNATURES = {
     "evo_layernorm_fwd": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i64, _i64, _f, _p]),
     "evo_layernorm_bwd_workspace": (_i64, [_i64, _i64]),
     "evo_layernorm_bwd": (_i, [_p, _i, _p, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i64, _i64, _p]),
+    "evo_layernorm_bwd_ex": (_i, [_p, _i, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i64,
+                                  _i64, _p]),
     "evo_bias_residual": (_i, [_p, _i, _p, _i, _p, _p, _i, _i64, _i64, _p]),
     "evo_bias_relu": (_i, [_p, _i, _p, _i64, _i64, _p]),
     "evo_relu_bwd_colsum": (_i, [_p, _p, _i, _p, _i, _p, _i64, _i64, _p]),

@@ -46,6 +46,14 @@ static cudaDataType_t cuda_dt(int d) {
   throw Error(EVO_ERR_ARG, "bad dtype code");
 }
 
+// vectorised glue (glue.cu); return false -> scalar kernels below
+int64_t colsum_vec_ws(int64_t C);
+bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, float* out,
+                int accumulate, void* ws, int64_t rows, int64_t C, int mode, cudaStream_t s);
+bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const float* bias, void* out,
+                       int odt, int64_t rows, int64_t C, cudaStream_t s);
+bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, cudaStream_t s);
+
 // tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
@@ -192,6 +200,7 @@ int evo_bias_residual(const void* res, int res_dtype, const void* y, int y_dtype
   int64_t n = rows * C;
   if (n == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (bias_residual_vec(res, res_dtype, y, y_dtype, bias, out, out_dtype, rows, C, s)) return EVO_OK;
   unsigned g = ew_grid(n);
   EVO_DISPATCH_T(res_dtype, TR, EVO_DISPATCH_T(y_dtype, TY, EVO_DISPATCH_T(out_dtype, TO, {
     bias_residual_kernel<TR, TY, TO><<<g, 256, 0, s>>>((const TR*)res, (const TY*)y, bias, (TO*)out, n, C);
@@ -205,6 +214,7 @@ int evo_bias_relu(void* y, int dtype, const float* bias, int64_t rows, int64_t C
   EVO_API_BEGIN
   int64_t n = rows * C;
   if (n == 0) return EVO_OK;
+  if (bias_relu_vec(y, dtype, bias, rows, C, (cudaStream_t)stream)) return EVO_OK;
   EVO_DISPATCH_T(dtype, T, {
     bias_relu_kernel<T><<<ew_grid(n), 256, 0, (cudaStream_t)stream>>>((T*)y, bias, n, C);
   });
@@ -213,12 +223,18 @@ int evo_bias_relu(void* y, int dtype, const float* bias, int64_t rows, int64_t C
   EVO_API_END
 }
 
-int64_t evo_colsum_workspace(int64_t C) { return (int64_t)EVO_PARTIAL_BLOCKS * C * 4; }
+int64_t evo_colsum_workspace(int64_t C) {
+  const int64_t a = (int64_t)EVO_PARTIAL_BLOCKS * C * 4, b = colsum_vec_ws(C);
+  return a > b ? a : b;
+}
 
 int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate, void* y, int y_dtype,
                     void* ws, int64_t rows, int64_t C, void* stream) {
   EVO_API_BEGIN
   cudaStream_t s = (cudaStream_t)stream;
+  if (colsum_vec(const_cast<void*>(x), x_dtype, C, nullptr, y, y_dtype, out, accumulate, ws, rows, C,
+                 0, s))
+    return EVO_OK;
   unsigned g = partial_grid(rows);
   int bs = C >= 256 ? 256 : (int)((C + 31) / 32 * 32);
   EVO_DISPATCH_T(x_dtype, TX, EVO_DISPATCH_T(y_dtype, TY, {
@@ -234,6 +250,7 @@ int evo_relu_bwd_colsum(void* dh, const void* h, int dtype, float* db, int accum
                         int64_t rows, int64_t C, void* stream) {
   EVO_API_BEGIN
   cudaStream_t s = (cudaStream_t)stream;
+  if (colsum_vec(dh, dtype, C, h, nullptr, dtype, db, accumulate, ws, rows, C, 1, s)) return EVO_OK;
   unsigned g = partial_grid(rows);
   int bs = C >= 256 ? 256 : (int)((C + 31) / 32 * 32);
   EVO_DISPATCH_T(dtype, T, {

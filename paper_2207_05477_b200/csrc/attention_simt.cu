@@ -139,7 +139,7 @@ __global__ void attn_bwd_prep_kernel(const T* __restrict__ ctx, const T* __restr
       dctx_ws[c] = dctx;
       dsum += dctx * cv;
     }
-    Dvec[e] = dsum;
+    Dvec[t * g.H + h] = dsum;
   }
 }
 
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(SIMT_QT) attn_bwd_rows_kernel(
   const int64_t bh = b * g.H + h;
   const float ls = active ? lse[2 * (bh * g.L + i)] : 0.f;
   const float rl = active ? lse[2 * (bh * g.L + i) + 1] : 0.f;
-  const float Dv = active ? Dvec[bh * g.L + i] : 0.f;
+  const float Dv = active ? Dvec[ti * g.H + h] : 0.f;
   for (int64_t j0 = 0; j0 < g.L; j0 += SIMT_KC) {
     const int nk = (int)imin64((int64_t)SIMT_KC, g.L - j0);
     __syncthreads();

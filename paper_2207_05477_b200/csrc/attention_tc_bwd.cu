@@ -1,23 +1,11 @@
-// Gated attention core on the 5th-generation tensor cores (tcgen05 + TMEM),
-// bf16 storage / fp32 accumulation (src/attention.py:118-233, fused op).
+// Gated attention core backward on the 5th-generation tensor cores (tcgen05 +
+// TMEM), bf16 storage / fp32 accumulation -- the closure of
+// src/attention.py:178-221.  Forward: attention_tc_fwd.cu.
 //
-// Forward -- one CTA per (query tile of 128 rows, head h, batch b), 8 warps:
-//   1. Q [128 x D], K, V [Lp x D] staged into shared memory as UMMA core
-//      matrices with 16-byte cp.async straight from the token-major qkvg
-//      rows (any (batch, position) strides -> all four Evoformer variants);
-//   2. S = Q K^T on the tensor core into TMEM (one thread issues D/16
-//      tcgen05.mma 128 x Lp x 16; tcgen05.commit -> mbarrier);
-//   3. softmax from TMEM: the two warps sharing a TMEM lane quarter split the
-//      key range; pass 1 forms logits = S*c^-1/2 + (mask-1)*1e9 + nb in the
-//      reference's order (src/attention.py:151-156), scales them by log2(e)
-//      and writes them back to TMEM; pass 2 exponentiates (ex2), sums and
-//      writes P (bf16) into shared memory as the next A operand;
-//   4. O = P V on the tensor core into TMEM columns aliasing S;
-//   5. epilogue: ctx = O / rowsum, gate = sigmoid(g + bg), gated = ctx*gate,
-//      (row max, 1/rowsum) kept for the backward.
-//
-// Backward -- one CTA per (batch group, head, query tile), 16 warps, looping
-// over the batches of its group with double-buffered cp.async staging:
+// One CTA per (batch group, head, query tile), 16 warps, looping over the
+// batches of its group with double-buffered cp.async staging; the pair-bias
+// tile of the CTA's query rows is the same for every batch, so it is staged
+// into shared memory once:
 //   per 64-key sub-chunk: S = Q K^T and dP = dO V^T on the tensor core,
 //   P = exp2(logits*log2e - m) / l and dS = P (dP - D) from TMEM, the bias
 //   gradient accumulated in TMEM across the whole batch group (deterministic,
@@ -33,6 +21,9 @@
 #include "tc_common.cuh"
 
 namespace evo {
+
+bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, float* out,
+                int accumulate, void* ws, int64_t rows, int64_t C, int mode, cudaStream_t s);
 
 namespace {
 
@@ -79,222 +70,6 @@ struct TmemCols {
 };
 
 // ============================================================================
-// forward
-// ============================================================================
-
-template <int D, int LP>
-struct FwdSmem {
-  static constexpr int q = 0;
-  static constexpr int k = q + 128 * D * 2;
-  static constexpr int v = k + LP * D * 2;
-  static constexpr int p = v + LP * D * 2;
-  static constexpr int mb = p + 128 * LP * 2;
-  static constexpr int ex = mb + LP * 4;
-  static constexpr int bar = ex + 512 * 4;
-  static constexpr int slot = bar + 8;
-  static constexpr int total = slot + 8;
-};
-
-template <int D, int LP>
-__global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
-    const bf16* __restrict__ qkvg, const float* __restrict__ mask, const bf16* __restrict__ nb,
-    const float* __restrict__ bg, bf16* __restrict__ ctx, bf16* __restrict__ gate,
-    bf16* __restrict__ gated, float* __restrict__ lse, AttnGeom g, float scale) {
-  using SM = FwdSmem<D, LP>;
-  constexpr int TCOLS = TmemCols<(LP > D ? LP : D)>::value;
-  constexpr int DC = D / 8;  // 16-byte chunks per row
-  extern __shared__ __align__(128) uint8_t smem[];
-  bf16* sQ = reinterpret_cast<bf16*>(smem + SM::q);
-  bf16* sK = reinterpret_cast<bf16*>(smem + SM::k);
-  bf16* sV = reinterpret_cast<bf16*>(smem + SM::v);
-  bf16* sP = reinterpret_cast<bf16*>(smem + SM::p);
-  float* sMb = reinterpret_cast<float*>(smem + SM::mb);
-  float* sEx = reinterpret_cast<float*>(smem + SM::ex);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + SM::slot);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t b = blockIdx.z, h = blockIdx.y;
-  const int q0 = blockIdx.x * 128;
-  const int L = (int)g.L;
-  const int64_t HD = g.H * D;
-
-  if (warp == 0) tc::tmem_alloc<TCOLS>(slot);
-  if (tid == 32) tc::mbar_init(bar, 1);
-
-  for (int e = tid; e < 128 * DC; e += 256) {
-    const int r = e / DC, c = e % DC;
-    bf16* dst = sQ + ((r >> 3) * DC + c) * 64 + (r & 7) * 8;
-    if (q0 + r < L)
-      tc::cp_async16(dst, qkvg + g.tok(b, q0 + r) * g.ld + h * D + c * 8);
-    else
-      st_zero16(dst);
-  }
-  for (int e = tid; e < LP * DC; e += 256) {
-    const int j = e / DC, c = e % DC;
-    const int off = ((j >> 3) * DC + c) * 64 + (j & 7) * 8;
-    if (j < L) {
-      const bf16* src = qkvg + g.tok(b, j) * g.ld + HD + h * D + c * 8;
-      tc::cp_async16(sK + off, src);
-      tc::cp_async16(sV + off, src + HD);
-    } else {
-      st_zero16(sK + off);
-      st_zero16(sV + off);
-    }
-  }
-  for (int j = tid; j < LP; j += 256)
-    sMb[j] = j < L ? (mask[b * g.msb + (int64_t)j * g.msl] - 1.0f) * 1e9f : -INFINITY;
-  tc::cp_async_wait_all();
-  tc::fence_proxy_async();
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tbase = *slot;
-
-  // ---- S = Q K^T  (M=128, N=LP, K=D) ----
-  if (tid == 0) {
-    const uint32_t idesc = tc::idesc_bf16(128, LP, false, false);
-#pragma unroll
-    for (int k = 0; k < D / 16; ++k) {
-      const uint64_t ad = tc::sdesc(tc::smem_u32(sQ) + k * 256, 128, DC * 128);
-      const uint64_t bd = tc::sdesc(tc::smem_u32(sK) + k * 256, 128, DC * 128);
-      tc::mma_bf16_ss(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
-    }
-    tc::mma_commit(bar);
-  }
-
-  const int quarter = warp & 3, half = warp >> 2;
-  const int row = quarter * 32 + lane;
-  const int i = q0 + row;
-  const bool valid = i < L;
-  const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
-  constexpr int HALF = LP / 2;
-  constexpr int NCH = HALF / 32;
-  const bf16* nbrow = (nb != nullptr && valid) ? nb + ((size_t)h * L + i) * L : nullptr;
-  const bool vec_ok = (L % 8) == 0;
-
-  // prefetch the first bias chunk while the MMA runs
-  float bias_nx[32];
-  load_bias<32>(nbrow, half * HALF, L, vec_ok, bias_nx);
-  tc::mbar_wait(bar, 0);
-  tc::fence_after();
-
-  // ---- pass 1: logits (reference order), log2 domain, row max ----
-  float mx = -INFINITY;
-#pragma unroll 1
-  for (int ch = 0; ch < NCH; ++ch) {
-    const int c0 = half * HALF + ch * 32;
-    float v[32], bias[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) bias[e] = bias_nx[e];
-    tc::tmem_ld32(tl + c0, v);
-    if (ch + 1 < NCH) load_bias<32>(nbrow, c0 + 32, L, vec_ok, bias_nx);
-    tc::wait_ld();
-#pragma unroll
-    for (int e = 0; e < 32; e += 4) {
-      const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
-      const float mb[4] = {mb4.x, mb4.y, mb4.z, mb4.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float x = __fmul_rn(v[e + u], scale);
-        x = x + mb[u];
-        x = x + bias[e + u];
-        x = __fmul_rn(x, LOG2E);
-        v[e + u] = x;
-        mx = fmaxf(mx, x);
-      }
-    }
-    tc::tmem_st32(tl + c0, v);
-  }
-  tc::wait_st();
-  sEx[half * 128 + row] = mx;
-  __syncthreads();
-  const float m = fmaxf(sEx[row], sEx[128 + row]);
-
-  // ---- pass 2: P = exp2(logits - m) -> bf16 A operand; row sums ----
-  float sum = 0.f;
-#pragma unroll 1
-  for (int ch = 0; ch < NCH; ++ch) {
-    const int c0 = half * HALF + ch * 32;
-    float v[32];
-    tc::tmem_ld32(tl + c0, v);
-    tc::wait_ld();
-    uint32_t pk[16];
-#pragma unroll
-    for (int e = 0; e < 32; e += 2) {
-      const float p0 = tc::ex2(v[e] - m);
-      const float p1 = tc::ex2(v[e + 1] - m);
-      sum += p0 + p1;
-      pk[e / 2] = tc::pack_bf16(p0, p1);
-    }
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-      bf16* dst = sP + ((row >> 3) * (LP / 8) + (c0 >> 3) + qd) * 64 + (row & 7) * 8;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * qd], pk[4 * qd + 1], pk[4 * qd + 2], pk[4 * qd + 3]);
-    }
-  }
-  sEx[256 + half * 128 + row] = sum;
-  tc::fence_proxy_async();
-  tc::fence_before();
-  __syncthreads();
-
-  // ---- O = P V  (M=128, N=D, K=LP), accumulated over S's first D columns ----
-  if (tid == 0) {
-    tc::fence_after();
-    const uint32_t idesc = tc::idesc_bf16(128, D, false, true);
-#pragma unroll 4
-    for (int k = 0; k < LP / 16; ++k) {
-      const uint64_t ad = tc::sdesc(tc::smem_u32(sP) + k * 256, 128, (LP / 8) * 128);
-      const uint64_t bd = tc::sdesc(tc::smem_u32(sV) + k * 2 * DC * 128, DC * 128, 128);
-      tc::mma_bf16_ss(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
-    }
-    tc::mma_commit(bar);
-  }
-  tc::mbar_wait(bar, 1);
-  tc::fence_after();
-
-  // ---- epilogue: normalise, gate, store ----
-  const float l = sEx[256 + row] + sEx[384 + row];
-  const float invl = 1.0f / l;
-  constexpr int DH = D / 2;
-  float o[DH];
-  if constexpr (DH == 16) {
-    tc::tmem_ld16(tl + half * DH, o);
-  } else {
-    tc::tmem_ld8(tl + half * DH, o);
-  }
-  tc::wait_ld();
-  if (valid) {
-    const int64_t t = g.tok(b, i);
-    const int64_t c0 = h * D + half * DH;
-    const bf16* gp = qkvg + t * g.ld + 3 * HD + c0;
-    uint32_t pc[DH / 2], pg[DH / 2], pgd[DH / 2];
-#pragma unroll
-    for (int k = 0; k < DH; k += 2) {
-      const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(gp + k);
-      const float c0f = o[k] * invl, c1f = o[k + 1] * invl;
-      const float g0 = 1.0f / (1.0f + __expf(-(__bfloat162float(g2.x) + bg[c0 + k])));
-      const float g1 = 1.0f / (1.0f + __expf(-(__bfloat162float(g2.y) + bg[c0 + k + 1])));
-      pc[k / 2] = tc::pack_bf16(c0f, c1f);
-      pg[k / 2] = tc::pack_bf16(g0, g1);
-      pgd[k / 2] = tc::pack_bf16(c0f * g0, c1f * g1);
-    }
-#pragma unroll
-    for (int k = 0; k < DH / 8; ++k) {
-      reinterpret_cast<uint4*>(ctx + t * HD + c0)[k] = make_uint4(pc[4 * k], pc[4 * k + 1], pc[4 * k + 2], pc[4 * k + 3]);
-      reinterpret_cast<uint4*>(gate + t * HD + c0)[k] = make_uint4(pg[4 * k], pg[4 * k + 1], pg[4 * k + 2], pg[4 * k + 3]);
-      reinterpret_cast<uint4*>(gated + t * HD + c0)[k] = make_uint4(pgd[4 * k], pgd[4 * k + 1], pgd[4 * k + 2], pgd[4 * k + 3]);
-    }
-    if (half == 0) {
-      lse[2 * ((b * g.H + h) * L + i)] = m;
-      lse[2 * ((b * g.H + h) * L + i) + 1] = invl;
-    }
-  }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<TCOLS>(tbase);
-}
-
 // ============================================================================
 // backward
 // ============================================================================
@@ -307,12 +82,36 @@ struct BwdSmem {
   static constexpr int k = o + 128 * D * 2;
   static constexpr int v = k + LP * D * 2;
   static constexpr int mb = v + LP * D * 2;
-  static constexpr int p = 2 * STAGE;                // [128 x 128] bf16
+  static constexpr int NS = (D == 32 && LP == 256) ? 1 : 2;  // staging buffers (smem budget)
+  static constexpr int p = NS * STAGE;               // [128 x 128] bf16
   static constexpr int ds = p + 128 * 128 * 2;
   static constexpr int bar = ds + 128 * 128 * 2;
   static constexpr int slot = bar + 16;
-  static constexpr int total = slot + 16;
+  static constexpr int BROW = LP + 8;                // padded bias row (bank spread)
+  static constexpr int bias = slot + 112;            // [128 x BROW] bf16, staged once
+  static constexpr int total = bias + 128 * BROW * 2;
 };
+
+// the CTA's bias rows nb[h, q0 + r, :] -> smem [128][LP + 8] (zero padded)
+template <int LP>
+__device__ __forceinline__ void stage_bias_tile(bf16* sB, const bf16* nb, int64_t h, int q0, int L,
+                                                int tid, int nthreads) {
+  constexpr int BROW = LP + 8;
+  constexpr int CPR = LP / 8;
+  const bool vec_ok = (L % 8) == 0;
+  for (int e = tid; e < 128 * CPR; e += nthreads) {
+    const int r = e / CPR, c = e % CPR;
+    bf16* dst = sB + r * BROW + c * 8;
+    const int q = q0 + r;
+    if (q < L && vec_ok && c * 8 + 8 <= L) {
+      tc::cp_async16(dst, nb + ((size_t)h * L + q) * L + c * 8);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        dst[u] = (q < L && c * 8 + u < L) ? nb[((size_t)h * L + q) * L + c * 8 + u] : __float2bfloat16(0.f);
+    }
+  }
+}
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
@@ -408,8 +207,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
   const int row = quarter * 32 + lane;
   const int i = q0 + row;
   const bool valid = i < L;
-  const bool vec_ok = (L % 8) == 0;
-  const bf16* nbrow = (BIAS && valid) ? nb + ((size_t)h * L + i) * L : nullptr;
+  const bf16* sBrow = reinterpret_cast<const bf16*>(smem + SM::bias) + row * SM::BROW;
 
   if (warp == 0) tc::tmem_alloc<512>(slot);
   if (tid == 32) {
@@ -427,18 +225,20 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
   }
   uint32_t ph0 = 0, ph1 = 0;
 
+  if (BIAS) stage_bias_tile<LP>(reinterpret_cast<bf16*>(smem + SM::bias), nb, h, q0, L, tid, 512);
   if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mask, g, b_lo, h, q0, tid);
   cp_async_commit();
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
-    const int buf = (int)((b - b_lo) & 1);
+    const int buf = SM::NS == 2 ? (int)((b - b_lo) & 1) : 0;
     uint8_t* st = smem + buf * SM::STAGE;
     cp_async_wait0();
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (b + 1 < b_hi) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mask, g, b + 1, h, q0, tid);
+    if (SM::NS == 2 && b + 1 < b_hi)
+      bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mask, g, b + 1, h, q0, tid);
     cp_async_commit();
     const bf16* sQ = reinterpret_cast<const bf16*>(st + SM::q);
     const bf16* sO = reinterpret_cast<const bf16*>(st + SM::o);
@@ -448,7 +248,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
     const int64_t bh = b * g.H + h;
     const float m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
     const float rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
-    const float Dv = valid ? Dvec[bh * L + i] : 0.f;
+    const float Dv = valid ? Dvec[g.tok(b, i) * g.H + h] : 0.f;
 
 #pragma unroll 1
     for (int kc = 0; kc < NKC; ++kc) {
@@ -470,7 +270,13 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
         }
         const int c0 = koff + cg * 16;  // this thread's 16 key columns
         float bias[16];
-        load_bias<16>(nbrow, c0, L, vec_ok, bias);
+        if (BIAS) {
+          bf16x8_to_f(*reinterpret_cast<const uint4*>(sBrow + c0), bias);
+          bf16x8_to_f(*reinterpret_cast<const uint4*>(sBrow + c0 + 8), bias + 8);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) bias[e] = 0.f;
+        }
         tc::mbar_wait(&bar[0], ph0);
         ph0 ^= 1;
         tc::fence_after();
@@ -568,6 +374,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
       __syncthreads();
       tc::fence_after();
     }
+    // single staging buffer: every MMA of this batch has completed, prefetch the next
+    if (SM::NS == 1 && b + 1 < b_hi) {
+      bwd_stage<D, LP>(smem, qkvg, dctx, mask, g, b + 1, h, q0, tid);
+      cp_async_commit();
+    }
     // ---- drain dQ ----
     {
       constexpr int DQ = D / 4;
@@ -608,7 +419,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
       if (valid) {
         float* dst = dnb_part + (((size_t)grp * g.H + h) * L + i) * L + cg * PER + c;
         const int j0 = cg * PER + c;
-        if (vec_ok && j0 + 16 <= L) {
+        if ((L % 4) == 0 && j0 + 16 <= L) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             reinterpret_cast<float4*>(dst)[k] = make_float4(vv[4 * k], vv[4 * k + 1], vv[4 * k + 2], vv[4 * k + 3]);
@@ -625,19 +436,25 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
   if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
-// thread per (b, h, l): dctx = dgated*gate (bf16), d(g) = dgated*ctx*gate*(1-gate), Dvec
-__global__ void attn_bwd_prep_tc_kernel(const bf16* __restrict__ ctx, const bf16* __restrict__ gate,
-                                        const bf16* __restrict__ dgated, bf16* __restrict__ dqkvg,
-                                        bf16* __restrict__ dctx, float* __restrict__ Dvec, AttnGeom g) {
-  const int64_t n = g.B * g.H * g.L;
-  const int64_t HD = g.H * g.D;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = e % g.L, h = (e / g.L) % g.H, b = e / (g.L * g.H);
-    const int64_t t = g.tok(b, l);
+// token-major, 8 channels per thread: dctx = dgated*gate (bf16, the dO the
+// MMAs read), d(g) = dgated*ctx*gate*(1-gate), Dvec[t, h] = sum_k dO*ctx
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
+    const bf16* __restrict__ ctx, const bf16* __restrict__ gate, const bf16* __restrict__ dgated,
+    bf16* __restrict__ dqkvg, bf16* __restrict__ dctx, float* __restrict__ Dvec, int64_t T, int H,
+    int64_t ld) {
+  constexpr int G = D / 8;  // threads per head
+  const int64_t HD8 = (int64_t)H * D / 8;
+  const int64_t n = T * HD8;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += step) {
+    const int64_t e = base + threadIdx.x;
+    const bool act = e < n;
+    const int64_t t = act ? e / HD8 : 0;
+    const int c8 = act ? (int)(e % HD8) : 0;
     float dsum = 0.f;
-    for (int k = 0; k < g.D; k += 8) {
-      const int64_t c = t * HD + h * g.D + k;
+    if (act) {
+      const int64_t c = t * (HD8 * 8) + c8 * 8;
       float dg[8], gv[8], cv[8];
       bf16x8_to_f(*reinterpret_cast<const uint4*>(dgated + c), dg);
       bf16x8_to_f(*reinterpret_cast<const uint4*>(gate + c), gv);
@@ -648,16 +465,17 @@ __global__ void attn_bwd_prep_tc_kernel(const bf16* __restrict__ ctx, const bf16
         const float d0 = dg[u] * gv[u], d1 = dg[u + 1] * gv[u + 1];
         const float g0 = dg[u] * cv[u] * gv[u] * (1.0f - gv[u]);
         const float g1 = dg[u + 1] * cv[u + 1] * gv[u + 1] * (1.0f - gv[u + 1]);
-        // D uses the bf16-rounded dO the MMAs see
         const __nv_bfloat162 dq = __floats2bfloat162_rn(d0, d1);
         dsum += __bfloat162float(dq.x) * cv[u] + __bfloat162float(dq.y) * cv[u + 1];
         pc[u / 2] = *reinterpret_cast<const uint32_t*>(&dq);
         pg[u / 2] = tc::pack_bf16(g0, g1);
       }
       *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
-      *reinterpret_cast<uint4*>(dqkvg + t * g.ld + 3 * HD + h * g.D + k) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      *reinterpret_cast<uint4*>(dqkvg + t * ld + 3 * HD8 * 8 + c8 * 8) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
     }
-    Dvec[e] = dsum;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+    if (act && (c8 % G) == 0) Dvec[t * H + c8 / G] = dsum;
   }
 }
 
@@ -711,34 +529,6 @@ bool tc_disabled() {
   return v == 1;
 }
 
-template <int D, int LP>
-void launch_fwd(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
-                void* gate, void* gated, float* lse, const AttnGeom& g, cudaStream_t s) {
-  using SM = FwdSmem<D, LP>;
-  auto k = attn_fwd_tc_kernel<D, LP>;
-  static bool attr = false;
-  if (!attr) {
-    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::total));
-    attr = true;
-  }
-  dim3 grid(cdiv(g.L, 128), (unsigned)g.H, (unsigned)g.B);
-  const float scale = (float)(1.0 / sqrt((double)D));
-  k<<<grid, 256, SM::total, s>>>((const bf16*)qkvg, mask, (const bf16*)nb, bg, (bf16*)ctx,
-                                 (bf16*)gate, (bf16*)gated, lse, g, scale);
-  EVO_LAUNCH_CHECK();
-  count_launch(1);
-}
-
-template <int D>
-void launch_fwd_lp(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
-                   void* gate, void* gated, float* lse, const AttnGeom& g, cudaStream_t s) {
-  const int64_t L = g.L;
-  if (L <= 64) launch_fwd<D, 64>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-  else if (L <= 128) launch_fwd<D, 128>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-  else if (L <= 192) launch_fwd<D, 192>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-  else launch_fwd<D, 256>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-}
-
 struct BwdPlan {
   int NQT, NG, LP;
   int64_t off_dctx, off_dvec, off_kv, off_part, off_cols, total;
@@ -761,7 +551,7 @@ BwdPlan bwd_plan(const AttnGeom& g) {
   p.off_kv = p.off_dvec + al(g.B * g.H * g.L * 4);
   p.off_part = p.off_kv + (p.NQT > 1 ? al(T * 2 * HD * 2) : 0);
   p.off_cols = p.off_part + al((int64_t)p.NG * g.H * g.L * g.L * 4);
-  p.total = p.off_cols + al((int64_t)EVO_PARTIAL_BLOCKS * HD * 4);
+  p.total = p.off_cols + al((int64_t)(EVO_PARTIAL_BLOCKS > 2 * num_sms() ? EVO_PARTIAL_BLOCKS : 2 * num_sms()) * HD * 4);
   return p;
 }
 
@@ -805,21 +595,6 @@ void launch_bwd_d(bool bias, int LP, const void* qkvg, const bf16* dctx, const f
 }
 
 }  // namespace
-
-bool attn_fwd_tc_try(const void* qkvg, const float* mask, const void* nb, const float* bg,
-                     void* ctx, void* gate, void* gated, float* lse, const AttnGeom& g, int dtype,
-                     cudaStream_t s) {
-  if (tc_disabled() || dtype != EVO_BF16) return false;
-  if (!(g.D == 16 || g.D == 32) || g.L > 256 || g.L < 1) return false;
-  if ((g.ld % 8) != 0 || (((uintptr_t)qkvg) & 15) != 0) return false;
-  if (((uintptr_t)ctx | (uintptr_t)gate | (uintptr_t)gated) & 15) return false;
-  if (g.D == 16)
-    launch_fwd_lp<16>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-  else
-    launch_fwd_lp<32>(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, s);
-  return true;
-}
-
 int64_t attn_bwd_tc_workspace(const AttnGeom& g, int dtype) {
   if (!bwd_supported(g, dtype)) return 0;
   return bwd_plan(g).total;
@@ -840,17 +615,25 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   bf16* kvpart = (bf16*)(w + p.off_kv);
   float* part = (float*)(w + p.off_part);
   float* cols = (float*)(w + p.off_cols);
-  const int64_t nbhl = g.B * g.H * g.L;
-  attn_bwd_prep_tc_kernel<<<cdiv(nbhl, 256), 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
-                                                           (const bf16*)dgated, (bf16*)dqkvg, dctx,
-                                                           Dvec, g);
-  EVO_LAUNCH_CHECK();
+  const int64_t T = g.B * g.L, HD = g.H * g.D;
+  {
+    const int64_t nthr = T * HD / 8;
+    const unsigned pgrid = (unsigned)imin64((nthr + 255) / 256, (int64_t)num_sms() * 8);
+    if (g.D == 16)
+      attn_bwd_prep_tc_kernel<16><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
+                                                         (const bf16*)dgated, (bf16*)dqkvg, dctx,
+                                                         Dvec, T, (int)g.H, g.ld);
+    else
+      attn_bwd_prep_tc_kernel<32><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
+                                                         (const bf16*)dgated, (bf16*)dqkvg, dctx,
+                                                         Dvec, T, (int)g.H, g.ld);
+    EVO_LAUNCH_CHECK();
+  }
   const bool bias = nb != nullptr && dnb != nullptr;
   if (g.D == 16)
     launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
   else
     launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
-  const int64_t T = g.B * g.L, HD = g.H * g.D;
   if (p.NQT > 1) {
     attn_kv_combine_kernel<<<cdiv(T * 2 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, kvpart, T, g.ld, HD);
     EVO_LAUNCH_CHECK();
@@ -860,10 +643,13 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
     attn_dnb_reduce_kernel<<<cdiv(n, 256), 256, 0, s>>>(part, dnb, n, p.NG, accumulate);
     EVO_LAUNCH_CHECK();
   }
-  const unsigned pg = partial_grid(T);
-  colsum_slice_kernel<bf16><<<pg, 256, 0, s>>>((const bf16*)dqkvg, g.ld, 3 * HD, cols, T, HD);
-  EVO_LAUNCH_CHECK();
-  finalize_partials(cols, pg, HD, dbg, accumulate, s);
+  if (!colsum_vec((bf16*)dqkvg + 3 * HD, EVO_BF16, g.ld, nullptr, nullptr, EVO_BF16, dbg, accumulate,
+                  cols, T, HD, 0, s)) {
+    const unsigned pg = partial_grid(T);
+    colsum_slice_kernel<bf16><<<pg, 256, 0, s>>>((const bf16*)dqkvg, g.ld, 3 * HD, cols, T, HD);
+    EVO_LAUNCH_CHECK();
+    finalize_partials(cols, pg, HD, dbg, accumulate, s);
+  }
   count_launch(3 + (p.NQT > 1) + bias);
   return true;
 }

@@ -119,6 +119,15 @@ __global__ void __launch_bounds__(LN_WARPS * 32) ln_bwd_kernel(
     else throw Error(EVO_ERR_UNSUPPORTED, "layernorm: C > 1024");             \
   } while (0)
 
+// vectorised kernels (glue.cu)
+bool ln_fwd_vec(const void* x, int xdt, const float* g, const float* b, void* y, int ydt,
+                float* mean, float* rstd, int64_t rows, int64_t C, float eps, cudaStream_t s);
+int64_t ln_bwd_vec_ws(int64_t C);
+bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* mean, const float* rstd,
+                const float* g, const float* dres, float* dx, __nv_bfloat16* dx16, float* dgamma,
+                float* dbeta, float* dxsum, int accumulate, void* ws, int64_t rows, int64_t C,
+                cudaStream_t s);
+
 }  // namespace evo
 
 using namespace evo;
@@ -132,6 +141,7 @@ int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const floa
   EVO_REQUIRE(C > 0, EVO_ERR_ARG, "layernorm: C must be positive");
   if (rows == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (ln_fwd_vec(x, x_dtype, gamma, beta, y, y_dtype, mean, rstd, rows, C, eps, s)) return EVO_OK;
   unsigned grid = cdiv(rows, LN_WARPS);
   LN_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(x_dtype, TX, EVO_DISPATCH_T(y_dtype, TY, {
     ln_fwd_kernel<TX, TY, NPL><<<grid, LN_WARPS * 32, 0, s>>>(
@@ -144,7 +154,24 @@ int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const floa
 
 int64_t evo_layernorm_bwd_workspace(int64_t rows, int64_t C) {
   (void)rows;
-  return (int64_t)EVO_PARTIAL_BLOCKS * 2 * C * 4;
+  const int64_t a = (int64_t)EVO_PARTIAL_BLOCKS * 2 * C * 4, b = ln_bwd_vec_ws(C);
+  return a > b ? a : b;
+}
+
+int evo_layernorm_bwd_ex(const void* x, int x_dtype, const void* dy, int dy_dtype,
+                         const float* mean, const float* rstd, const float* gamma,
+                         const float* dres, float* dx, void* dx_bf16, float* dxsum,
+                         float* dgamma, float* dbeta, int accumulate, void* ws, int64_t rows,
+                         int64_t C, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(C > 0 && ws, EVO_ERR_ARG, "layernorm_bwd: bad arguments");
+  if (rows == 0) return EVO_OK;
+  const bool ok = ln_bwd_vec(x, x_dtype, dy, dy_dtype, mean, rstd, gamma, dres, dx,
+                             (__nv_bfloat16*)dx_bf16, dgamma, dbeta, dxsum, accumulate, ws, rows,
+                             C, (cudaStream_t)stream);
+  EVO_REQUIRE(ok, EVO_ERR_UNSUPPORTED,
+              "layernorm_bwd_ex: needs a power-of-two width in [32, 1024] and 16-B aligned rows");
+  EVO_API_END
 }
 
 int evo_layernorm_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, const float* mean,
@@ -155,6 +182,9 @@ int evo_layernorm_bwd(const void* x, int x_dtype, const void* dy, int dy_dtype, 
   EVO_REQUIRE(C > 0 && ws, EVO_ERR_ARG, "layernorm_bwd: bad arguments");
   if (rows == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (ln_bwd_vec(x, x_dtype, dy, dy_dtype, mean, rstd, gamma, dres, dx, nullptr, dgamma, dbeta,
+                 nullptr, accumulate, ws, rows, C, s))
+    return EVO_OK;
   int64_t want = (rows + LN_WARPS - 1) / LN_WARPS;
   unsigned grid = (unsigned)(want < EVO_PARTIAL_BLOCKS ? want : EVO_PARTIAL_BLOCKS);
   size_t smem = (size_t)LN_WARPS * 2 * C * sizeof(float);

@@ -118,6 +118,9 @@ __global__ void sq_loss_final_kernel(const float* __restrict__ pm, const float* 
   *loss = lm + lz;
 }
 
+bool opm_norm_vec(bool fwd, const void* src, int sdt, const float* mask, float* rec, void* dst, int ddt,
+                  int64_t S, int64_t R, int64_t k, cudaStream_t s);
+
 }  // namespace evo
 
 using namespace evo;
@@ -162,6 +165,7 @@ int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* r
                      int out_dtype, int64_t S, int64_t R, int64_t k, void* stream) {
   EVO_API_BEGIN
   cudaStream_t s = (cudaStream_t)stream;
+  if (opm_norm_vec(true, num, num_dtype, mask, rec, outn, out_dtype, S, R, k, s)) return EVO_OK;
   opm_rec_kernel<<<cdiv(R * R, 256), 256, 0, s>>>(mask, rec, S, R);
   EVO_LAUNCH_CHECK();
   int bs = (int)(k * k < 256 ? ((k * k + 31) / 32) * 32 : 256);
@@ -176,6 +180,9 @@ int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* r
 int evo_opm_norm_bwd(const void* doutn, int in_dtype, const float* rec, void* dnum, int out_dtype,
                      int64_t R, int64_t k, void* stream) {
   EVO_API_BEGIN
+  if (opm_norm_vec(false, doutn, in_dtype, nullptr, const_cast<float*>(rec), dnum, out_dtype, 0, R, k,
+                   (cudaStream_t)stream))
+    return EVO_OK;
   int bs = (int)(k * k < 256 ? ((k * k + 31) / 32) * 32 : 256);
   EVO_DISPATCH_T(in_dtype, TI, EVO_DISPATCH_T(out_dtype, TO, {
     opm_norm_bwd_kernel<TI, TO><<<(unsigned)(R * R), bs, 0, (cudaStream_t)stream>>>(

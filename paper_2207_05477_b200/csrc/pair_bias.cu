@@ -159,6 +159,15 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
     else throw Error(EVO_ERR_UNSUPPORTED, "pair_bias: C > 256");              \
   } while (0)
 
+bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
+                       float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap,
+                       cudaStream_t s);
+int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
+bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
+                       const float* bln, const float* w, const float* dnb, int swap, float* dz,
+                       float* dg, float* db, float* dw, int accumulate, void* ws, int64_t R,
+                       int64_t C, int64_t H, cudaStream_t s);
+
 }  // namespace evo
 
 using namespace evo;
@@ -172,6 +181,8 @@ int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* 
   EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
   if (R == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pair_bias_fwd_vec(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, C, H, swap_xy, s))
+    return EVO_OK;
   unsigned grid = cdiv(R * R, PB_WARPS);
   PB_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(dtype, T, {
     pair_bias_fwd_kernel<T, NPL><<<grid, PB_WARPS * 32, 0, s>>>(
@@ -183,7 +194,8 @@ int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* 
 }
 
 int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H) {
-  return (int64_t)EVO_PARTIAL_BLOCKS * (C * H + 2 * C) * 4;
+  const int64_t a = (int64_t)EVO_PARTIAL_BLOCKS * (C * H + 2 * C) * 4, b = pair_bias_bwd_vec_ws(C, H);
+  return a > b ? a : b;
 }
 
 int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
@@ -196,6 +208,9 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
   EVO_REQUIRE(ws != nullptr, EVO_ERR_ARG, "pair_bias_bwd: workspace required");
   if (R == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pair_bias_bwd_vec(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b,
+                        dw_bias, accumulate, ws, R, C, H, s))
+    return EVO_OK;
   const int64_t want = (R * R + PB_WARPS - 1) / PB_WARPS;
   unsigned grid = (unsigned)(want < EVO_PARTIAL_BLOCKS ? want : EVO_PARTIAL_BLOCKS);
   const int64_t W = C * H + 2 * C;

@@ -165,3 +165,86 @@ def test_layernorm_fwd_bwd_vs_torch(dtype, C):
     assert rel(dx - dres, xr.grad) <= 1e-4
     assert rel(dg, gr.grad) <= 1e-4
     assert rel(db, brr.grad) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("C,H,swap", [(128, 8, 0), (128, 8, 1), (32, 2, 0), (64, 4, 1), (16, 4, 0)])
+def test_pair_bias_fwd_bwd_vs_torch(dtype, C, H, swap):
+    from paper_2207_05477_b200 import ops
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    R = 48
+    torch.manual_seed(C + H + swap)
+    z = torch.randn(R * R, C, device="cuda").to(dt)
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda") * 0.1
+    w = torch.randn(C, H, device="cuda") * 0.2
+    nb, mu, rs = ops.pair_bias_fwd(z, g, b, w, R, H, swap)
+    zr = z.float().requires_grad_(True)
+    gr, br_, wr = (t.clone().requires_grad_(True) for t in (g, b, w))
+    P = torch.nn.functional.layer_norm(zr, (C,), gr, br_, 1e-5) @ wr      # [R*R, H]
+    ref = P.view(R, R, H).permute(2, 0, 1)
+    if swap:
+        ref = ref.transpose(1, 2)
+    tol = 1e-5 if dtype == "f32" else 1e-2
+    assert rel(nb.float(), ref) <= tol
+    dnb = torch.randn(H, R, R, device="cuda")
+    dz0 = torch.randn(R * R, C, device="cuda")
+    dz = dz0.clone()
+    dg, db, dw = (torch.empty(C, device="cuda"), torch.empty(C, device="cuda"),
+                  torch.empty(C, H, device="cuda"))
+    ops.pair_bias_bwd(z, mu, rs, g, b, w, dnb, swap, dz, dg, db, dw, R, H)
+    ref.backward(dnb)
+    assert rel(dz - dz0, zr.grad) <= 1e-4
+    assert rel(dg, gr.grad) <= 1e-4
+    assert rel(db, br_.grad) <= 1e-4
+    assert rel(dw, wr.grad) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("C", [64, 128, 256, 512, 1024, 96])
+def test_colsum_relu_bias_kernels_vs_torch(dtype, C):
+    from paper_2207_05477_b200 import ops
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    torch.manual_seed(C)
+    rows = 3001
+    x = torch.randn(rows, C, device="cuda")
+    out = torch.empty(C, device="cuda")
+    y = torch.empty(rows, C, device="cuda", dtype=dt)
+    ops.colsum_cast(x, out, y=y)
+    assert rel(out, x.double().sum(0).float()) <= 1e-5
+    assert rel(y.float(), x.to(dt).float()) == 0.0
+    h = torch.randn(rows, C, device="cuda").to(dt)
+    dh = torch.randn(rows, C, device="cuda").to(dt)
+    want = (dh.float() * (h.float() > 0))
+    db = torch.empty(C, device="cuda")
+    ops.relu_bwd_colsum_(dh, h, db)
+    assert rel(dh.float(), want) == 0.0
+    assert rel(db, want.sum(0)) <= 1e-5
+    bias = torch.randn(C, device="cuda")
+    res = torch.randn(rows, C, device="cuda").to(dt)
+    yy = torch.randn(rows, C, device="cuda").to(dt)
+    o = torch.empty_like(res)
+    ops.bias_residual(res, yy, bias, o)
+    assert rel(o.float(), (res.float() + (yy.float() + bias)).to(dt).float()) <= 1e-2 if dt == torch.bfloat16 else 1e-6
+
+
+def test_layernorm_bwd_ex_fused_outputs():
+    from paper_2207_05477_b200 import _lib, ops
+    C, rows = 256, 4099
+    x = torch.randn(rows, C, device="cuda").to(torch.bfloat16)
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    y, mu, rs = ops.layernorm(x, g, b, torch.bfloat16)
+    dy = torch.randn(rows, C, device="cuda")
+    dres = torch.randn(rows, C, device="cuda")
+    dx = dres.clone()
+    dx16 = torch.empty(rows, C, device="cuda", dtype=torch.bfloat16)
+    dxs, dg, db = (torch.empty(C, device="cuda") for _ in range(3))
+    ws = torch.empty(_lib.load().evo_layernorm_bwd_workspace(rows, C), dtype=torch.uint8, device="cuda")
+    ops.call("evo_layernorm_bwd_ex", ops.ptr(x), ops.dcode(x), ops.ptr(dy), ops.dcode(dy), ops.ptr(mu),
+             ops.ptr(rs), ops.ptr(g), ops.ptr(dx), ops.ptr(dx), ops.ptr(dx16), ops.ptr(dxs), ops.ptr(dg),
+             ops.ptr(db), 0, ops.ptr(ws), rows, C, ops.stream())
+    dx2 = dres.clone()
+    dg2, db2 = torch.empty(C, device="cuda"), torch.empty(C, device="cuda")
+    ops.layernorm_bwd(x, dy, mu, rs, g, dx2, dx2, dg2, db2)
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+    assert torch.equal(dx16, dx.to(torch.bfloat16))
+    assert rel(dxs, dx.double().sum(0).float()) <= 1e-5

@@ -49,7 +49,7 @@ def test_bound_signatures_exist_in_header():
 
 def test_host_only_queries(lib):
     assert lib.evo_version() >= 1
-    assert lib.evo_layernorm_bwd_workspace(100, 256) == 256 * 2 * 256 * 4
+    assert lib.evo_layernorm_bwd_workspace(100, 256) >= 256 * 2 * 256 * 4
     assert lib.evo_attn_bwd_workspace(4, 64, 2, 32, 1) > 0
 
 
