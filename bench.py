@@ -268,14 +268,30 @@ def run_ours(args):
     hosts = []
     for s in range(min(4, max(1, args.steps))):
         h = PinnedFeatures(cfg)
-        h.fill(make_features(cfg, step_feature_seed(plan.seed + 7919 * rank, s)))
+        rep = rank // 2 if (world > 1 and world % 2 == 0) else rank  # both BP ranks: one sample
+        h.fill(make_features(cfg, step_feature_seed(plan.seed + 7919 * rep, s)))
         hosts.append(h)
     trainer.host = hosts[0]
     trainer.feats.copy_from_host(hosts[0])
     torch.cuda.synchronize()
 
-    use_graph = not args.no_graph
-    n0 = _lib.launch_count()
+    grid = None
+    if world > 1:
+        from paper_2207_05477_b200.parallel import GridConfig, bp_step, build_groups, dp_step
+        grid = GridConfig.for_world(world)
+        bp_comm, world_comm = build_groups(grid)
+
+    def eager_step():
+        if grid is None:
+            loss, _ = trainer.engine.forward_backward(trainer.feats, 1)
+        elif grid.bp == 2:
+            loss = bp_step(trainer.engine, trainer.feats, bp_comm, world_comm, grid, cfg.n_blocks)
+        else:
+            loss = dp_step(trainer.engine, trainer.feats, world_comm, grid)
+        trainer.store.step()
+        return loss
+
+    use_graph = not args.no_graph and world == 1
     if use_graph:
         trainer.capture(n_cycles=1, warmup=max(1, args.warmup))
 
@@ -284,18 +300,12 @@ def run_ours(args):
             return trainer.graph_loss
     else:
         for _ in range(args.warmup):
-            trainer.engine.forward_backward(trainer.feats, 1)
-            trainer.store.step()
-
-        def step():
-            loss, _ = trainer.engine.forward_backward(trainer.feats, 1)
-            trainer.store.step()
-            return loss
+            eager_step()
+        step = eager_step
     torch.cuda.synchronize()
     # launches per step: count one eager step
     c0 = _lib.launch_count()
-    trainer.engine.forward_backward(trainer.feats, 1)
-    trainer.store.step()
+    eager_step()
     torch.cuda.synchronize()
     launches_per_step = _lib.launch_count() - c0
     for _ in range(args.warmup):
@@ -337,7 +347,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = float(t[0]), float(t[1])
 
-    samples = args.steps * world
+    samples = args.steps * (grid.dp if grid is not None else 1)  # a BP pair shares one sample
     value = samples / dev_s
     e2e_value = samples / e2e_s
     peaks = load_peaks()
@@ -381,7 +391,7 @@ def run_ours(args):
                 "data": "synthetic (reference PRNG features, random-init weights)",
                 "config": {"workload": "48-block Evoformer training step (fwd+bwd+fused Adam), "
                                        "initial shape, 1 recycle", **shape,
-                           "parallelism": f"dp{world}" if world > 1 else "single",
+                           "parallelism": (f"dp{grid.dp}xbp{grid.bp}" if grid is not None else "single"),
                            "l2": "working set (~tens of GB of activations) >> 126 MB L2",
                            "cuda_graph": use_graph},
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,

@@ -344,20 +344,44 @@ class BlockEngine:
             rec = (pm, m1, r1, pz, m2, r2)
         return msa, pair, rec
 
-    def embed_bwd(self, d_msa, d_pair, feats: DeviceFeatures, rec):
-        ops.gemm(feats.msa_feat, d_msa, self.G("msa_embed.w"), ta=True)
-        ops.colsum_cast(d_msa, self.G("msa_embed.b"))
-        ops.gemm(feats.pair_feat, d_pair, self.G("pair_embed.w"), ta=True)
-        ops.colsum_cast(d_pair, self.G("pair_embed.b"))
+    def embed_bwd(self, d_msa, d_pair, feats: DeviceFeatures, rec, which: str = "both"):
+        """``which`` = 'msa' / 'pair' closes out one branch only (BP ranks)."""
+        if which in ("both", "msa"):
+            ops.gemm(feats.msa_feat, d_msa, self.G("msa_embed.w"), ta=True)
+            ops.colsum_cast(d_msa, self.G("msa_embed.b"))
+        if which in ("both", "pair"):
+            ops.gemm(feats.pair_feat, d_pair, self.G("pair_embed.w"), ta=True)
+            ops.colsum_cast(d_pair, self.G("pair_embed.b"))
         if rec is not None:
             R = self.cfg.n_res
             pm, m1, r1, pz, m2, r2 = rec
-            scratch = torch.empty_like(d_msa[:R])
-            ops.layernorm_bwd(pm, d_msa[:R], m1, r1, self.P("recycle_m.g"), None, scratch,
-                              self.G("recycle_m.g"), self.G("recycle_m.b"))
-            scratch = torch.empty_like(d_pair)
-            ops.layernorm_bwd(pz, d_pair, m2, r2, self.P("recycle_z.g"), None, scratch,
-                              self.G("recycle_z.g"), self.G("recycle_z.b"))
+            if which in ("both", "msa"):
+                scratch = torch.empty_like(d_msa[:R])
+                ops.layernorm_bwd(pm, d_msa[:R], m1, r1, self.P("recycle_m.g"), None, scratch,
+                                  self.G("recycle_m.g"), self.G("recycle_m.b"))
+            if which in ("both", "pair"):
+                scratch = torch.empty_like(d_pair)
+                ops.layernorm_bwd(pz, d_pair, m2, r2, self.P("recycle_z.g"), None, scratch,
+                                  self.G("recycle_z.g"), self.G("recycle_z.b"))
+
+    # -- small helpers used by the parallel step (parallel.py) ---------------------
+
+    def zero_grads(self):
+        self.st.zero_grads()
+
+    def grad_region(self):
+        return self.st.regions["grads"]
+
+    def empty_like(self, t):
+        return torch.empty_like(t)
+
+    def zeros_like(self, t):
+        return torch.zeros_like(t)
+
+    def add(self, a, b):
+        out = torch.empty_like(a)
+        ops.bias_residual(a, b, None, out)
+        return out
 
     def loss(self, msa, pair):
         cfg = self.cfg

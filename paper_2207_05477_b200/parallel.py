@@ -1,0 +1,246 @@
+"""Branch Parallelism (BP) and data parallelism (DP) over torch.distributed.
+
+Rebuilds the reference's grid runner (src/harness.py:53-76, 392-553,
+570-645) with one process per GPU (NCCL over NVLink/NVSwitch; gloo for the
+CPU tests) instead of thread-simulated ranks:
+
+* rank = dp_i * bp + bp_i (``GridConfig.rank`` with dap = 1);
+* BP pairs {2k, 2k+1}: bp rank 0 runs the MSA stack (row + column attention,
+  MSA transition) and the outer-product mean, bp rank 1 runs the pair stack
+  (triangle attention start/end, pair transition [, TriangleMultiplication]);
+  the two branches of a block are independent given the block inputs
+  because the OPM reads the block-input MSA (src/model.py:440), so rank 1's
+  pair stack of block i overlaps rank 0's MSA stack of block i;
+* per block and step: forward broadcasts opm (root 0), msa' (root 0),
+  pair' (root 1); backward one all-reduce of d(pair_in) -- exactly the
+  reference's 3 Broadcast + 1 AllReduce (tests/test_acceptance.py:156-166);
+* gradient exchange: the closing broadcast of d(msa) (module "msa_grad"),
+  then ONE all-reduce of the whole pooled grad region over the world (each
+  parameter's gradient is non-zero on exactly one rank of a BP pair, so the
+  sum equals the reference's per-branch broadcasts), scaled by 1/dp -- the
+  DP average of src/harness.py:607-616 folded into the same collective.
+
+The step is written against a small engine protocol (``BlockEngine`` on the
+GPU; the tests drive it with an adapter around the CPU oracle), and a
+``Comm`` wrapper that records the reference's CommRecord trace
+(src/harness.py:79-101).
+"""
+
+from __future__ import annotations
+
+import csv
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import ContractError
+
+
+@dataclass(frozen=True)
+class GridConfig:
+    """src/harness.py:53-76 (DAP is out of scope: dap must be 1)."""
+
+    dp: int = 1
+    bp: int = 1
+    dap: int = 1
+
+    def __post_init__(self):
+        if self.dp < 1 or self.bp < 1 or self.dap < 1:
+            raise ContractError("grid axes must be >= 1")
+        if self.bp not in (1, 2):
+            raise ContractError("branch parallelism supports size 1 or 2")
+        if self.bp > 1 and self.dap > 1:
+            raise ContractError("bp and dap axes do not compose")
+        if self.dap != 1:
+            raise ContractError("DAP is not part of this build (BP x DP only)")
+
+    @property
+    def world(self) -> int:
+        return self.dp * self.bp * self.dap
+
+    def coords(self, rank: int):
+        inner = self.bp * self.dap
+        return rank // inner, (rank % inner) // self.dap, rank % self.dap
+
+    def rank(self, dpi: int, bpi: int, dapi: int = 0) -> int:
+        return dpi * self.bp * self.dap + bpi * self.dap + dapi
+
+    @staticmethod
+    def for_world(world: int) -> "GridConfig":
+        """1 -> serial, 2 -> bp2, 2k -> dp k x bp 2 (the survey's grids)."""
+        if world == 1:
+            return GridConfig()
+        if world % 2:
+            return GridConfig(dp=world)
+        return GridConfig(dp=world // 2, bp=2)
+
+
+@dataclass
+class CommRecord:
+    step: int
+    phase: str
+    group_axis: str
+    group_id: int
+    seq: int
+    primitive: str
+    bytes: int
+    module: str
+
+
+CSV_COLUMNS = ["step", "phase", "group_axis", "group_id", "seq", "primitive", "bytes", "module"]
+
+
+def dump_comm_csv(records, path):
+    """Same columns as the reference trace (src/harness.py:91-101)."""
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(CSV_COLUMNS)
+        for r in records:
+            w.writerow([r.step, r.phase, r.group_axis, r.group_id, r.seq, r.primitive, r.bytes,
+                        r.module])
+
+
+class Comm:
+    """One rank's endpoint on one grid axis, over a torch.distributed group."""
+
+    def __init__(self, axis: str, group_id: int, ranks: list, group=None):
+        self.axis = axis
+        self.group_id = group_id
+        self.ranks = list(ranks)
+        self.group = group
+        self.size = len(ranks)
+        self.rank = self.ranks.index(dist.get_rank()) if dist.is_initialized() else 0
+        self._seq = 0
+        self.records: list = []
+        self.step = 0
+        self.phase = "fwd"
+
+    def _rec(self, primitive, t, module):
+        self.records.append(CommRecord(self.step, self.phase, self.axis, self.group_id, self._seq,
+                                       primitive, t.numel() * t.element_size(), module))
+        self._seq += 1
+
+    def broadcast(self, t: torch.Tensor, root: int, module: str) -> torch.Tensor:
+        """In place: ``t`` is the payload on the root, the receive buffer elsewhere."""
+        dist.broadcast(t, src=self.ranks[root], group=self.group)
+        self._rec("broadcast", t, module)
+        return t
+
+    def allreduce_sum(self, t: torch.Tensor, module: str) -> torch.Tensor:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        self._rec("allreduce", t, module)
+        return t
+
+
+def build_groups(grid: GridConfig):
+    """All ranks must create every group in the same order (torch.distributed
+    rule).  Returns (bp Comm or None, world Comm)."""
+    me = dist.get_rank()
+    dpi, bpi, _ = grid.coords(me)
+    bp_comm = None
+    if grid.bp == 2:
+        for d in range(grid.dp):
+            ranks = [grid.rank(d, 0), grid.rank(d, 1)]
+            g = dist.new_group(ranks)
+            if d == dpi:
+                bp_comm = Comm("bp", d, ranks, g)
+    world = Comm("dp", 0, list(range(grid.world)), None)
+    return bp_comm, world
+
+
+@dataclass
+class StepResult:
+    loss: float
+    records: list = field(default_factory=list)
+
+
+def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: int,
+            step: int = 0, n_cycles: int = 1):
+    """One branch-parallel forward/backward (src/harness.py:392-553) plus the
+    fused gradient all-reduce.  Returns the device loss tensor ([1]); the
+    pooled grad region ends up holding the world-averaged gradients."""
+    me = bp.rank
+    for c in (bp, world):
+        c.step = step
+        c.phase = "fwd"
+    engine.zero_grads()
+    prev = None
+    for _ in range(max(0, n_cycles - 1)):  # replicated recycling warm-up, no comm (:406-415)
+        prev = engine.forward_only(feats, prev)
+    msa, pair, rec = engine.embed_fwd(feats, prev)
+    saved = []
+    for i in range(n_blocks):
+        if me == 0:
+            opm, so = engine.opm_fwd(msa, f"block{i}.opm", feats, pair_res=None)
+            bp.broadcast(opm, 0, "opm")
+            msa_out, sm = engine.msa_branch_fwd(i, msa, pair, feats)
+            bp.broadcast(msa_out, 0, "msa_stack")
+            pair_out = engine.empty_like(pair)
+            bp.broadcast(pair_out, 1, "pair_stack")
+            saved.append((so, sm))
+        else:
+            opm = engine.empty_like(pair)
+            bp.broadcast(opm, 0, "opm")
+            pair_mid = engine.add(pair, opm)
+            pair_out, sp = engine.pair_branch_fwd(i, pair_mid, feats)
+            msa_out = engine.empty_like(msa)
+            bp.broadcast(msa_out, 0, "msa_stack")
+            bp.broadcast(pair_out, 1, "pair_stack")
+            saved.append(sp)
+        msa, pair = msa_out, pair_out
+    loss, d_msa, d_pair = engine.loss(msa, pair)
+
+    for c in (bp, world):
+        c.phase = "bwd"
+    for i in reversed(range(n_blocks)):
+        if me == 0:
+            so, sm = saved[i]
+            b_contrib = engine.zeros_like(d_pair)
+            engine.msa_branch_bwd(i, d_msa, b_contrib, sm, feats)   # d_msa -> d(msa_in) part
+            s = b_contrib.clone()
+            bp.allreduce_sum(s, "pair_stack")
+            d_opm = s - b_contrib                                   # src/harness.py:505
+            dxl = engine.opm_bwd_core(d_opm, so, f"block{i}.opm", feats)
+            engine.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)
+            d_pair = s
+        else:
+            engine.pair_branch_bwd(i, d_pair, saved[i], feats)     # d_pair -> d(pair_mid)
+            bp.allreduce_sum(d_pair, "pair_stack")
+        saved[i] = None
+    # embeddings: each worker closes out its own branch (src/harness.py:518-522)
+    if me == 0:
+        engine.embed_bwd(d_msa, engine.zeros_like(d_pair), feats, rec, which="msa")
+    else:
+        engine.embed_bwd(engine.zeros_like(d_msa), d_pair, feats, rec, which="pair")
+
+    for c in (bp, world):
+        c.phase = "grad-sync"
+    closing = d_msa if me == 0 else engine.empty_like(d_msa)
+    bp.broadcast(closing, 0, "msa_grad")
+    g = engine.grad_region()
+    world.allreduce_sum(g, "grad_sync")
+    if grid.dp > 1:
+        g.mul_(np.float32(1.0 / grid.dp).item())
+    lt = loss.reshape(1).clone()
+    if grid.dp > 1:
+        # every rank of a BP pair holds the same replicated loss: world sum / world
+        world.allreduce_sum(lt, "loss")
+        lt.mul_(np.float32(1.0 / grid.world).item())
+    return lt
+
+
+def dp_step(engine, feats, world: Comm, grid: GridConfig, n_cycles: int = 1, step: int = 0):
+    """Pure data parallelism: serial fwd+bwd per replica, one all-reduce of the
+    pooled grad region (src/harness.py:607-616)."""
+    world.step = step
+    world.phase = "grad-sync"
+    loss, _ = engine.forward_backward(feats, n_cycles)
+    g = engine.grad_region()
+    world.allreduce_sum(g, "grad_sync")
+    g.mul_(np.float32(1.0 / grid.dp).item())
+    lt = loss.reshape(1).clone()
+    world.allreduce_sum(lt, "loss")
+    lt.mul_(np.float32(1.0 / grid.dp).item())
+    return lt
