@@ -52,6 +52,14 @@ int evo_version(void);
 int evo_device_check(int* sm_major, int* sm_minor, int* num_sms);
 /* Kernel-launch counter (launches issued by this library on this thread). */
 int64_t evo_launch_count(void);
+/* Deferred reductions: between begin and end, the per-block partial rows of
+ * every column reduction (bias / LayerNorm-affine / pair-bias weight grads)
+ * go into `arena` and their finalisation is batched into one launch at
+ * evo_defer_end (fixed summation order, identical results).  The arena must
+ * stay alive until evo_defer_end's work has run on `stream`. */
+int evo_defer_begin(void* arena, size_t bytes);
+int evo_defer_end(void* stream);
+size_t evo_defer_used(void);
 
 /* ---- dense projections ----------------------------------------------------
  * Replaces the np.matmul projections of src/attention.py:141,167,173,

@@ -27,6 +27,9 @@ SIGNATURES = {
     "evo_version": (_i, []),
     "evo_device_check": (_i, [ctypes.POINTER(_i), ctypes.POINTER(_i), ctypes.POINTER(_i)]),
     "evo_launch_count": (_i64, []),
+    "evo_defer_begin": (_i, [_p, _sz]),
+    "evo_defer_end": (_i, [_p]),
+    "evo_defer_used": (_sz, []),
     "evo_gemm": (_i, [_i64, _i64, _i64, _p, _i64, _i, _i64, _p, _i64, _i, _i64, _p, _i64, _i64,
                       _i, _f, _f, _i, _i, _p]),
     "evo_layernorm_fwd": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i64, _i64, _f, _p]),

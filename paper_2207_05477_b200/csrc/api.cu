@@ -15,6 +15,18 @@ static thread_local int64_t g_launches = 0;
 void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(int n) { g_launches += n; }
 
+DeferState& defer_state() {
+  static thread_local DeferState st;
+  return st;
+}
+
+static __global__ void __launch_bounds__(256) finalize_batch_kernel(const __grid_constant__ FinBatch b) {
+  __shared__ float sm[8][33];
+  const FinDesc& d = b.d[blockIdx.y];
+  if ((int64_t)blockIdx.x * 32 >= d.C) return;  // whole block
+  finalize_cols(d.part, d.G, d.C, d.ld, d.out, d.accumulate, blockIdx.x, sm);
+}
+
 // ---------------------------------------------------------------------------
 // cuBLAS handle per (thread, device); a fixed workspace so the handle is
 // usable inside CUDA-graph capture.
@@ -147,6 +159,45 @@ extern "C" {
 const char* evo_last_error(void) { return g_last_error.c_str(); }
 int evo_version(void) { return 1; }
 int64_t evo_launch_count(void) { return g_launches; }
+
+int evo_defer_begin(void* arena, size_t bytes) {
+  EVO_API_BEGIN
+  DeferState& d = defer_state();
+  EVO_REQUIRE(!d.on, EVO_ERR_ARG, "evo_defer_begin: already deferring");
+  EVO_REQUIRE(arena != nullptr && bytes > 0, EVO_ERR_ARG, "evo_defer_begin: empty arena");
+  d.on = true;
+  d.arena = (char*)arena;
+  d.cap = bytes;
+  d.used = 0;
+  d.list.clear();
+  EVO_API_END
+}
+
+int evo_defer_end(void* stream) {
+  EVO_API_BEGIN
+  DeferState& d = defer_state();
+  EVO_REQUIRE(d.on, EVO_ERR_ARG, "evo_defer_end without evo_defer_begin");
+  d.on = false;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (size_t i0 = 0; i0 < d.list.size(); i0 += FIN_BATCH) {
+    FinBatch b{};
+    b.n = (int)std::min<size_t>(FIN_BATCH, d.list.size() - i0);
+    int maxc = 0;
+    for (int k = 0; k < b.n; ++k) {
+      b.d[k] = d.list[i0 + k];
+      maxc = std::max(maxc, b.d[k].C);
+    }
+    dim3 grid(cdiv(maxc, 32), (unsigned)b.n);
+    finalize_batch_kernel<<<grid, 256, 0, s>>>(b);
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+  }
+  d.list.clear();
+  d.used = 0;
+  EVO_API_END
+}
+
+size_t evo_defer_used(void) { return defer_state().used; }
 
 int evo_device_check(int* sm_major, int* sm_minor, int* nsm) {
   EVO_API_BEGIN

@@ -551,7 +551,7 @@ BwdPlan bwd_plan(const AttnGeom& g) {
   p.off_kv = p.off_dvec + al(g.B * g.H * g.L * 4);
   p.off_part = p.off_kv + (p.NQT > 1 ? al(T * 2 * HD * 2) : 0);
   p.off_cols = p.off_part + al((int64_t)p.NG * g.H * g.L * g.L * 4);
-  p.total = p.off_cols + al((int64_t)(EVO_PARTIAL_BLOCKS > 2 * num_sms() ? EVO_PARTIAL_BLOCKS : 2 * num_sms()) * HD * 4);
+  p.total = p.off_cols + al((int64_t)(EVO_PARTIAL_BLOCKS > 8 * num_sms() ? EVO_PARTIAL_BLOCKS : 8 * num_sms()) * HD * 4);
   return p;
 }
 

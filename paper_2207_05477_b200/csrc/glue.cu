@@ -21,9 +21,13 @@ constexpr int GT = 256;  // threads per block for all glue kernels
 
 inline bool pow2_width(int64_t C) { return C >= 32 && C <= 1024 && (C & (C - 1)) == 0; }
 
-inline unsigned glue_grid(int64_t rows, int rows_per_iter) {
+// Streaming kernels (no partials) take up to 16 blocks per SM so every warp
+// has its loads in flight at once; kernels writing per-block partials are
+// capped at PARTIAL_PER_SM blocks per SM (bounded partial rows).
+constexpr int PARTIAL_PER_SM = 2;
+inline unsigned glue_grid(int64_t rows, int rows_per_iter, int per_sm = 16) {
   int64_t want = (rows + rows_per_iter - 1) / rows_per_iter;
-  int64_t cap = (int64_t)num_sms() * 2;
+  int64_t cap = (int64_t)num_sms() * per_sm;
   if (want > cap) want = cap;
   return (unsigned)(want > 0 ? want : 1);
 }
@@ -487,7 +491,7 @@ template <int C, typename TX>
 void ln_fwd_dispatch_y(const void* x, const float* g, const float* b, void* y, int ydt, float* mean,
                        float* rstd, int64_t rows, float eps, cudaStream_t s) {
   using M = RowMap<C>;
-  unsigned grid = glue_grid(rows, M::GROUPS * 4);
+  unsigned grid = glue_grid(rows, M::GROUPS);
   EVO_DISPATCH_T(ydt, TY, {
     ln_fwd_vec_kernel<C, TX, TY><<<grid, GT, 0, s>>>((const TX*)x, g, b, (TY*)y, mean, rstd, rows, eps);
   });
@@ -524,7 +528,7 @@ bool ln_fwd_vec(const void* x, int xdt, const float* g, const float* b, void* y,
   return true;
 }
 
-int64_t ln_bwd_vec_ws(int64_t C) { return (int64_t)num_sms() * 2 * 3 * C * 4; }
+int64_t ln_bwd_vec_ws(int64_t C) { return (int64_t)num_sms() * PARTIAL_PER_SM * 3 * C * 4; }
 
 bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* mean, const float* rstd,
                 const float* g, const float* dres, float* dx, __nv_bfloat16* dx16, float* dgamma,
@@ -533,10 +537,11 @@ bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* m
   if (!pow2_width(C) || !al16(x) || !al16(dy) || !al16(dx) || (dres && !al16(dres)) ||
       (dx16 && !al16(dx16)))
     return false;
+  ws = partial_buffer(ws, ln_bwd_vec_ws(C));
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     using M = RowMap<CC>;
-    grid = glue_grid(rows, M::GROUPS * 2);
+    grid = glue_grid(rows, M::GROUPS * 2, PARTIAL_PER_SM);
     const size_t smem = (size_t)M::GROUPS * 3 * CC * sizeof(float);
     EVO_DISPATCH_T(xdt, TX, EVO_DISPATCH_T(dydt, TD, {
       auto k = ln_bwd_vec_kernel<CC, TX, TD>;
@@ -554,7 +559,7 @@ bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* m
   return true;
 }
 
-int64_t colsum_vec_ws(int64_t C) { return (int64_t)num_sms() * 2 * C * 4; }
+int64_t colsum_vec_ws(int64_t C) { return (int64_t)num_sms() * PARTIAL_PER_SM * C * 4; }
 
 // mode 0: plain colsum (+ optional cast copy y); mode 1: relu-backward in place
 bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, float* out,
@@ -563,8 +568,9 @@ bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, 
     return false;
   const int TPR = (int)(C / 8);
   if (TPR > GT) return false;
+  ws = partial_buffer(ws, colsum_vec_ws(C));
   const int RPB = GT / TPR;
-  unsigned grid = glue_grid(rows, RPB * 2);
+  unsigned grid = glue_grid(rows, RPB * 2, PARTIAL_PER_SM);
   const size_t smem = (size_t)RPB * C * sizeof(float);
   EVO_DISPATCH_T(xdt, TX, EVO_DISPATCH_T(ydt, TY, {
     if (mode == 1)
@@ -582,7 +588,7 @@ bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const f
                        int odt, int64_t rows, int64_t C, cudaStream_t s) {
   if ((C % 8) != 0 || !al16(y) || !al16(out) || (res && !al16(res))) return false;
   const int64_t n8 = rows * C / 8;
-  unsigned grid = glue_grid(n8, GT * 4);
+  unsigned grid = glue_grid(n8, GT * 2);
   EVO_DISPATCH_T(rdt, TR, EVO_DISPATCH_T(ydt, TY, EVO_DISPATCH_T(odt, TO, {
     bias_residual_vec_kernel<TR, TY, TO><<<grid, GT, 0, s>>>((const TR*)res, (const TY*)y, bias,
                                                              (TO*)out, n8, (int)(C / 8));
@@ -595,7 +601,7 @@ bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const f
 bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, cudaStream_t s) {
   if ((C % 8) != 0 || !al16(y)) return false;
   const int64_t n8 = rows * C / 8;
-  unsigned grid = glue_grid(n8, GT * 4);
+  unsigned grid = glue_grid(n8, GT * 2);
   EVO_DISPATCH_T(dt, T, {
     bias_relu_vec_kernel<T><<<grid, GT, 0, s>>>((T*)y, bias, n8, (int)(C / 8));
   });
@@ -611,7 +617,7 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
       using M = RowMap<CC>;
-      unsigned grid = glue_grid(R * R, M::GROUPS * 4);
+      unsigned grid = glue_grid(R * R, M::GROUPS * 4, 2);  // weights live in registers: few blocks
       EVO_DISPATCH_T(dt, T, {
         pair_bias_fwd_vec_kernel<CC, T><<<grid, GT, 0, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd,
                                                             R, (int)H, swap);
@@ -625,18 +631,21 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
   return true;
 }
 
-int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) { return (int64_t)num_sms() * 2 * (C * H + 2 * C) * 4; }
+int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) {
+  return (int64_t)num_sms() * PARTIAL_PER_SM * (C * H + 2 * C) * 4;
+}
 
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
                        float* dg, float* db, float* dw, int accumulate, void* ws, int64_t R,
                        int64_t C, int64_t H, cudaStream_t s) {
   if (!pow2_width(C) || C > 256 || H > 8 || H > C / 8 || !al16(z) || !al16(dz)) return false;
+  ws = partial_buffer(ws, pair_bias_bwd_vec_ws(C, H));
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
       using M = RowMap<CC>;
-      grid = glue_grid(R * R, M::GROUPS * 2);
+      grid = glue_grid(R * R, M::GROUPS * 2, PARTIAL_PER_SM);
       const int W = (int)(CC * H + 2 * CC);
       const size_t smem = ((size_t)CC * 8 + (size_t)M::GROUPS * W) * sizeof(float);
       EVO_DISPATCH_T(dt, T, {

@@ -148,6 +148,7 @@ int evo_opm_proj_bwd(const void* da, const void* dc, const float* mask, void* d_
   EVO_API_BEGIN
   cudaStream_t s = (cudaStream_t)stream;
   unsigned g = partial_grid(SR);
+  ws = partial_buffer(ws, (size_t)g * 2 * k * 4);
   int bs = (int)((2 * k + 31) / 32 * 32);
   if (bs > 256) bs = 256;
   EVO_DISPATCH_T(dtype, T, {

@@ -84,12 +84,20 @@ class DeviceFeatures:
 
 
 class BlockEngine:
-    def __init__(self, cfg: ModelConfig, store: FusionEngine, act_dtype=torch.bfloat16):
+    def __init__(self, cfg: ModelConfig, store: FusionEngine, act_dtype=torch.bfloat16,
+                 arena_mb: int = 96):
         cfg.validate()
         self.cfg = cfg
         self.st = store
         self.dt = act_dtype
         self.var = variants(cfg)
+        # partial rows of the deferred bias / LN-affine reductions of one block backward
+        self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
+
+    def deferred(self):
+        """Batch the ~40 small parameter-gradient reductions of a block backward
+        into one finalisation launch."""
+        return ops.deferred_reductions(self.arena)
 
     # -- parameter access ---------------------------------------------------------
 
@@ -412,7 +420,9 @@ class BlockEngine:
             saved.append(sv)
         loss, d_msa, d_pair = self.loss(msa, pair)
         for i in reversed(range(self.cfg.n_blocks)):
-            self.block_bwd(i, d_msa, d_pair, saved[i], feats)
+            with self.deferred():
+                self.block_bwd(i, d_msa, d_pair, saved[i], feats)
             saved[i] = None
-        self.embed_bwd(d_msa, d_pair, feats, rec)
+        with self.deferred():
+            self.embed_bwd(d_msa, d_pair, feats, rec)
         return loss, (msa, pair)

@@ -31,6 +31,22 @@ def _ws(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
 
 
+class deferred_reductions:
+    """Context manager: batch the finalisation of every column reduction
+    issued inside into one launch at exit (evo_defer_begin / evo_defer_end)."""
+
+    def __init__(self, arena: torch.Tensor):
+        self.arena = arena
+
+    def __enter__(self):
+        call("evo_defer_begin", ptr(self.arena), self.arena.numel() * self.arena.element_size())
+        return self
+
+    def __exit__(self, *exc):
+        call("evo_defer_end", stream())
+        return False
+
+
 # ---------------------------------------------------------------------------
 # GEMM
 

@@ -194,27 +194,50 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
 
     for c in (bp, world):
         c.phase = "bwd"
+    deferred = getattr(engine, "deferred", None)
     for i in reversed(range(n_blocks)):
-        if me == 0:
-            so, sm = saved[i]
-            b_contrib = engine.zeros_like(d_pair)
-            engine.msa_branch_bwd(i, d_msa, b_contrib, sm, feats)   # d_msa -> d(msa_in) part
-            s = b_contrib.clone()
-            bp.allreduce_sum(s, "pair_stack")
-            d_opm = s - b_contrib                                   # src/harness.py:505
-            dxl = engine.opm_bwd_core(d_opm, so, f"block{i}.opm", feats)
-            engine.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)
-            d_pair = s
-        else:
-            engine.pair_branch_bwd(i, d_pair, saved[i], feats)     # d_pair -> d(pair_mid)
-            bp.allreduce_sum(d_pair, "pair_stack")
+        ctx = deferred() if deferred is not None else _NullCtx()
+        with ctx:
+            _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair)
+            if me == 0:
+                d_pair = saved[i]  # the all-reduced d(pair_in), see _bp_block_bwd
         saved[i] = None
     # embeddings: each worker closes out its own branch (src/harness.py:518-522)
     if me == 0:
         engine.embed_bwd(d_msa, engine.zeros_like(d_pair), feats, rec, which="msa")
     else:
         engine.embed_bwd(engine.zeros_like(d_msa), d_pair, feats, rec, which="pair")
+    return _bp_close(engine, bp, world, grid, me, d_msa, loss)
 
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair):
+    """Block i backward on this BP rank (src/harness.py:497-516).  Rank 0
+    leaves the all-reduced d(pair_in) in saved[i] (its input d_pair is not
+    updated in place); rank 1 updates d_pair in place."""
+    if me == 0:
+        so, sm = saved[i]
+        b_contrib = engine.zeros_like(d_pair)
+        engine.msa_branch_bwd(i, d_msa, b_contrib, sm, feats)       # d_msa -> d(msa_in) part
+        s = b_contrib.clone()
+        bp.allreduce_sum(s, "pair_stack")
+        d_opm = s - b_contrib                                       # src/harness.py:505
+        dxl = engine.opm_bwd_core(d_opm, so, f"block{i}.opm", feats)
+        engine.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)
+        saved[i] = s
+    else:
+        engine.pair_branch_bwd(i, d_pair, saved[i], feats)         # d_pair -> d(pair_mid)
+        bp.allreduce_sum(d_pair, "pair_stack")
+
+
+def _bp_close(engine, bp, world, grid, me, d_msa, loss):
     for c in (bp, world):
         c.phase = "grad-sync"
     closing = d_msa if me == 0 else engine.empty_like(d_msa)
