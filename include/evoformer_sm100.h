@@ -111,6 +111,13 @@ int64_t evo_colsum_workspace(int64_t C);
 int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate,
                     void* y, int y_dtype, void* ws, int64_t rows, int64_t C, void* stream);
 int evo_cast(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, void* stream);
+/* Column-block packing for the merged Q|K|V|G projection (src/attention.py:
+ * 133-141 concatenates Wq|Wk|Wv the same way): unpack=0 packs, for each of the
+ * n groups, four [C, N] matrices src[4*i + s] into dst[i] = [C, 4N]; unpack=1
+ * splits src[i] = [C, 4N] into dst[4*i + s].  Pointer/size arrays are host
+ * memory; one launch per 64 groups. */
+int evo_pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N,
+                  int n, int src_dtype, int dst_dtype, int unpack, void* stream);
 /* in-place y *= s (fp32) */
 int evo_scale_inplace(float* y, float s, int64_t n, void* stream);
 

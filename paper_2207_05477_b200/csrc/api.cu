@@ -65,6 +65,8 @@ bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, 
 bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const float* bias, void* out,
                        int odt, int64_t rows, int64_t C, cudaStream_t s);
 bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, cudaStream_t s);
+void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N, int n,
+               int sdt, int ddt, int unpack, cudaStream_t s);
 
 // tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
@@ -198,6 +200,15 @@ int evo_defer_end(void* stream) {
 }
 
 size_t evo_defer_used(void) { return defer_state().used; }
+
+int evo_pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N,
+                  int n, int src_dtype, int dst_dtype, int unpack, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(n >= 0 && src && dst && C && N, EVO_ERR_ARG, "pack_cols: bad arguments");
+  if (n == 0) return EVO_OK;
+  pack_cols(src, dst, C, N, n, src_dtype, dst_dtype, unpack, (cudaStream_t)stream);
+  EVO_API_END
+}
 
 int evo_device_check(int* sm_major, int* sm_minor, int* nsm) {
   EVO_API_BEGIN

@@ -9,6 +9,8 @@
 // These kernels serve the storage dtypes of the engine (bf16 or fp32 rows)
 // whenever C is a power of two in [32, 1024]; other widths use the scalar
 // kernels in layernorm.cu / api.cu / pair_bias.cu / opm.cu.
+#include <algorithm>
+
 #include "common.cuh"
 #include "reduce.cuh"
 #include "vec.cuh"
@@ -473,6 +475,38 @@ __global__ void __launch_bounds__(GT) opm_relayout_kernel(const TI* __restrict__
   }
 }
 
+// ---------------------------------------------------------------------------
+// column-block packing of the four attention projections:
+//   pack:   dst[c, s*N + j] = src_s[c*N + j]          (Wq|Wk|Wv|Wg -> [C, 4N])
+//   unpack: dst_s[c*N + j]  = src[c, s*N + j]          ([C, 4N] grad -> 4 slots)
+// one launch handles up to PACK_MAX matrices (descriptor table as a parameter)
+
+constexpr int PACK_MAX = 64;
+struct PackDesc {
+  const void* src[4];
+  void* dst[4];
+  int64_t C, N;
+};
+struct PackBatch {
+  int n, dtype_src, dtype_dst, unpack;
+  PackDesc d[PACK_MAX];
+};
+
+template <typename TS, typename TD>
+__global__ void __launch_bounds__(GT) pack_cols_kernel(const __grid_constant__ PackBatch pb) {
+  const PackDesc& d = pb.d[blockIdx.y];
+  const int64_t n = d.C * 4 * d.N;
+  for (int64_t e = blockIdx.x * (int64_t)GT + threadIdx.x; e < n; e += (int64_t)gridDim.x * GT) {
+    const int64_t c = e / (4 * d.N), r = e % (4 * d.N);
+    const int s = (int)(r / d.N);
+    const int64_t j = r % d.N;
+    if (!pb.unpack)
+      reinterpret_cast<TD*>(d.dst[0])[e] = from_f<TD>(to_f(reinterpret_cast<const TS*>(d.src[s])[c * d.N + j]));
+    else
+      reinterpret_cast<TD*>(d.dst[s])[c * d.N + j] = from_f<TD>(to_f(reinterpret_cast<const TS*>(d.src[0])[e]));
+  }
+}
+
 // rec[i, j] = 1 / (sum_s m[s, i] m[s, j] + 1e-3)   (block per i; exact integer sums)
 __global__ void __launch_bounds__(GT) opm_rec_vec_kernel(const float* __restrict__ mask,
                                                          float* __restrict__ rec, int64_t S, int64_t R) {
@@ -513,6 +547,32 @@ void ln_fwd_dispatch_y(const void* x, const float* g, const float* b, void* y, i
 inline bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 }  // namespace
+
+void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N, int n,
+               int sdt, int ddt, int unpack, cudaStream_t s) {
+  for (int i0 = 0; i0 < n; i0 += PACK_MAX) {
+    PackBatch pb{};
+    pb.n = n - i0 < PACK_MAX ? n - i0 : PACK_MAX;
+    pb.dtype_src = sdt;
+    pb.dtype_dst = ddt;
+    pb.unpack = unpack;
+    int64_t maxe = 0;
+    for (int k = 0; k < pb.n; ++k) {
+      const int i = i0 + k;
+      for (int q = 0; q < 4; ++q) {
+        pb.d[k].src[q] = unpack ? src[i] : src[4 * i + q];
+        pb.d[k].dst[q] = unpack ? dst[4 * i + q] : dst[i];
+      }
+      pb.d[k].C = C[i];
+      pb.d[k].N = N[i];
+      maxe = std::max<int64_t>(maxe, C[i] * 4 * N[i]);
+    }
+    dim3 grid((unsigned)std::min<int64_t>((maxe + GT - 1) / GT, 1024), (unsigned)pb.n);
+    EVO_DISPATCH_T(sdt, TS, EVO_DISPATCH_T(ddt, TD, { pack_cols_kernel<TS, TD><<<grid, GT, 0, s>>>(pb); }));
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+  }
+}
 
 // ============================================================================
 // entry points used by the C ABI wrappers (return false -> scalar fallback)

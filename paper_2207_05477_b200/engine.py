@@ -93,6 +93,29 @@ class BlockEngine:
         self.var = variants(cfg)
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
+        # merged Q|K|V|G projection weights [C, 4*H*c] per attention module (the
+        # reference concatenates Wq|Wk|Wv the same way, src/attention.py:133-141),
+        # refreshed from the (bf16 shadow of the) pooled params every step
+        self.wcat = {}
+        srcs, dsts, Cs, Ns = [], [], [], []
+        for i in range(cfg.n_blocks):
+            for mod, C in (("row_attn", cfg.c_m), ("col_attn", cfg.c_m), ("tri_start", cfg.c_z),
+                           ("tri_end", cfg.c_z)):
+                p = f"block{i}.{mod}"
+                buf = torch.empty((C, 4 * C), dtype=act_dtype, device=store.device)
+                self.wcat[p] = buf
+                srcs += [store.weight(f"{p}.attn.{f}") for f in ("wq", "wk", "wv", "wg")]
+                dsts.append(buf)
+                Cs.append(C)
+                Ns.append(C)
+        wdt = ops.dcode(store.weight(f"block0.row_attn.attn.wq")) if cfg.n_blocks else 0
+        self._pack = ops.PackPlan(srcs, dsts, Cs, Ns, False, wdt, ops.dcode(torch.empty(0, dtype=act_dtype)))
+        self.refresh_weights()
+
+    def refresh_weights(self):
+        """Re-pack the merged projection weights after an optimizer step."""
+        if self._pack.n:
+            self._pack.run()
 
     def deferred(self):
         """Batch the ~40 small parameter-gradient reductions of a block backward
@@ -134,8 +157,7 @@ class BlockEngine:
                                              self.P(f"{prefix}.bias_ln_b"),
                                              self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.swap_xy)
         qkvg = torch.empty((T, 4 * HD), dtype=dt, device=x.device)
-        for s, f in enumerate(("wq", "wk", "wv", "wg")):
-            ops.gemm(xl, self.W(f"{prefix}.attn.{f}", C), qkvg[:, s * HD:(s + 1) * HD])
+        ops.gemm(xl, self.wcat[prefix], qkvg)                         # one merged projection
         mask = self.mask(feats, v.mask)
         ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, v.msb, v.msl, nb,
                                              self.P(f"{prefix}.attn.bg"), v.B, v.L, H, D, v.sb, v.sl)
@@ -168,13 +190,13 @@ class BlockEngine:
                                   v.sb, v.sl, want_dbias=v.bias)
         del dgated
         xl = sv["xl"]
-        for s, f in enumerate(("wq", "wk", "wv", "wg")):
-            ops.gemm(xl, dqkvg[:, s * HD:(s + 1) * HD], self.Gm(f"{prefix}.attn.{f}", C), ta=True)
+        dwcat = torch.empty((C, 4 * HD), dtype=F32, device=d.device)
+        ops.gemm(xl, dqkvg, dwcat, ta=True)                           # d[Wq|Wk|Wv|Wg] in one GEMM
+        ops.PackPlan([dwcat], [self.Gm(f"{prefix}.attn.{f}", C) for f in ("wq", "wk", "wv", "wg")],
+                     [C], [HD], True, ops.F32, ops.F32).run()
         dxl = torch.empty((T, C), dtype=F32, device=d.device)
-        for s, f in enumerate(("wq", "wk", "wv", "wg")):
-            ops.gemm(dqkvg[:, s * HD:(s + 1) * HD], self.W(f"{prefix}.attn.{f}", C), dxl, tb=True,
-                     beta=0.0 if s == 0 else 1.0)
-        del dqkvg
+        ops.gemm(dqkvg, self.wcat[prefix], dxl, tb=True)
+        del dqkvg, dwcat
         ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d, d,
                           self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
         if v.bias:
@@ -409,6 +431,7 @@ class BlockEngine:
         """``_serial_grads`` (src/harness.py:327-352): n-1 untaped recycling
         passes, one differentiated pass; grads land in the pooled region.
         Returns (loss device tensor [1], (msa, pair))."""
+        self.refresh_weights()
         self.st.zero_grads()
         prev = None
         for _ in range(max(0, n_cycles - 1)):

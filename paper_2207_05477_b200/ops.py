@@ -115,6 +115,26 @@ def colsum_cast(x, out, y=None, accumulate=False):
          dcode(y) if y is not None else F32, ptr(ws), rows, C, stream())
 
 
+class PackPlan:
+    """Host-side pointer tables for evo_pack_cols (built once: the pooled
+    parameter storage and the packed buffers never move)."""
+
+    def __init__(self, srcs, dsts, Cs, Ns, unpack, sdt, ddt):
+        import ctypes
+        P = ctypes.c_void_p
+        self.src = (P * len(srcs))(*[t.data_ptr() for t in srcs])
+        self.dst = (P * len(dsts))(*[t.data_ptr() for t in dsts])
+        self.C = (ctypes.c_int64 * len(Cs))(*Cs)
+        self.N = (ctypes.c_int64 * len(Ns))(*Ns)
+        self.n = len(Cs)
+        self.unpack, self.sdt, self.ddt = int(unpack), sdt, ddt
+        self.keep = (srcs, dsts)
+
+    def run(self):
+        call("evo_pack_cols", self.src, self.dst, self.C, self.N, self.n, self.sdt, self.ddt,
+             self.unpack, stream())
+
+
 def cast(x, y):
     call("evo_cast", ptr(x), dcode(x), ptr(y), dcode(y), x.numel(), stream())
     return y

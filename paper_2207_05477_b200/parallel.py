@@ -165,6 +165,9 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
     for c in (bp, world):
         c.step = step
         c.phase = "fwd"
+    refresh = getattr(engine, "refresh_weights", None)
+    if refresh is not None:
+        refresh()
     engine.zero_grads()
     prev = None
     for _ in range(max(0, n_cycles - 1)):  # replicated recycling warm-up, no comm (:406-415)
