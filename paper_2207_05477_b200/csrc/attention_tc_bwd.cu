@@ -175,7 +175,10 @@ __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const b
     }
   }
   for (int j = tid; j < LP; j += 512)
-    sMb[j] = j < L ? (mask[b * g.msb + (int64_t)j * g.msl] - 1.0f) * 1e9f : -INFINITY;
+    if (j < L)
+      tc::cp_async4(sMb + j, mask + b * g.msb + (int64_t)j * g.msl);  // converted by mask_to_bias
+    else
+      sMb[j] = -INFINITY;
 }
 
 template <int D, int LP, bool BIAS>
@@ -249,6 +252,8 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
     const float m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
     const float rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
     const float Dv = valid ? Dvec[g.tok(b, i) * g.H + h] : 0.f;
+    tc::mask_to_bias(const_cast<float*>(sMb), LP, L, tid, 512);
+    __syncthreads();
 
 #pragma unroll 1
     for (int kc = 0; kc < NKC; ++kc) {

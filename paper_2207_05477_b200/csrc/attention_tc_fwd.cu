@@ -99,7 +99,10 @@ __device__ __forceinline__ void fwd_stage(uint8_t* st, const bf16* qkvg, const f
     }
   }
   for (int j = tid; j < LP; j += 256)
-    sMb[j] = j < L ? (mask[b * g.msb + (int64_t)j * g.msl] - 1.0f) * 1e9f : -INFINITY;
+    if (j < L)
+      tc::cp_async4(sMb + j, mask + b * g.msb + (int64_t)j * g.msl);  // converted by mask_to_bias
+    else
+      sMb[j] = -INFINITY;
 }
 
 template <int LP>
@@ -183,6 +186,8 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
       }
       tc::mma_commit(bar);
     }
+    tc::mask_to_bias(const_cast<float*>(sMb), LP, L, tid, 256);
+    __syncthreads();
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after();

@@ -165,6 +165,16 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+// staged raw key-mask m in smem -> additive mask bias (m - 1) * 1e9 in place
+// (src/attention.py:151); keys beyond L were staged as -inf and stay so
+__device__ __forceinline__ void mask_to_bias(float* sMb, int LP, int L, int tid, int nthreads) {
+  for (int j = tid; j < LP; j += nthreads)
+    if (j < L) sMb[j] = (sMb[j] - 1.0f) * 1e9f;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
