@@ -110,6 +110,11 @@ int evo_relu_bwd_colsum(void* dh, const void* h, int dtype, float* db, int accum
 int64_t evo_colsum_workspace(int64_t C);
 int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate,
                     void* y, int y_dtype, void* ws, int64_t rows, int64_t C, void* stream);
+/* Column sums of a row-strided [rows, C] view (leading dimension ld >= C):
+ * bias gradients of column slices of a merged projection (the
+ * `reduce_sum(dy, axis=0)` of src/attention.py:187 applied per slice). */
+int evo_colsum_strided(const void* x, int x_dtype, int64_t ld, float* out, int accumulate, void* ws,
+                       int64_t rows, int64_t C, void* stream);
 int evo_cast(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, void* stream);
 /* Column-block packing for the merged Q|K|V|G projection (src/attention.py:
  * 133-141 concatenates Wq|Wk|Wv the same way): unpack=0 packs, for each of the
@@ -200,6 +205,30 @@ int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema,
                       void* p_bf16, int64_t n, const double* sumsq, double clip,
                       float lr, float b1, float omb1, float b2, float omb2, float eps,
                       float bc1, float bc2, float decay, float omdecay, void* stream);
+
+/* ---- triangle multiplication (extension; AF2 Supplementary Alg. 11/12) -----
+ * Absent from the reference (planner inventory only, src/planner.py:37-45).
+ * proj: [R*R, ld] token-major with column blocks [ap | ag | bp | bg] (width ch);
+ * a = sigmoid(ag + b_ag) * (ap + b_ap) * mask (b likewise) written
+ * channel-major [ch, R*R] for the channel-batched contractions (evo_gemm). */
+int evo_trimul_gate_fwd(const void* proj, int64_t ld, const float* b_ap, const float* b_ag,
+                        const float* b_bp, const float* b_bg, const float* mask, void* a_cm,
+                        void* b_cm, int64_t RR, int64_t ch, int dtype, void* stream);
+/* channel-major da, db -> token-major d(proj) [R*R, 4*ch] */
+int evo_trimul_gate_bwd(const void* proj, int64_t ld, const float* b_ap, const float* b_ag,
+                        const float* b_bp, const float* b_bg, const float* mask, const void* da_cm,
+                        const void* db_cm, void* dproj, int64_t RR, int64_t ch, int dtype,
+                        void* stream);
+/* y[c, r] = x[r, c] (tiled; dtype conversion allowed) */
+int evo_transpose2d(const void* x, int x_dtype, void* y, int y_dtype, int64_t rows, int64_t cols,
+                    void* stream);
+/* out = res + sigmoid(gp + bg) * (y + by), g_out = sigmoid(gp + bg); gp row stride ld_gp */
+int evo_gated_residual(const void* res, const void* gp, int64_t ld_gp, const float* bg, const void* y,
+                       const float* by, void* g_out, void* out, int64_t rows, int64_t C, int dtype,
+                       void* stream);
+/* dyb = dout*g, dgp = dout*(y+by)*g*(1-g) */
+int evo_gated_residual_bwd(const float* dout, const void* g, const void* y, const float* by, void* dyb,
+                           void* dgp, int64_t rows, int64_t C, int dtype, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,7 @@ SIGNATURES = {
     "evo_relu_bwd_colsum": (_i, [_p, _p, _i, _p, _i, _p, _i64, _i64, _p]),
     "evo_colsum_workspace": (_i64, [_i64]),
     "evo_colsum_cast": (_i, [_p, _i, _p, _i, _p, _i, _p, _i64, _i64, _p]),
+    "evo_colsum_strided": (_i, [_p, _i, _i64, _p, _i, _p, _i64, _i64, _p]),
     "evo_cast": (_i, [_p, _i, _p, _i, _i64, _p]),
     "evo_pack_cols": (_i, [ctypes.POINTER(_p), ctypes.POINTER(_p), ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64), _i, _i, _i, _i, _p]),
@@ -61,6 +62,11 @@ SIGNATURES = {
     "evo_opm_norm_bwd": (_i, [_p, _i, _p, _p, _i, _i64, _i64, _p]),
     "evo_sq_loss_workspace": (_i64, []),
     "evo_sq_loss": (_i, [_p, _i64, _p, _i64, _i, _f, _f, _p, _p, _p, _p, _p]),
+    "evo_trimul_gate_fwd": (_i, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i, _p]),
+    "evo_trimul_gate_bwd": (_i, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i, _p]),
+    "evo_transpose2d": (_i, [_p, _i, _p, _i, _i64, _i64, _p]),
+    "evo_gated_residual": (_i, [_p, _p, _i64, _p, _p, _p, _p, _p, _i64, _i64, _i, _p]),
+    "evo_gated_residual_bwd": (_i, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i, _p]),
     "evo_sumsq_workspace": (_i64, []),
     "evo_sumsq_f64": (_i, [_p, _i64, _p, _p, _p]),
     "evo_adam_clip_ema": (_i, [_p, _p, _p, _p, _p, _p, _i64, _p, _d, _f, _f, _f, _f, _f, _f,

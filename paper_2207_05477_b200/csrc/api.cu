@@ -308,6 +308,18 @@ int evo_colsum_cast(const void* x, int x_dtype, float* out, int accumulate, void
   EVO_API_END
 }
 
+int evo_colsum_strided(const void* x, int x_dtype, int64_t ld, float* out, int accumulate, void* ws,
+                       int64_t rows, int64_t C, void* stream) {
+  EVO_API_BEGIN
+  cudaStream_t s = (cudaStream_t)stream;
+  if (colsum_vec(const_cast<void*>(x), x_dtype, ld, nullptr, nullptr, x_dtype, out, accumulate, ws, rows, C,
+                 0, s))
+    return EVO_OK;
+  EVO_REQUIRE(ld == C, EVO_ERR_UNSUPPORTED, "colsum_strided: strided rows need 16-B aligned power-of-two widths");
+  return evo_colsum_cast(x, x_dtype, out, accumulate, nullptr, x_dtype, ws, rows, C, stream);
+  EVO_API_END
+}
+
 int evo_relu_bwd_colsum(void* dh, const void* h, int dtype, float* db, int accumulate, void* ws,
                         int64_t rows, int64_t C, void* stream) {
   EVO_API_BEGIN

@@ -1,0 +1,210 @@
+// Triangle multiplicative update glue (AlphaFold2 Supplementary Alg. 11/12;
+// absent from the reference, which lists it only as planner inventory,
+// src/planner.py:37-45).  The two contractions o[c] = a[c] b[c]^T (outgoing)
+// / a[c]^T b[c] (incoming) are channel-batched [R x R] GEMMs (evo_gemm,
+// batched); these kernels produce and consume their channel-major operands:
+//   gate_fwd   a = sigmoid(ag + bag) * (ap + bap) * mask, b likewise,
+//              token-major projections -> channel-major [ch, R*R]
+//   gate_bwd   channel-major da/db -> token-major d(projections)
+//   transpose  [rows, cols] <-> [cols, rows] (smem tiled, coalesced both ways)
+//   gated residual  out = z + sigmoid(gp + bg) * (y + by) and its backward
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace evo {
+
+namespace {
+
+constexpr int TT = 32;  // tile edge
+
+__device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+// proj: [RR, ld] with column blocks [ap | ag | bp | bg] of width ch
+template <typename T>
+__global__ void __launch_bounds__(256) trimul_gate_fwd_kernel(
+    const T* __restrict__ proj, int64_t ld, const float* __restrict__ bap, const float* __restrict__ bag,
+    const float* __restrict__ bbp, const float* __restrict__ bbg, const float* __restrict__ mask,
+    T* __restrict__ a_cm, T* __restrict__ b_cm, int64_t RR, int ch) {
+  __shared__ float ta[TT][TT + 1], tb[TT][TT + 1];
+  const int64_t t0 = (int64_t)blockIdx.x * TT;
+  const int c0 = blockIdx.y * TT;
+  const int tx = threadIdx.x % TT, ty = threadIdx.x / TT;  // 32 x 8
+  for (int r = ty; r < TT; r += 8) {
+    const int64_t t = t0 + r;
+    const int c = c0 + tx;
+    float av = 0.f, bv = 0.f;
+    if (t < RR && c < ch) {
+      const T* row = proj + t * ld;
+      const float m = mask[t];
+      av = sigm(to_f(row[ch + c]) + bag[c]) * (to_f(row[c]) + bap[c]) * m;
+      bv = sigm(to_f(row[3 * ch + c]) + bbg[c]) * (to_f(row[2 * ch + c]) + bbp[c]) * m;
+    }
+    ta[r][tx] = av;
+    tb[r][tx] = bv;
+  }
+  __syncthreads();
+  for (int r = ty; r < TT; r += 8) {
+    const int c = c0 + r;
+    const int64_t t = t0 + tx;
+    if (c < ch && t < RR) {
+      a_cm[(int64_t)c * RR + t] = from_f<T>(ta[tx][r]);
+      b_cm[(int64_t)c * RR + t] = from_f<T>(tb[tx][r]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) trimul_gate_bwd_kernel(
+    const T* __restrict__ proj, int64_t ld, const float* __restrict__ bap, const float* __restrict__ bag,
+    const float* __restrict__ bbp, const float* __restrict__ bbg, const float* __restrict__ mask,
+    const T* __restrict__ da_cm, const T* __restrict__ db_cm, T* __restrict__ dproj, int64_t RR, int ch) {
+  __shared__ float ta[TT][TT + 1], tb[TT][TT + 1];
+  const int64_t t0 = (int64_t)blockIdx.x * TT;
+  const int c0 = blockIdx.y * TT;
+  const int tx = threadIdx.x % TT, ty = threadIdx.x / TT;
+  for (int r = ty; r < TT; r += 8) {  // read channel-major rows (coalesced along t)
+    const int c = c0 + r;
+    const int64_t t = t0 + tx;
+    ta[r][tx] = (c < ch && t < RR) ? to_f(da_cm[(int64_t)c * RR + t]) : 0.f;
+    tb[r][tx] = (c < ch && t < RR) ? to_f(db_cm[(int64_t)c * RR + t]) : 0.f;
+  }
+  __syncthreads();
+  for (int r = ty; r < TT; r += 8) {  // write token-major rows (coalesced along c)
+    const int64_t t = t0 + r;
+    const int c = c0 + tx;
+    if (t < RR && c < ch) {
+      const T* row = proj + t * ld;
+      T* drow = dproj + t * 4 * ch;
+      const float m = mask[t];
+      const float da = ta[tx][r] * m, db = tb[tx][r] * m;
+      const float ap = to_f(row[c]) + bap[c], sa = sigm(to_f(row[ch + c]) + bag[c]);
+      const float bp = to_f(row[2 * ch + c]) + bbp[c], sb = sigm(to_f(row[3 * ch + c]) + bbg[c]);
+      drow[c] = from_f<T>(da * sa);
+      drow[ch + c] = from_f<T>(da * ap * sa * (1.0f - sa));
+      drow[2 * ch + c] = from_f<T>(db * sb);
+      drow[3 * ch + c] = from_f<T>(db * bp * sb * (1.0f - sb));
+    }
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) transpose_kernel(const TI* __restrict__ x, TO* __restrict__ y,
+                                                        int64_t rows, int64_t cols) {
+  __shared__ float t[TT][TT + 1];
+  const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
+  const int tx = threadIdx.x % TT, ty = threadIdx.x / TT;
+  for (int r = ty; r < TT; r += 8)
+    t[r][tx] = (r0 + r < rows && c0 + tx < cols) ? to_f(x[(r0 + r) * cols + c0 + tx]) : 0.f;
+  __syncthreads();
+  for (int r = ty; r < TT; r += 8)
+    if (c0 + r < cols && r0 + tx < rows) y[(c0 + r) * rows + r0 + tx] = from_f<TO>(t[tx][r]);
+}
+
+// out = res + sigmoid(gp + bg) * (y + by); g saved
+template <typename T>
+__global__ void gated_residual_kernel(const T* __restrict__ res, const T* __restrict__ gp, int64_t ld_gp,
+                                      const float* __restrict__ bg, const T* __restrict__ y,
+                                      const float* __restrict__ by, T* __restrict__ g_out,
+                                      T* __restrict__ out, int64_t rows, int64_t C) {
+  const int64_t n = rows * C;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / C, c = e % C;
+    const float gv = sigm(to_f(gp[r * ld_gp + c]) + bg[c]);
+    g_out[e] = from_f<T>(gv);
+    out[e] = from_f<T>(to_f(res[e]) + gv * (to_f(y[e]) + by[c]));
+  }
+}
+
+// dyb = dout * g ;  dgp = dout * (y + by) * g * (1 - g)
+template <typename T>
+__global__ void gated_residual_bwd_kernel(const float* __restrict__ dout, const T* __restrict__ g,
+                                          const T* __restrict__ y, const float* __restrict__ by,
+                                          T* __restrict__ dyb, T* __restrict__ dgp, int64_t rows, int64_t C) {
+  const int64_t n = rows * C;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e % C;
+    const float d = dout[e], gv = to_f(g[e]);
+    dyb[e] = from_f<T>(d * gv);
+    dgp[e] = from_f<T>(d * (to_f(y[e]) + by[c]) * gv * (1.0f - gv));
+  }
+}
+
+}  // namespace
+}  // namespace evo
+
+using namespace evo;
+
+extern "C" {
+
+int evo_trimul_gate_fwd(const void* proj, int64_t ld, const float* b_ap, const float* b_ag,
+                        const float* b_bp, const float* b_bg, const float* mask, void* a_cm,
+                        void* b_cm, int64_t RR, int64_t ch, int dtype, void* stream) {
+  EVO_API_BEGIN
+  dim3 grid(cdiv(RR, TT), cdiv(ch, TT));
+  EVO_DISPATCH_T(dtype, T, {
+    trimul_gate_fwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const T*)proj, ld, b_ap, b_ag, b_bp, b_bg, mask, (T*)a_cm, (T*)b_cm, RR, (int)ch);
+  });
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_trimul_gate_bwd(const void* proj, int64_t ld, const float* b_ap, const float* b_ag,
+                        const float* b_bp, const float* b_bg, const float* mask, const void* da_cm,
+                        const void* db_cm, void* dproj, int64_t RR, int64_t ch, int dtype,
+                        void* stream) {
+  EVO_API_BEGIN
+  dim3 grid(cdiv(RR, TT), cdiv(ch, TT));
+  EVO_DISPATCH_T(dtype, T, {
+    trimul_gate_bwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const T*)proj, ld, b_ap, b_ag, b_bp, b_bg, mask, (const T*)da_cm, (const T*)db_cm, (T*)dproj,
+        RR, (int)ch);
+  });
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_transpose2d(const void* x, int x_dtype, void* y, int y_dtype, int64_t rows, int64_t cols,
+                    void* stream) {
+  EVO_API_BEGIN
+  dim3 grid(cdiv(cols, TT), cdiv(rows, TT));
+  EVO_DISPATCH_T(x_dtype, TI, EVO_DISPATCH_T(y_dtype, TO, {
+    transpose_kernel<TI, TO><<<grid, 256, 0, (cudaStream_t)stream>>>((const TI*)x, (TO*)y, rows, cols);
+  }));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_gated_residual(const void* res, const void* gp, int64_t ld_gp, const float* bg, const void* y,
+                       const float* by, void* g_out, void* out, int64_t rows, int64_t C, int dtype,
+                       void* stream) {
+  EVO_API_BEGIN
+  const int64_t n = rows * C;
+  const unsigned grid = (unsigned)imin64((n + 255) / 256, (int64_t)num_sms() * 16);
+  EVO_DISPATCH_T(dtype, T, {
+    gated_residual_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const T*)res, (const T*)gp, ld_gp, bg, (const T*)y, by, (T*)g_out, (T*)out, rows, C);
+  });
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+int evo_gated_residual_bwd(const float* dout, const void* g, const void* y, const float* by, void* dyb,
+                           void* dgp, int64_t rows, int64_t C, int dtype, void* stream) {
+  EVO_API_BEGIN
+  const int64_t n = rows * C;
+  const unsigned grid = (unsigned)imin64((n + 255) / 256, (int64_t)num_sms() * 16);
+  EVO_DISPATCH_T(dtype, T, {
+    gated_residual_bwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        dout, (const T*)g, (const T*)y, by, (T*)dyb, (T*)dgp, rows, C);
+  });
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  EVO_API_END
+}
+
+}  // extern "C"

@@ -108,6 +108,17 @@ class BlockEngine:
                 dsts.append(buf)
                 Cs.append(C)
                 Ns.append(C)
+        if cfg.trimul:  # [ap | ag | bp | bg] projections of TriangleMultiplication
+            ch = cfg.c_hidden_mul
+            for i in range(cfg.n_blocks):
+                for mod in ("tri_mul_out", "tri_mul_in"):
+                    p = f"block{i}.{mod}"
+                    buf = torch.empty((cfg.c_z, 4 * ch), dtype=act_dtype, device=store.device)
+                    self.wcat[p] = buf
+                    srcs += [store.weight(f"{p}.w_{nm}") for nm in ("ap", "ag", "bp", "bg")]
+                    dsts.append(buf)
+                    Cs.append(cfg.c_z)
+                    Ns.append(ch)
         wdt = ops.dcode(store.weight(f"block0.row_attn.attn.wq")) if cfg.n_blocks else 0
         self._pack = ops.PackPlan(srcs, dsts, Cs, Ns, False, wdt, ops.dcode(torch.empty(0, dtype=act_dtype)))
         self.refresh_weights()
@@ -301,6 +312,84 @@ class BlockEngine:
         ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d_msa, d_msa,
                           self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
 
+    # -- TriangleMultiplication (extension; AF2 Alg 11 outgoing / Alg 12 incoming) ---
+
+    def trimul_fwd(self, x, prefix, feats, outgoing: bool):
+        cfg, dt = self.cfg, self.dt
+        RR, Cz = x.shape
+        R, ch = cfg.n_res, cfg.c_hidden_mul
+        P = self.P
+        zl, mu, rs = ops.layernorm(x, P(f"{prefix}.ln_in_g"), P(f"{prefix}.ln_in_b"), dt)
+        proj = torch.empty((RR, 4 * ch), dtype=dt, device=x.device)
+        ops.gemm(zl, self.wcat[prefix], proj)
+        gp = torch.empty((RR, Cz), dtype=dt, device=x.device)
+        ops.gemm(zl, self.W(f"{prefix}.w_g", Cz), gp)
+        biases = [P(f"{prefix}.b_{nm}") for nm in ("ap", "ag", "bp", "bg")]
+        a_cm, b_cm = ops.trimul_gate_fwd(proj, biases, feats.pair_mask, ch)
+        o_cm = torch.empty((ch, RR), dtype=dt, device=x.device)
+        A0, B0, O0 = a_cm[0].view(R, R), b_cm[0].view(R, R), o_cm[0].view(R, R)
+        if outgoing:   # o_ij = sum_k a_ik b_jk
+            ops.gemm_batched(A0, B0, O0, ch, RR, RR, RR, tb=True)
+        else:          # o_ij = sum_k a_ki b_kj
+            ops.gemm_batched(A0, B0, O0, ch, RR, RR, RR, ta=True)
+        o = ops.transpose2d(o_cm)                                   # [RR, ch]
+        del o_cm
+        ol, mu2, rs2 = ops.layernorm(o, P(f"{prefix}.ln_out_g"), P(f"{prefix}.ln_out_b"), dt)
+        y = torch.empty((RR, Cz), dtype=dt, device=x.device)
+        ops.gemm(ol, self.W(f"{prefix}.w_o", ch), y)
+        g, out = ops.gated_residual(x, gp, P(f"{prefix}.b_g"), y, P(f"{prefix}.b_o"))
+        return out, dict(x=x, zl=zl, mu=mu, rs=rs, proj=proj, a=a_cm, b=b_cm, o=o, mu2=mu2, rs2=rs2,
+                         ol=ol, y=y, g=g, outgoing=outgoing)
+
+    def trimul_bwd(self, d, sv, prefix, feats):
+        cfg, dt = self.cfg, self.dt
+        RR, Cz = d.shape
+        R, ch = cfg.n_res, cfg.c_hidden_mul
+        P, G = self.P, self.G
+        dyb, dgp = ops.gated_residual_bwd(d, sv["g"], sv["y"], P(f"{prefix}.b_o"))
+        ops.colsum_cast(dyb, G(f"{prefix}.b_o"))
+        ops.colsum_cast(dgp, G(f"{prefix}.b_g"))
+        ops.gemm(sv["ol"], dyb, self.Gm(f"{prefix}.w_o", ch), ta=True)
+        dol = torch.empty((RR, ch), dtype=F32, device=d.device)
+        ops.gemm(dyb, self.W(f"{prefix}.w_o", ch), dol, tb=True)
+        del dyb
+        do = torch.empty((RR, ch), dtype=F32, device=d.device)
+        ops.layernorm_bwd(sv["o"], dol, sv["mu2"], sv["rs2"], P(f"{prefix}.ln_out_g"), None, do,
+                          G(f"{prefix}.ln_out_g"), G(f"{prefix}.ln_out_b"))
+        del dol
+        do_cm = ops.transpose2d(do, dt)                              # [ch, RR]
+        del do
+        a_cm, b_cm = sv["a"], sv["b"]
+        da = torch.empty_like(a_cm)
+        db = torch.empty_like(b_cm)
+        D0, A0, B0 = do_cm[0].view(R, R), a_cm[0].view(R, R), b_cm[0].view(R, R)
+        dA0, dB0 = da[0].view(R, R), db[0].view(R, R)
+        if sv["outgoing"]:   # o = a b^T: da = do b, db = do^T a
+            ops.gemm_batched(D0, B0, dA0, ch, RR, RR, RR)
+            ops.gemm_batched(D0, A0, dB0, ch, RR, RR, RR, ta=True)
+        else:                # o = a^T b: da = b do^T, db = a do
+            ops.gemm_batched(B0, D0, dA0, ch, RR, RR, RR, tb=True)
+            ops.gemm_batched(A0, D0, dB0, ch, RR, RR, RR)
+        del do_cm
+        biases = [P(f"{prefix}.b_{nm}") for nm in ("ap", "ag", "bp", "bg")]
+        dproj = ops.trimul_gate_bwd(sv["proj"], biases, feats.pair_mask, da, db, ch)
+        del da, db
+        # per-slice column sums straight into the grad slots (these may be
+        # deferred reductions, so nothing here may read their output)
+        for s, nm in enumerate(("ap", "ag", "bp", "bg")):
+            ops.colsum_strided(dproj[:, s * ch:(s + 1) * ch], G(f"{prefix}.b_{nm}"), accumulate=True)
+        zl = sv["zl"]
+        dw4 = torch.empty((Cz, 4 * ch), dtype=F32, device=d.device)
+        ops.gemm(zl, dproj, dw4, ta=True)
+        ops.PackPlan([dw4], [self.Gm(f"{prefix}.w_{nm}", Cz) for nm in ("ap", "ag", "bp", "bg")],
+                     [Cz], [ch], True, ops.F32, ops.F32).run()
+        ops.gemm(zl, dgp, self.Gm(f"{prefix}.w_g", Cz), ta=True)
+        dzl = torch.empty((RR, Cz), dtype=F32, device=d.device)
+        ops.gemm(dproj, self.wcat[prefix], dzl, tb=True)
+        ops.gemm(dgp, self.W(f"{prefix}.w_g", Cz), dzl, tb=True, beta=1.0)
+        ops.layernorm_bwd(sv["x"], dzl, sv["mu"], sv["rs"], P(f"{prefix}.ln_in_g"), d, d,
+                          G(f"{prefix}.ln_in_g"), G(f"{prefix}.ln_in_b"))
+
     # -- branches (the split used by branch parallelism, src/harness.py:447-486) ----
 
     def msa_branch_fwd(self, i, msa_in, pair_in, feats):
@@ -321,18 +410,27 @@ class BlockEngine:
 
     def pair_branch_fwd(self, i, pair_mid, feats):
         p = f"block{i}"
-        pair, s1 = self.attn_fwd(pair_mid, f"{p}.tri_start", self.var["tri_start"], feats)
+        pair, tm = pair_mid, []
+        if self.cfg.trimul:  # extension, after pair += OPM (SURVEY A14 placement)
+            pair, s = self.trimul_fwd(pair, f"{p}.tri_mul_out", feats, True)
+            tm.append(s)
+            pair, s = self.trimul_fwd(pair, f"{p}.tri_mul_in", feats, False)
+            tm.append(s)
+        pair, s1 = self.attn_fwd(pair, f"{p}.tri_start", self.var["tri_start"], feats)
         pair, s2 = self.attn_fwd(pair, f"{p}.tri_end", self.var["tri_end"], feats)
         pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
-        return pair, (s1, s2, s3)
+        return pair, (tm, s1, s2, s3)
 
     def pair_branch_bwd(self, i, d_pair, saved, feats):
         """d(pair_out) -> d(pair_mid) in place."""
         p = f"block{i}"
-        s1, s2, s3 = saved
+        tm, s1, s2, s3 = saved
         self.trans_bwd(d_pair, s3, f"{p}.pair_trans")
         self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats)
         self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats)
+        if tm:
+            self.trimul_bwd(d_pair, tm[1], f"{p}.tri_mul_in", feats)
+            self.trimul_bwd(d_pair, tm[0], f"{p}.tri_mul_out", feats)
 
     # -- whole block (src/model.py:431-445) -------------------------------------------
 

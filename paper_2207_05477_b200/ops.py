@@ -68,6 +68,63 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, ta: bool = False, tb
          ptr(c), c.stride(0), 0, 1, alpha, beta, dcode(a), dcode(c), stream())
 
 
+def gemm_batched(a, b, c, batch, sa, sb, sc, ta=False, tb=False, alpha=1.0, beta=0.0):
+    """Strided-batched row-major GEMM on flat buffers: operand k of batch i is
+    the matrix at data_ptr + i*s (elements); a, b, c are 2-D views of batch 0."""
+    M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
+    Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
+    if K != Kb or tuple(c.shape) != (M, N):
+        raise ValueError("gemm_batched shape mismatch")
+    call("evo_gemm", M, N, K, ptr(a), a.stride(0), int(ta), sa, ptr(b), b.stride(0), int(tb), sb,
+         ptr(c), c.stride(0), sc, batch, alpha, beta, dcode(a), dcode(c), stream())
+
+
+# ---------------------------------------------------------------------------
+# triangle multiplication glue
+
+
+def trimul_gate_fwd(proj, biases, mask, ch):
+    RR = proj.shape[0]
+    a = torch.empty((ch, RR), dtype=proj.dtype, device=proj.device)
+    b = torch.empty_like(a)
+    call("evo_trimul_gate_fwd", ptr(proj), proj.stride(0), *[ptr(t) for t in biases], ptr(mask),
+         ptr(a), ptr(b), RR, ch, dcode(proj), stream())
+    return a, b
+
+
+def trimul_gate_bwd(proj, biases, mask, da, db, ch):
+    RR = proj.shape[0]
+    dproj = torch.empty((RR, 4 * ch), dtype=proj.dtype, device=proj.device)
+    call("evo_trimul_gate_bwd", ptr(proj), proj.stride(0), *[ptr(t) for t in biases], ptr(mask),
+         ptr(da), ptr(db), ptr(dproj), RR, ch, dcode(proj), stream())
+    return dproj
+
+
+def transpose2d(x, out_dtype=None):
+    rows, cols = x.shape
+    y = torch.empty((cols, rows), dtype=out_dtype or x.dtype, device=x.device)
+    call("evo_transpose2d", ptr(x), dcode(x), ptr(y), dcode(y), rows, cols, stream())
+    return y
+
+
+def gated_residual(res, gp, bg, y, by):
+    rows, C = y.shape
+    g = torch.empty_like(y)
+    out = torch.empty_like(y)
+    call("evo_gated_residual", ptr(res), ptr(gp), gp.stride(0), ptr(bg), ptr(y), ptr(by), ptr(g),
+         ptr(out), rows, C, dcode(y), stream())
+    return g, out
+
+
+def gated_residual_bwd(dout, g, y, by):
+    rows, C = y.shape
+    dyb = torch.empty_like(y)
+    dgp = torch.empty_like(y)
+    call("evo_gated_residual_bwd", ptr(dout), ptr(g), ptr(y), ptr(by), ptr(dyb), ptr(dgp), rows, C,
+         dcode(y), stream())
+    return dyb, dgp
+
+
 # ---------------------------------------------------------------------------
 # LayerNorm / glue
 
@@ -113,6 +170,15 @@ def colsum_cast(x, out, y=None, accumulate=False):
     ws = _ws(_lib.load().evo_colsum_workspace(C), x.device)
     call("evo_colsum_cast", ptr(x), dcode(x), ptr(out), int(accumulate), ptr(y),
          dcode(y) if y is not None else F32, ptr(ws), rows, C, stream())
+
+
+def colsum_strided(x, out, accumulate=False):
+    """Column sums of a 2-D view whose rows are strided (a column slice)."""
+    rows, C = x.shape
+    assert x.stride(1) == 1
+    ws = _ws(_lib.load().evo_colsum_workspace(C), x.device)
+    call("evo_colsum_strided", ptr(x), dcode(x), x.stride(0), ptr(out), int(accumulate), ptr(ws),
+         rows, C, stream())
 
 
 class PackPlan:

@@ -130,3 +130,26 @@ def test_fully_masked_rows_uniform_on_gpu():
     v = qkvg[L:, 2 * H * D:3 * H * D]
     expect = v.mean(dim=0, keepdim=True).expand(L, -1)
     assert torch.allclose(ctx[L:], expect, atol=1e-5)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_block_with_trimul_matches_oracle(dtype):
+    """TriangleMultiplication extension (AF2 Alg 11/12) against the oracle
+    restatement -- parity UNPINNED (no reference code), so this checks the
+    GPU path against the restatement, whose backward is FD-checked on CPU."""
+    from oracle import evoformer_np as O
+    from paper_2207_05477_b200.model import ModelConfig
+    kw = dict(n_blocks=1, n_seq=16, n_res=32, c_m=32, c_z=32, heads=2, opm_dim=8, trimul=True)
+    cfg = ModelConfig(**kw)
+    ocfg = O.ModelConfig(**kw)
+    oloss, ograds, (omsa, opair) = O.serial_grads(ocfg, O.init_params(ocfg, 7), O.make_features(ocfg, 3))
+    dt = torch.float32 if dtype == "f32" else torch.bfloat16
+    loss, msa, pair, grads = _run_engine(cfg, 7, 3, 1, dt)
+    tol_o, tol_g, floor = (FP32_TOL, FP32_TOL, 1e-6) if dtype == "f32" else (BF16_OUT_TOL, BF16_GRAD_TOL, 1e-3)
+    assert rel_err(pair.reshape(opair.shape), opair) <= tol_o
+    assert rel_err(msa.reshape(omsa.shape), omsa) <= tol_o
+    gmax = max(np.abs(v).max() for v in ograds.values())
+    errs = {n: rel_err(grads[n], ograds[n], floor * gmax) for n in ograds}
+    worst = max(errs, key=errs.get)
+    assert errs[worst] <= tol_g, (worst, errs[worst])
+    assert any("tri_mul" in n and np.abs(grads[n]).max() > 0 for n in grads)
