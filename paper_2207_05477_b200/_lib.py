@@ -13,7 +13,8 @@ import os
 from .errors import ContractError, DimensionError, NativeUnavailable
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libevoformer_sm100.so")
+# EVO_LIB_PATH: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("EVO_LIB_PATH") or os.path.join(_HERE, "libevoformer_sm100.so")
 
 F32, BF16 = 0, 1
 PARTIAL_BLOCKS = 256

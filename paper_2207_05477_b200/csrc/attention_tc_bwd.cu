@@ -28,7 +28,6 @@ bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, 
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void st_zero16(void* p) {
   *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
@@ -41,26 +40,6 @@ __device__ __forceinline__ void bf16x8_to_f(const uint4& u, float* f) {
     float2 t = __bfloat1622float2(h[k]);
     f[2 * k] = t.x;
     f[2 * k + 1] = t.y;
-  }
-}
-
-// load N bias values nb_row[c0 .. c0+N) (bf16) as floats; zero beyond L
-template <int N>
-__device__ __forceinline__ void load_bias(const bf16* nb_row, int c0, int L, bool vec_ok, float* f) {
-  if (nb_row == nullptr) {
-#pragma unroll
-    for (int e = 0; e < N; ++e) f[e] = 0.f;
-    return;
-  }
-  if (vec_ok && c0 + N <= L) {
-#pragma unroll
-    for (int k = 0; k < N / 8; ++k) {
-      uint4 u = __ldg(reinterpret_cast<const uint4*>(nb_row + c0) + k);
-      bf16x8_to_f(u, f + 8 * k);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < N; ++e) f[e] = (c0 + e < L) ? __bfloat162float(nb_row[c0 + e]) : 0.f;
   }
 }
 
@@ -274,13 +253,15 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
           tc::mma_commit(&bar[0]);
         }
         const int c0 = koff + cg * 16;  // this thread's 16 key columns
-        float bias[16];
+        uint32_t braw[8];
         if (BIAS) {
-          bf16x8_to_f(*reinterpret_cast<const uint4*>(sBrow + c0), bias);
-          bf16x8_to_f(*reinterpret_cast<const uint4*>(sBrow + c0 + 8), bias + 8);
+          const uint4 u0 = *reinterpret_cast<const uint4*>(sBrow + c0);
+          const uint4 u1 = *reinterpret_cast<const uint4*>(sBrow + c0 + 8);
+          braw[0] = u0.x, braw[1] = u0.y, braw[2] = u0.z, braw[3] = u0.w;
+          braw[4] = u1.x, braw[5] = u1.y, braw[6] = u1.z, braw[7] = u1.w;
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) bias[e] = 0.f;
+          for (int e = 0; e < 8; ++e) braw[e] = 0u;
         }
         tc::mbar_wait(&bar[0], ph0);
         ph0 ^= 1;
@@ -291,26 +272,24 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
         if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
         tc::wait_ld();
         uint32_t pp[8], pd[8];
+        const float2 nm2 = make_float2(-m2, -m2), rl2 = make_float2(rl, rl), nD2 = make_float2(-Dv, -Dv);
 #pragma unroll
         for (int e = 0; e < 16; e += 4) {
           const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
-          const float mb[4] = {mb4.x, mb4.y, mb4.z, mb4.w};
-          float pv[4], dv[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float x = __fmul_rn(s[e + u], scale);
-            x = x + mb[u];
-            x = x + bias[e + u];
-            const float p = tc::ex2(__fmul_rn(x, LOG2E) - m2) * rl;
-            const float d = p * (dp[e + u] - Dv);
-            pv[u] = p;
-            dv[u] = d;
-            if (BIAS) acc[e + u] += d;
+          for (int u = 0; u < 4; u += 2) {
+            const float2 x = tc::logit2(make_float2(s[e + u], s[e + u + 1]), tc::bf16x2_f2(braw[(e + u) / 2]),
+                                        u == 0 ? make_float2(mb4.x, mb4.y) : make_float2(mb4.z, mb4.w), scale);
+            const float2 xd = __fadd2_rn(x, nm2);
+            const float2 p = __fmul2_rn(make_float2(tc::ex2(xd.x), tc::ex2(xd.y)), rl2);
+            const float2 d = __fmul2_rn(p, __fadd2_rn(make_float2(dp[e + u], dp[e + u + 1]), nD2));
+            if (BIAS) {
+              const float2 a = __fadd2_rn(make_float2(acc[e + u], acc[e + u + 1]), d);
+              acc[e + u] = a.x, acc[e + u + 1] = a.y;
+            }
+            pp[(e + u) / 2] = tc::pack_bf16(p.x, p.y);
+            pd[(e + u) / 2] = tc::pack_bf16(d.x, d.y);
           }
-          pp[e / 2] = tc::pack_bf16(pv[0], pv[1]);
-          pp[e / 2 + 1] = tc::pack_bf16(pv[2], pv[3]);
-          pd[e / 2] = tc::pack_bf16(dv[0], dv[1]);
-          pd[e / 2 + 1] = tc::pack_bf16(dv[2], dv[3]);
         }
         if (BIAS) tmem_st16(tl + C_DB + c0, acc);
         // P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B

@@ -31,7 +31,6 @@ namespace evo {
 namespace {
 
 using bf16 = __nv_bfloat16;
-constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ void st_zero16(void* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u); }
 
@@ -197,26 +196,29 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       const int c0 = half * HALF + ch * 32;
-      float v[32], bias[32];
+      float v[32];
+      uint32_t braw[16];
       tc::tmem_ld32(tl + c0, v);
       if (BIAS) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bf16x8_to_f(*reinterpret_cast<const uint4*>(sBrow + c0 + 8 * k), bias + 8 * k);
+        for (int k = 0; k < 4; ++k) {
+          const uint4 u = *reinterpret_cast<const uint4*>(sBrow + c0 + 8 * k);
+          braw[4 * k] = u.x, braw[4 * k + 1] = u.y, braw[4 * k + 2] = u.z, braw[4 * k + 3] = u.w;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) braw[k] = 0u;
       }
       tc::wait_ld();
 #pragma unroll
       for (int e = 0; e < 32; e += 4) {
         const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
-        const float mb[4] = {mb4.x, mb4.y, mb4.z, mb4.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float x = __fmul_rn(v[e + u], scale);
-          x = x + mb[u];
-          if (BIAS) x = x + bias[e + u];
-          x = __fmul_rn(x, LOG2E);
-          v[e + u] = x;
-          mx = fmaxf(mx, x);
-        }
+        const float2 x0 = tc::logit2(make_float2(v[e], v[e + 1]), tc::bf16x2_f2(braw[e / 2]),
+                                     make_float2(mb4.x, mb4.y), scale);
+        const float2 x1 = tc::logit2(make_float2(v[e + 2], v[e + 3]), tc::bf16x2_f2(braw[e / 2 + 1]),
+                                     make_float2(mb4.z, mb4.w), scale);
+        v[e] = x0.x, v[e + 1] = x0.y, v[e + 2] = x1.x, v[e + 3] = x1.y;
+        mx = fmaxf(mx, fmaxf(fmaxf(x0.x, x0.y), fmaxf(x1.x, x1.y)));
       }
       tc::tmem_st32(tl + c0, v);
     }
@@ -226,7 +228,8 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     const float m = fmaxf(sEx[row], sEx[128 + row]);
 
     // ---- pass 2: P = exp2(logits - m), packed bf16 pairs back into TMEM ----
-    float sum = 0.f;
+    float2 sum2 = make_float2(0.f, 0.f);
+    const float2 nm2 = make_float2(-m, -m);
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       const int c0 = half * HALF + ch * 32;
@@ -236,16 +239,16 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
-        const float p0 = tc::ex2(v[e] - m);
-        const float p1 = tc::ex2(v[e + 1] - m);
-        sum += p0 + p1;
-        pk[e / 2] = tc::pack_bf16(p0, p1);
+        const float2 d = __fadd2_rn(make_float2(v[e], v[e + 1]), nm2);  // exact near the max
+        const float2 p = make_float2(tc::ex2(d.x), tc::ex2(d.y));
+        sum2 = __fadd2_rn(sum2, p);
+        pk[e / 2] = tc::pack_bf16(p.x, p.y);
       }
       // keys [c0, c0+32) -> columns half*HALF + (c0 - half*HALF)/2 ... (+16)
       tc::tmem_st16u(tl + half * HALF + ch * 16, pk);
     }
     tc::wait_st();
-    sEx[256 + half * 128 + row] = sum;
+    sEx[256 + half * 128 + row] = sum2.x + sum2.y;
     tc::fence_before();
     __syncthreads();
 

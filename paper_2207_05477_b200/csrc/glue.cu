@@ -27,6 +27,8 @@ inline bool pow2_width(int64_t C) { return C >= 32 && C <= 1024 && (C & (C - 1))
 // has its loads in flight at once; kernels writing per-block partials are
 // capped at PARTIAL_PER_SM blocks per SM (bounded partial rows).
 constexpr int PARTIAL_PER_SM = 2;
+constexpr int EW_UNROLL = 4;          // 16-B vectors per thread in flight in the elementwise kernels
+constexpr int PB_PARTIAL_PER_SM = 2;  // pair-bias backward: 128 registers, 2 blocks per SM
 inline unsigned glue_grid(int64_t rows, int rows_per_iter, int per_sm = 16) {
   int64_t want = (rows + rows_per_iter - 1) / rows_per_iter;
   int64_t cap = (int64_t)num_sms() * per_sm;
@@ -34,16 +36,27 @@ inline unsigned glue_grid(int64_t rows, int rows_per_iter, int per_sm = 16) {
   return (unsigned)(want > 0 ? want : 1);
 }
 
+// 16 channels (two 16-B chunks) per lane: the per-row shuffle reductions are
+// amortised over twice the elements of an 8-channel mapping
 template <int C>
 struct RowMap {
-  static constexpr int LANES = (C / 8) < 32 ? (C / 8) : 32;  // lanes per row
-  static constexpr int CH = C / (8 * LANES);                  // 8-chunks per lane
+  static constexpr int LANES = (C / 16) < 2 ? 2 : ((C / 16) < 32 ? (C / 16) : 32);  // lanes per row
+  static constexpr int CH = C / (8 * LANES);                                        // 8-chunks per lane
   static constexpr int RPW = 32 / LANES;                      // rows per warp
   static constexpr int GROUPS = GT / LANES;                   // rows per block iteration
 };
 
 // ---------------------------------------------------------------------------
 // LayerNorm forward
+
+// rows a thread group keeps in flight per iteration: every load of the U rows
+// is issued before the first reduction, so each thread has U x 16 B (bf16) or
+// U x 32 B (fp32) outstanding -- what HBM3e needs to stay busy at 2048
+// threads per SM
+template <int C>
+struct Unroll {
+  static constexpr int value = RowMap<C>::CH >= 4 ? 1 : 4 / RowMap<C>::CH;
+};
 
 template <int C, typename TX, typename TY>
 __global__ void __launch_bounds__(GT) ln_fwd_vec_kernel(const TX* __restrict__ x,
@@ -52,41 +65,64 @@ __global__ void __launch_bounds__(GT) ln_fwd_vec_kernel(const TX* __restrict__ x
                                                         TY* __restrict__ y, float* __restrict__ mean,
                                                         float* __restrict__ rstd, int64_t rows, float eps) {
   using M = RowMap<C>;
+  constexpr int U = Unroll<C>::value;
   const int l = threadIdx.x % M::LANES;
   const int grp = threadIdx.x / M::LANES;
+  float gg[M::CH][8], bb[M::CH][8];  // this lane's affine parameters, loaded once
+#pragma unroll
+  for (int k = 0; k < M::CH; ++k) {
+    ld8(g + (k * M::LANES + l) * 8, gg[k]);
+    ld8(b + (k * M::LANES + l) * 8, bb[k]);
+  }
   // block-uniform trip count: the row groups of a warp always shuffle together
-  for (int64_t rb = blockIdx.x * (int64_t)M::GROUPS; rb < rows; rb += (int64_t)gridDim.x * M::GROUPS) {
-    const bool act = rb + grp < rows;
-    const int64_t r = act ? rb + grp : rows - 1;
-    float v[M::CH][8];
-    float s = 0.f;
+  for (int64_t rb = blockIdx.x * (int64_t)(M::GROUPS * U); rb < rows;
+       rb += (int64_t)gridDim.x * M::GROUPS * U) {
+    float v[U][M::CH][8];
+    int64_t r[U];
 #pragma unroll
-    for (int k = 0; k < M::CH; ++k) {
-      ld8(x + r * C + (k * M::LANES + l) * 8, v[k]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t rr = rb + u * M::GROUPS + grp;
+      r[u] = rr < rows ? rr : rows - 1;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += v[k][e];
+      for (int k = 0; k < M::CH; ++k) ld8(x + r[u] * C + (k * M::LANES + l) * 8, v[u][k]);
     }
-    const float mu = group_sum<M::LANES>(s) / (float)C;
-    float q = 0.f;
+    float mu[U], inv[U];
 #pragma unroll
-    for (int k = 0; k < M::CH; ++k)
+    for (int u = 0; u < U; ++u) {
+      float s = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = v[k][e] - mu;
-        q += d * d;
+      for (int k = 0; k < M::CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += v[u][k][e];
+      mu[u] = group_sum<M::LANES>(s) / (float)C;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = v[u][k][e] - mu[u];
+          q += d * d;
+        }
+      inv[u] = rsqrtf(group_sum<M::LANES>(q) / (float)C + eps);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool act = rb + u * M::GROUPS + grp < rows;
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k) {
+        const int c0 = (k * M::LANES + l) * 8;
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = (v[u][k][e] - mu[u]) * inv[u] * gg[k][e] + bb[k][e];
+        if (act) st8(y + r[u] * C + c0, o);
       }
-    const float inv = 1.0f / sqrtf(group_sum<M::LANES>(q) / (float)C + eps);
-#pragma unroll
-    for (int k = 0; k < M::CH; ++k) {
-      const int c0 = (k * M::LANES + l) * 8;
-      float o[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = (v[k][e] - mu) * inv * g[c0 + e] + b[c0 + e];
-      if (act) st8(y + r * C + c0, o);
-    }
-    if (act && l == 0) {
-      if (mean) mean[r] = mu;
-      if (rstd) rstd[r] = inv;
+      if (act && l == 0) {
+        if (mean) mean[r[u]] = mu[u];
+        if (rstd) rstd[r[u]] = inv[u];
+      }
     }
   }
 }
@@ -114,50 +150,65 @@ __global__ void __launch_bounds__(GT) ln_bwd_vec_kernel(
       dg[k][e] = db[k][e] = dsx[k][e] = 0.f;
       gg[k][e] = g[(k * M::LANES + l) * 8 + e];
     }
-  for (int64_t rb = r0; rb < r1; rb += M::GROUPS) {
-    const bool act = rb + grp < r1;
-    const int64_t r = act ? rb + grp : r1 - 1;
-    const float mu = mean[r], inv = rstd[r];
-    const float w = act ? 1.f : 0.f;
-    float xh[M::CH][8], dxh[M::CH][8];
-    float s1 = 0.f, s2 = 0.f;
+  constexpr int U = M::CH == 1 ? 2 : 1;  // rows in flight per thread group
+  for (int64_t rb = r0; rb < r1; rb += M::GROUPS * U) {
+    int64_t r[U];
+    float w[U], mu[U], inv[U];
+    float xh[U][M::CH][8], dxh[U][M::CH][8], o[U][M::CH][8];
+    // issue every load of the U rows first (x, dy, dres), then reduce
 #pragma unroll
-    for (int k = 0; k < M::CH; ++k) {
-      const int c0 = (k * M::LANES + l) * 8;
-      float xv[8], d[8];
-      ld8(x + r * C + c0, xv);
-      ld8(dy + r * C + c0, d);
+    for (int u = 0; u < U; ++u) {
+      const bool act = rb + u * M::GROUPS + grp < r1;
+      r[u] = act ? rb + u * M::GROUPS + grp : r1 - 1;
+      w[u] = act ? 1.f : 0.f;
+      mu[u] = mean[r[u]];
+      inv[u] = rstd[r[u]];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        d[e] *= w;
-        xh[k][e] = (xv[e] - mu) * inv;
-        dxh[k][e] = d[e] * gg[k][e];
-        dg[k][e] += d[e] * xh[k][e];
-        db[k][e] += d[e];
-        s1 += dxh[k][e];
-        s2 += dxh[k][e] * xh[k][e];
+      for (int k = 0; k < M::CH; ++k) {
+        const int c0 = (k * M::LANES + l) * 8;
+        ld8(x + r[u] * C + c0, xh[u][k]);
+        ld8(dy + r[u] * C + c0, dxh[u][k]);
+        if (dres) {
+          ld8(dres + r[u] * C + c0, o[u][k]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[u][k][e] = 0.f;
+        }
       }
     }
-    const float m1 = group_sum<M::LANES>(s1) / (float)C;
-    const float m2 = group_sum<M::LANES>(s2) / (float)C;
+    float m1[U], m2[U];
 #pragma unroll
-    for (int k = 0; k < M::CH; ++k) {
-      const int c0 = (k * M::LANES + l) * 8;
-      float o[8];
-      if (dres) {
-        ld8(dres + r * C + c0, o);
-      } else {
+    for (int u = 0; u < U; ++u) {
+      float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = 0.f;
-      }
+      for (int k = 0; k < M::CH; ++k)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        o[e] += inv * (dxh[k][e] - m1 - xh[k][e] * m2);
-        dsx[k][e] += w * o[e];
-      }
-      if (act) {
-        st8(dx + r * C + c0, o);
-        if (dx16) st8(dx16 + r * C + c0, o);
+        for (int e = 0; e < 8; ++e) {
+          const float d = dxh[u][k][e] * w[u];
+          xh[u][k][e] = (xh[u][k][e] - mu[u]) * inv[u];
+          dxh[u][k][e] = d * gg[k][e];
+          dg[k][e] += d * xh[u][k][e];
+          db[k][e] += d;
+          s1 += dxh[u][k][e];
+          s2 += dxh[u][k][e] * xh[u][k][e];
+        }
+      m1[u] = group_sum<M::LANES>(s1) / (float)C;
+      m2[u] = group_sum<M::LANES>(s2) / (float)C;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k) {
+        const int c0 = (k * M::LANES + l) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          o[u][k][e] += inv[u] * (dxh[u][k][e] - m1[u] - xh[u][k][e] * m2[u]);
+          dsx[k][e] += w[u] * o[u][k][e];
+        }
+        if (w[u] != 0.f) {
+          st8(dx + r[u] * C + c0, o[u][k]);
+          if (dx16) st8(dx16 + r[u] * C + c0, o[u][k]);
+        }
       }
     }
   }
@@ -197,20 +248,34 @@ __global__ void __launch_bounds__(GT) colsum_vec_kernel(TX* x, int64_t ldx, cons
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#pragma unroll 2
-  for (int64_t r = r0 + rg; r < r1; r += RPB) {
-    float v[8];
-    ld8(x + r * ldx + ct * 8, v);
-    if (MODE == 1) {
-      float hv[8];
-      ld8(h + r * C + ct * 8, hv);
+  constexpr int U = 4;  // rows in flight per thread: all loads before any store
+  for (int64_t rb = r0 + rg; rb < r1; rb += (int64_t)RPB * U) {
+    Vec8<TX> vx[U], vh[U];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = hv[e] > 0.f ? v[e] : 0.f;
-      st8(x + r * ldx + ct * 8, v);
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = rb + (int64_t)u * RPB;
+      if (r < r1) {
+        ldv8(x + r * ldx + ct * 8, vx[u]);
+        if (MODE == 1) ldv8(h + r * C + ct * 8, vh[u]);
+      }
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] += v[e];
-    if (y) st8(y + r * C + ct * 8, v);
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = rb + (int64_t)u * RPB;
+      if (r >= r1) continue;  // rows ascend with u: acc sees rows in order
+      float v[8];
+      cvt8(vx[u], v);
+      if (MODE == 1) {
+        float hv[8];
+        cvt8(vh[u], hv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = hv[e] > 0.f ? v[e] : 0.f;
+        st8(x + r * ldx + ct * 8, v);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += v[e];
+      if (y) st8(y + r * C + ct * 8, v);
+    }
   }
 #pragma unroll
   for (int e = 0; e < 8; ++e) sm[rg * C + ct * 8 + e] = acc[e];
@@ -230,186 +295,306 @@ __global__ void __launch_bounds__(GT) bias_residual_vec_kernel(const TR* __restr
                                                                const TY* __restrict__ y,
                                                                const float* __restrict__ bias,
                                                                TO* __restrict__ out, int64_t n8, int C8) {
-  for (int64_t e = blockIdx.x * (int64_t)GT + threadIdx.x; e < n8; e += (int64_t)gridDim.x * GT) {
-    const int c0 = (int)(e % C8) * 8;
-    float v[8];
-    ld8(y + e * 8, v);
-    if (bias) {
+  constexpr int U = EW_UNROLL;
+  for (int64_t e0 = blockIdx.x * (int64_t)(GT * U) + threadIdx.x; e0 < n8; e0 += (int64_t)gridDim.x * GT * U) {
+    Vec8<TY> vy[U];
+    Vec8<TR> vr[U];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] += bias[c0 + k];
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * GT;
+      if (e < n8) {
+        ldv8(y + e * 8, vy[u]);
+        if (res) ldv8(res + e * 8, vr[u]);
+      }
     }
-    if (res) {
-      float r[8];
-      ld8(res + e * 8, r);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = r[k] + v[k];
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * GT;
+      if (e >= n8) continue;
+      const int c0 = (int)(e % C8) * 8;
+      float v[8];
+      cvt8(vy[u], v);
+      if (bias) {
+        float bv[8];
+        ld8(bias + c0, bv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += bv[k];
+      }
+      if (res) {
+        float r[8];
+        cvt8(vr[u], r);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = r[k] + v[k];
+      }
+      st8(out + e * 8, v);
     }
-    st8(out + e * 8, v);
   }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(GT) bias_relu_vec_kernel(T* __restrict__ y, const float* __restrict__ bias,
                                                            int64_t n8, int C8) {
-  for (int64_t e = blockIdx.x * (int64_t)GT + threadIdx.x; e < n8; e += (int64_t)gridDim.x * GT) {
-    const int c0 = (int)(e % C8) * 8;
-    float v[8];
-    ld8(y + e * 8, v);
+  constexpr int U = EW_UNROLL;
+  for (int64_t e0 = blockIdx.x * (int64_t)(GT * U) + threadIdx.x; e0 < n8; e0 += (int64_t)gridDim.x * GT * U) {
+    Vec8<T> vy[U];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = fmaxf(v[k] + (bias ? bias[c0 + k] : 0.f), 0.f);
-    st8(y + e * 8, v);
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * GT;
+      if (e < n8) ldv8(y + e * 8, vy[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * GT;
+      if (e >= n8) continue;
+      const int c0 = (int)(e % C8) * 8;
+      float v[8], bv[8];
+      cvt8(vy[u], v);
+      if (bias) {
+        ld8(bias + c0, bv);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bv[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = fmaxf(v[k] + bv[k], 0.f);
+      st8(y + e * 8, v);
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // pair bias: nb[h, x, y] (or [h, y, x]) = LN(z[x, y]) . w[:, h]
+//
+// A token row is spread over PB_LANES lanes with 4 channels each (8-byte bf16
+// / 16-byte fp32 accesses), so a lane's slice of w (4 channels x 8 heads) and,
+// in the backward, of dw stay in registers at ~100 registers per thread; two
+// tokens per row group are in flight per iteration.  The 8 per-head dot
+// products are reduced across the row group by a halving butterfly (8 -> 4
+// -> 2 -> 1 values per lane, then plain sums): 9 shuffles per token instead
+// of 8 full reductions.
+
+template <int C>
+struct PbMap {
+  static constexpr int LANES = (C / 4) < 32 ? (C / 4) : 32;  // lanes per token
+  static constexpr int CH = C / (4 * LANES);                  // 4-channel chunks per lane
+  static constexpr int GROUPS = GT / LANES;                   // tokens per block iteration
+  static constexpr int U = 2;                                 // tokens in flight per row group
+};
+
+// p[h]: this lane's partial dot product for head h.  Returns the sum over the
+// row group's LANES lanes for head pb_head<LANES>(l).
+template <int LANES>
+__device__ __forceinline__ float head_reduce8(const float (&p)[8], int l) {
+  static_assert(LANES >= 8, "head butterfly needs >= 8 lanes per token");
+  float q4[4], q2[2];
+  {
+    const bool hi = (l & (LANES / 2)) != 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      q4[j] = (hi ? p[j + 4] : p[j]) + __shfl_xor_sync(0xffffffffu, hi ? p[j] : p[j + 4], LANES / 2);
+  }
+  {
+    const bool hi = (l & (LANES / 4)) != 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      q2[j] = (hi ? q4[j + 2] : q4[j]) + __shfl_xor_sync(0xffffffffu, hi ? q4[j] : q4[j + 2], LANES / 4);
+  }
+  const bool hi = (l & (LANES / 8)) != 0;
+  float q = (hi ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, hi ? q2[0] : q2[1], LANES / 8);
+#pragma unroll
+  for (int o = LANES / 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  return q;
+}
+template <int LANES>
+__device__ __forceinline__ int pb_head(int l) {
+  return ((l & (LANES / 2)) ? 4 : 0) | ((l & (LANES / 4)) ? 2 : 0) | ((l & (LANES / 8)) ? 1 : 0);
+}
 
 template <int C, typename T>
 __global__ void __launch_bounds__(GT) pair_bias_fwd_vec_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
     const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
     float* __restrict__ rstd, int64_t R, int H, int swap_xy) {
-  using M = RowMap<C>;
-  static_assert(M::CH == 1, "pair bias expects C <= 256");
+  using M = PbMap<C>;
+  constexpr int U = M::U;
   const int l = threadIdx.x % M::LANES;
   const int grp = threadIdx.x / M::LANES;
-  const int c0 = l * 8;
-  float gg[8], bb[8], wr[8][8];  // this lane's 8 channels x (up to 8) heads, in registers
+  float gg[M::CH][4], bb[M::CH][4], wr[M::CH][4][8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    gg[e] = g[c0 + e];
-    bb[e] = b[c0 + e];
+  for (int k = 0; k < M::CH; ++k)
 #pragma unroll
-    for (int hh = 0; hh < 8; ++hh) wr[e][hh] = hh < H ? w[(c0 + e) * H + hh] : 0.f;
-  }
+    for (int e = 0; e < 4; ++e) {
+      const int c = (k * M::LANES + l) * 4 + e;
+      gg[k][e] = g[c];
+      bb[k][e] = b[c];
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) wr[k][e][hh] = hh < H ? w[c * H + hh] : 0.f;
+    }
+  const int hme = pb_head<M::LANES>(l);
+  const bool writer = (l & (M::LANES / 8 - 1)) == 0 && hme < H;
   const int64_t NT = R * R;
-  for (int64_t tb = blockIdx.x * (int64_t)M::GROUPS; tb < NT; tb += (int64_t)gridDim.x * M::GROUPS) {
-    const bool act = tb + grp < NT;
-    const int64_t t = act ? tb + grp : NT - 1;
-    float v[8];
-    ld8(z + t * C + c0, v);
-    float s = 0.f;
+  for (int64_t tb = blockIdx.x * (int64_t)(M::GROUPS * U); tb < NT; tb += (int64_t)gridDim.x * M::GROUPS * U) {
+    float v[U][M::CH][4];
+    int64_t t[U];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) s += v[e];
-    const float mu = group_sum<M::LANES>(s) / (float)C;
-    float q = 0.f;
+    for (int u = 0; u < U; ++u) {
+      const int64_t tt = tb + u * M::GROUPS + grp;
+      t[u] = tt < NT ? tt : NT - 1;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float d = v[e] - mu;
-      q += d * d;
+      for (int k = 0; k < M::CH; ++k) ld4(z + t[u] * C + (k * M::LANES + l) * 4, v[u][k]);
     }
-    const float inv = 1.0f / sqrtf(group_sum<M::LANES>(q) / (float)C + 1e-5f);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = (v[e] - mu) * inv * gg[e] + bb[e];
-    const int64_t x = t / R, y = t % R;
-    float mine = 0.f;
+    for (int u = 0; u < U; ++u) {
+      float s = 0.f;
 #pragma unroll
-    for (int hh = 0; hh < 8; ++hh) {
-      if (hh < H) {
-        float p = 0.f;
+      for (int k = 0; k < M::CH; ++k)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) p = fmaf(v[e], wr[e][hh], p);
-        p = group_sum<M::LANES>(p);
-        if (l == hh) mine = p;
+        for (int e = 0; e < 4; ++e) s += v[u][k][e];
+      const float mu = group_sum<M::LANES>(s) / (float)C;
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float d = v[u][k][e] - mu;
+          q += d * d;
+        }
+      const float inv = rsqrtf(group_sum<M::LANES>(q) / (float)C + 1e-5f);
+      float p[8];
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) p[hh] = 0.f;
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float zl = (v[u][k][e] - mu) * inv * gg[k][e] + bb[k][e];
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) p[hh] = fmaf(zl, wr[k][e][hh], p[hh]);
+        }
+      const float mine = head_reduce8<M::LANES>(p, l);
+      const bool act = tb + u * M::GROUPS + grp < NT;
+      if (act && writer) {
+        const int64_t x = t[u] / R, y = t[u] % R;
+        const int64_t o = swap_xy ? ((int64_t)hme * R + y) * R + x : ((int64_t)hme * R + x) * R + y;
+        nb[o] = from_f<T>(mine);
       }
-    }
-    if (act && l < H) {
-      const int64_t o = swap_xy ? ((int64_t)l * R + y) * R + x : ((int64_t)l * R + x) * R + y;
-      nb[o] = from_f<T>(mine);
-    }
-    if (act && l == 0) {
-      mean[t] = mu;
-      rstd[t] = inv;
+      if (act && l == 0) {
+        mean[t[u]] = mu;
+        rstd[t[u]] = inv;
+      }
     }
   }
 }
 
 // partial layout per block: [dw (C*H) | dgamma (C) | dbeta (C)]
-template <int C, int HM, typename T>
+template <int C, typename T>
 __global__ void __launch_bounds__(GT) pair_bias_bwd_vec_kernel(
     const T* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
     const float* __restrict__ dnb, int swap_xy, float* __restrict__ dz,
     float* __restrict__ partials, int64_t R, int H) {
-  using M = RowMap<C>;
-  static_assert(M::CH == 1, "pair bias expects C <= 256");
-  extern __shared__ float sm[];  // (unused [C*HM]) then reduction scratch [GROUPS][C*H + 2C]
-  float* red = sm + C * HM;
+  using M = PbMap<C>;
+  constexpr int U = M::U;
+  extern __shared__ float red[];  // [GROUPS][C*H + 2C]
   const int l = threadIdx.x % M::LANES;
   const int grp = threadIdx.x / M::LANES;
-  const int c0 = l * 8;
-  float gg[8], bb[8], wr[8][HM];  // this lane's channels x heads, in registers
+  float gg[M::CH][4], bb[M::CH][4], wr[M::CH][4][8], dw[M::CH][4][8], dgs[M::CH][4], dbs[M::CH][4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    gg[e] = g[c0 + e];
-    bb[e] = bln[c0 + e];
+  for (int k = 0; k < M::CH; ++k)
 #pragma unroll
-    for (int hh = 0; hh < HM; ++hh) wr[e][hh] = hh < H ? w[(c0 + e) * H + hh] : 0.f;
-  }
-  float dw[8][HM], dgs[8], dbs[8];
+    for (int e = 0; e < 4; ++e) {
+      const int c = (k * M::LANES + l) * 4 + e;
+      gg[k][e] = g[c];
+      bb[k][e] = bln[c];
+      dgs[k][e] = dbs[k][e] = 0.f;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    dgs[e] = dbs[e] = 0.f;
-#pragma unroll
-    for (int hh = 0; hh < HM; ++hh) dw[e][hh] = 0.f;
-  }
+      for (int hh = 0; hh < 8; ++hh) {
+        wr[k][e][hh] = hh < H ? w[c * H + hh] : 0.f;
+        dw[k][e][hh] = 0.f;
+      }
+    }
+  const int base = (threadIdx.x & 31) - l;  // first lane of this row group
   const int64_t NT = R * R;
   const int64_t t0 = (NT * blockIdx.x) / gridDim.x, t1 = (NT * (blockIdx.x + 1)) / gridDim.x;
-  for (int64_t tb = t0; tb < t1; tb += M::GROUPS) {
-    const bool act = tb + grp < t1;
-    const int64_t t = act ? tb + grp : t1 - 1;
-    const int64_t x = t / R, y = t % R;
-    float dp_mine = 0.f;
-    if (act && l < H) {  // inactive groups carry dP = 0: no contribution anywhere
-      const int64_t o = swap_xy ? ((int64_t)l * R + y) * R + x : ((int64_t)l * R + x) * R + y;
-      dp_mine = dnb[o];
-    }
-    float dP[HM];
-    const int base = (threadIdx.x & 31) - l;  // first lane of this row group
+  for (int64_t tb = t0; tb < t1; tb += M::GROUPS * U) {
+    int64_t t[U];
+    bool act[U];
+    float dpm[U], mu[U], inv[U];
+    float v[U][M::CH][4], o[U][M::CH][4];
+    // every load of the U tokens first: z, dz, dnb, statistics
 #pragma unroll
-    for (int hh = 0; hh < HM; ++hh) dP[hh] = __shfl_sync(0xffffffffu, dp_mine, base + (hh < M::LANES ? hh : 0));
-    const float mu = mean[t], inv = rstd[t];
-    float v[8];
-    ld8(z + t * C + c0, v);
-    float xh[8], dxh[8];
-    float s1 = 0.f, s2 = 0.f;
+    for (int u = 0; u < U; ++u) {
+      act[u] = tb + u * M::GROUPS + grp < t1;
+      t[u] = act[u] ? tb + u * M::GROUPS + grp : t1 - 1;
+      const int64_t x = t[u] / R, y = t[u] % R;
+      dpm[u] = 0.f;
+      if (act[u] && l < H) {  // inactive groups carry dP = 0: no contribution anywhere
+        const int64_t od = swap_xy ? ((int64_t)l * R + y) * R + x : ((int64_t)l * R + x) * R + y;
+        dpm[u] = dnb[od];
+      }
+      mu[u] = mean[t[u]];
+      inv[u] = rstd[t[u]];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      xh[e] = (v[e] - mu) * inv;
-      const float zl = xh[e] * gg[e] + bb[e];
-      float dzl = 0.f;
+      for (int k = 0; k < M::CH; ++k) {
+        const int c0 = (k * M::LANES + l) * 4;
+        ld4(z + t[u] * C + c0, v[u][k]);
+        if (act[u]) {
+          ld4(dz + t[u] * C + c0, o[u][k]);
+        } else {
 #pragma unroll
-      for (int hh = 0; hh < HM; ++hh) {
-        if (hh < H) {
-          dzl = fmaf(dP[hh], wr[e][hh], dzl);
-          dw[e][hh] = fmaf(zl, dP[hh], dw[e][hh]);
+          for (int e = 0; e < 4; ++e) o[u][k][e] = 0.f;
         }
       }
-      dgs[e] += dzl * xh[e];
-      dbs[e] += dzl;
-      dxh[e] = dzl * gg[e];
-      s1 += dxh[e];
-      s2 += dxh[e] * xh[e];
     }
-    const float m1 = group_sum<M::LANES>(s1) / (float)C, m2 = group_sum<M::LANES>(s2) / (float)C;
-    if (act) {
-      float o[8];
-      ld8(dz + t * C + c0, o);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] += inv * (dxh[e] - m1 - xh[e] * m2);
-      st8(dz + t * C + c0, o);
+    for (int u = 0; u < U; ++u) {
+      float dP[8];
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) dP[hh] = __shfl_sync(0xffffffffu, dpm[u], base + hh);
+      float xh[M::CH][4], dxh[M::CH][4];
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < M::CH; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          xh[k][e] = (v[u][k][e] - mu[u]) * inv[u];
+          const float zl = xh[k][e] * gg[k][e] + bb[k][e];
+          float dzl = 0.f;
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) {
+            dzl = fmaf(dP[hh], wr[k][e][hh], dzl);
+            dw[k][e][hh] = fmaf(zl, dP[hh], dw[k][e][hh]);
+          }
+          dgs[k][e] += dzl * xh[k][e];
+          dbs[k][e] += dzl;
+          dxh[k][e] = dzl * gg[k][e];
+          s1 += dxh[k][e];
+          s2 += dxh[k][e] * xh[k][e];
+        }
+      const float m1 = group_sum<M::LANES>(s1) / (float)C, m2 = group_sum<M::LANES>(s2) / (float)C;
+      if (act[u]) {
+#pragma unroll
+        for (int k = 0; k < M::CH; ++k) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[u][k][e] += inv[u] * (dxh[k][e] - m1 - xh[k][e] * m2);
+          st4(dz + t[u] * C + (k * M::LANES + l) * 4, o[u][k]);
+        }
+      }
     }
   }
   const int W = C * H + 2 * C;
   float* mine = red + grp * W;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
+  for (int k = 0; k < M::CH; ++k)
 #pragma unroll
-    for (int hh = 0; hh < HM; ++hh)
-      if (hh < H) mine[(c0 + e) * H + hh] = dw[e][hh];
-    mine[C * H + c0 + e] = dgs[e];
-    mine[C * H + C + c0 + e] = dbs[e];
-  }
+    for (int e = 0; e < 4; ++e) {
+      const int c = (k * M::LANES + l) * 4 + e;
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh)
+        if (hh < H) mine[c * H + hh] = dw[k][e][hh];
+      mine[C * H + c] = dgs[k][e];
+      mine[C * H + C + c] = dbs[k][e];
+    }
   __syncthreads();
   for (int c = threadIdx.x; c < W; c += GT) {
     float acc = 0.f;
@@ -525,7 +710,7 @@ template <int C, typename TX>
 void ln_fwd_dispatch_y(const void* x, const float* g, const float* b, void* y, int ydt, float* mean,
                        float* rstd, int64_t rows, float eps, cudaStream_t s) {
   using M = RowMap<C>;
-  unsigned grid = glue_grid(rows, M::GROUPS);
+  unsigned grid = glue_grid(rows, M::GROUPS * Unroll<C>::value);
   EVO_DISPATCH_T(ydt, TY, {
     ln_fwd_vec_kernel<C, TX, TY><<<grid, GT, 0, s>>>((const TX*)x, g, b, (TY*)y, mean, rstd, rows, eps);
   });
@@ -646,9 +831,9 @@ bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, 
 
 bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const float* bias, void* out,
                        int odt, int64_t rows, int64_t C, cudaStream_t s) {
-  if ((C % 8) != 0 || !al16(y) || !al16(out) || (res && !al16(res))) return false;
+  if ((C % 8) != 0 || !al16(y) || !al16(out) || (res && !al16(res)) || (bias && !al16(bias))) return false;
   const int64_t n8 = rows * C / 8;
-  unsigned grid = glue_grid(n8, GT * 2);
+  unsigned grid = glue_grid(n8, GT * EW_UNROLL);
   EVO_DISPATCH_T(rdt, TR, EVO_DISPATCH_T(ydt, TY, EVO_DISPATCH_T(odt, TO, {
     bias_residual_vec_kernel<TR, TY, TO><<<grid, GT, 0, s>>>((const TR*)res, (const TY*)y, bias,
                                                              (TO*)out, n8, (int)(C / 8));
@@ -659,9 +844,9 @@ bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const f
 }
 
 bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, cudaStream_t s) {
-  if ((C % 8) != 0 || !al16(y)) return false;
+  if ((C % 8) != 0 || !al16(y) || (bias && !al16(bias))) return false;
   const int64_t n8 = rows * C / 8;
-  unsigned grid = glue_grid(n8, GT * 2);
+  unsigned grid = glue_grid(n8, GT * EW_UNROLL);
   EVO_DISPATCH_T(dt, T, {
     bias_relu_vec_kernel<T><<<grid, GT, 0, s>>>((T*)y, bias, n8, (int)(C / 8));
   });
@@ -673,11 +858,12 @@ bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, 
 bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
                        float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap,
                        cudaStream_t s) {
-  if (!pow2_width(C) || C > 256 || H > 8 || H > C / 8 || !al16(z)) return false;
+  if (!pow2_width(C) || C > 256 || H > 8 || !al16(z)) return false;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
-      using M = RowMap<CC>;
-      unsigned grid = glue_grid(R * R, M::GROUPS * 4, 2);  // weights live in registers: few blocks
+      using M = PbMap<CC>;
+      // resident blocks only: each block loads its slice of w once and loops
+      unsigned grid = glue_grid(R * R, M::GROUPS * M::U, 3);
       EVO_DISPATCH_T(dt, T, {
         pair_bias_fwd_vec_kernel<CC, T><<<grid, GT, 0, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd,
                                                             R, (int)H, swap);
@@ -692,24 +878,24 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
 }
 
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) {
-  return (int64_t)num_sms() * PARTIAL_PER_SM * (C * H + 2 * C) * 4;
+  return (int64_t)num_sms() * PB_PARTIAL_PER_SM * (C * H + 2 * C) * 4;
 }
 
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
                        float* dg, float* db, float* dw, int accumulate, void* ws, int64_t R,
                        int64_t C, int64_t H, cudaStream_t s) {
-  if (!pow2_width(C) || C > 256 || H > 8 || H > C / 8 || !al16(z) || !al16(dz)) return false;
+  if (!pow2_width(C) || C > 256 || H > 8 || !al16(z) || !al16(dz)) return false;
   ws = partial_buffer(ws, pair_bias_bwd_vec_ws(C, H));
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
-      using M = RowMap<CC>;
-      grid = glue_grid(R * R, M::GROUPS * 2, PARTIAL_PER_SM);
+      using M = PbMap<CC>;
+      grid = glue_grid(R * R, M::GROUPS * M::U, PB_PARTIAL_PER_SM);
       const int W = (int)(CC * H + 2 * CC);
-      const size_t smem = ((size_t)CC * 8 + (size_t)M::GROUPS * W) * sizeof(float);
+      const size_t smem = (size_t)M::GROUPS * W * sizeof(float);
       EVO_DISPATCH_T(dt, T, {
-        auto k = pair_bias_bwd_vec_kernel<CC, 8, T>;
+        auto k = pair_bias_bwd_vec_kernel<CC, T>;
         if (smem > 48 * 1024)
           EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k<<<grid, GT, smem, s>>>((const T*)z, mean, rstd, g, bln, w, dnb, swap, dz, (float*)ws, R, (int)H);

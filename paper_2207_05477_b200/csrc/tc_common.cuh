@@ -169,11 +169,32 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 
-// staged raw key-mask m in smem -> additive mask bias (m - 1) * 1e9 in place
-// (src/attention.py:151); keys beyond L were staged as -inf and stay so
+constexpr float LOG2E_F = 1.4426950408889634f;
+constexpr float MASK_BIAS_L2 = 1.4426950408889634e9f;  // 1e9 * log2(e)
+
+// staged raw key-mask m in smem -> additive mask bias (m - 1) * 1e9
+// (src/attention.py:151), kept in the log2 domain of the softmax; keys beyond
+// L were staged as -inf and stay so
 __device__ __forceinline__ void mask_to_bias(float* sMb, int LP, int L, int tid, int nthreads) {
   for (int j = tid; j < LP; j += nthreads)
-    if (j < L) sMb[j] = (sMb[j] - 1.0f) * 1e9f;
+    if (j < L) sMb[j] = (sMb[j] - 1.0f) * MASK_BIAS_L2;
+}
+
+// two bf16 packed in a 32-bit word -> two floats (exact; a shift and a mask)
+__device__ __forceinline__ float2 bf16x2_f2(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+}
+
+// Softmax logits of two keys in the log2 domain,
+//   x = (s * c^-1/2 + nb) * log2(e) + mask_bias * log2(e),
+// on the paired fp32 pipes (FFMA2).  The forward and the backward both form
+// x with exactly this sequence, so the backward's recomputed P is bit-equal to
+// the forward's, including a fully-masked row where every x rounds onto the
+// same mask_bias value and P is uniform (the reference semantics,
+// src/attention.py:151-161).
+__device__ __forceinline__ float2 logit2(float2 s, float2 nb, float2 mb, float scale) {
+  const float2 t = __ffma2_rn(s, make_float2(scale, scale), nb);
+  return __ffma2_rn(t, make_float2(LOG2E_F, LOG2E_F), mb);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
