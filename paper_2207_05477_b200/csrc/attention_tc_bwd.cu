@@ -311,18 +311,17 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
         const uint32_t id_q = tc::idesc_bf16(128, D, false, true);
         const uint32_t id_kv = tc::idesc_bf16(128, D, true, true);
         const uint32_t kbase = tc::smem_u32(sK) + (kc * 16) * DC * 128;
+        // three independent accumulation chains, interleaved so the tensor
+        // pipe always has a ready MMA (N = D is small: latency, not FLOPs)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint64_t a = tc::sdesc(tc::smem_u32(sdS) + k * 256, 128, 16 * 128);
           const uint64_t bb = tc::sdesc(kbase + k * 2 * DC * 128, DC * 128, 128);
-          tc::mma_bf16_ss(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
           const uint64_t a_ds = tc::sdesc(tc::smem_u32(sdS) + k * 2 * 16 * 128, 16 * 128, 128);
           const uint64_t a_p = tc::sdesc(tc::smem_u32(sP) + k * 2 * 16 * 128, 16 * 128, 128);
           const uint64_t b_q = tc::sdesc(tc::smem_u32(sQ) + k * 2 * DC * 128, DC * 128, 128);
           const uint64_t b_o = tc::sdesc(tc::smem_u32(sO) + k * 2 * DC * 128, DC * 128, 128);
+          tc::mma_bf16_ss(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
           tc::mma_bf16_ss(tbase + C_DK, a_ds, b_q, id_kv, k > 0 ? 1u : 0u);
           tc::mma_bf16_ss(tbase + C_DV, a_p, b_o, id_kv, k > 0 ? 1u : 0u);
         }

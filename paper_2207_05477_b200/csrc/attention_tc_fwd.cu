@@ -156,10 +156,23 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   if (b_lo < b_hi) fwd_stage<D, LP>(smem, qkvg, mask, g, b_lo, h, q0, tid);
   tc::cp_async_commit();
   uint32_t phase = 0;
+  constexpr int DH = D / 2;  // output channels of this thread (its half of the head)
+  const int64_t cbase = h * D + half * DH;
+  float bgv[DH];  // gate bias, loaded once
+#pragma unroll
+  for (int k = 0; k < DH; ++k) bgv[k] = bg[cbase + k];
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
     const int buf = F::NS == 2 ? (int)((b - b_lo) & 1) : 0;
     uint8_t* st = smem + buf * F::STAGE;
+    // this row's gate pre-activations: issued now, consumed after P.V
+    uint4 graw[DH / 8];
+    const int64_t tok = valid ? g.tok(b, i) : 0;
+    if (valid) {
+#pragma unroll
+      for (int k = 0; k < DH / 8; ++k)
+        graw[k] = __ldg(reinterpret_cast<const uint4*>(qkvg + tok * g.ld + 3 * HD + cbase) + k);
+    }
     tc::cp_async_wait0();
     tc::fence_proxy_async();
     tc::fence_before();
@@ -265,6 +278,22 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
       }
       tc::mma_commit(bar);
     }
+    // gate = sigmoid(g + bg) while the tensor core runs P.V
+    float gt[DH];
+    if (valid) {
+#pragma unroll
+      for (int k = 0; k < DH / 8; ++k) {
+        const uint32_t w4[4] = {graw[k].x, graw[k].y, graw[k].z, graw[k].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 gp = tc::bf16x2_f2(w4[q]);
+          gt[8 * k + 2 * q] = 1.0f / (1.0f + __expf(-(gp.x + bgv[8 * k + 2 * q])));
+          gt[8 * k + 2 * q + 1] = 1.0f / (1.0f + __expf(-(gp.y + bgv[8 * k + 2 * q + 1])));
+        }
+      }
+    }
+    const float l = sEx[256 + row] + sEx[384 + row];
+    const float invl = 1.0f / l;
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after();
@@ -274,9 +303,6 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     }
 
     // ---- epilogue: normalise, gate, store ----
-    const float l = sEx[256 + row] + sEx[384 + row];
-    const float invl = 1.0f / l;
-    constexpr int DH = D / 2;
     float o[DH];
     if constexpr (DH == 16) {
       tc::tmem_ld16(tl + F::OC + half * DH, o);
@@ -285,21 +311,15 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     }
     tc::wait_ld();
     if (valid) {
-      const int64_t t = g.tok(b, i);
-      const int64_t c0 = h * D + half * DH;
-      const bf16* gp = qkvg + t * g.ld + 3 * HD + c0;
-      float gpv[DH];
-#pragma unroll
-      for (int k = 0; k < DH / 8; ++k) bf16x8_to_f(*reinterpret_cast<const uint4*>(gp + 8 * k), gpv + 8 * k);
+      const int64_t t = tok;
+      const int64_t c0 = cbase;
       uint32_t pc[DH / 2], pg[DH / 2], pgd[DH / 2];
 #pragma unroll
       for (int k = 0; k < DH; k += 2) {
         const float c0f = o[k] * invl, c1f = o[k + 1] * invl;
-        const float g0 = 1.0f / (1.0f + __expf(-(gpv[k] + bg[c0 + k])));
-        const float g1 = 1.0f / (1.0f + __expf(-(gpv[k + 1] + bg[c0 + k + 1])));
         pc[k / 2] = tc::pack_bf16(c0f, c1f);
-        pg[k / 2] = tc::pack_bf16(g0, g1);
-        pgd[k / 2] = tc::pack_bf16(c0f * g0, c1f * g1);
+        pg[k / 2] = tc::pack_bf16(gt[k], gt[k + 1]);
+        pgd[k / 2] = tc::pack_bf16(c0f * gt[k], c1f * gt[k + 1]);
       }
 #pragma unroll
       for (int k = 0; k < DH / 8; ++k) {
