@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
 #pragma unroll 1
       for (int sub = 0; sub < 2; ++sub) {
         const int koff = kc * 128 + sub * 64;
-        if (tid == 0) {
+        if (warp == 0) {  // warp-collective issue (uniform descriptors)
           const uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
@@ -247,10 +247,10 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
             const uint64_t ao = tc::sdesc(tc::smem_u32(sO) + k * 256, 128, DC * 128);
             const uint64_t bk = tc::sdesc(tc::smem_u32(sK) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
             const uint64_t bv = tc::sdesc(tc::smem_u32(sV) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
-            tc::mma_bf16_ss(tbase + C_S, aq, bk, idesc, k > 0 ? 1u : 0u);
-            tc::mma_bf16_ss(tbase + C_DP, ao, bv, idesc, k > 0 ? 1u : 0u);
+            tc::mma_bf16_ss_w(tbase + C_S, aq, bk, idesc, k > 0 ? 1u : 0u);
+            tc::mma_bf16_ss_w(tbase + C_DP, ao, bv, idesc, k > 0 ? 1u : 0u);
           }
-          tc::mma_commit(&bar[0]);
+          tc::mma_commit_w(&bar[0]);
         }
         const int c0 = koff + cg * 16;  // this thread's 16 key columns
         uint32_t braw[8];
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
         tc::fence_after();
       }
       // ---- dQ += dS Kc ; dK = dS^T Q ; dV = P^T dO  (chunk of 128 keys) ----
-      if (tid == 0) {
+      if (warp == 0) {  // warp-collective issue (uniform descriptors)
         const uint32_t id_q = tc::idesc_bf16(128, D, false, true);
         const uint32_t id_kv = tc::idesc_bf16(128, D, true, true);
         const uint32_t kbase = tc::smem_u32(sK) + (kc * 16) * DC * 128;
@@ -321,11 +321,11 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
           const uint64_t a_p = tc::sdesc(tc::smem_u32(sP) + k * 2 * 16 * 128, 16 * 128, 128);
           const uint64_t b_q = tc::sdesc(tc::smem_u32(sQ) + k * 2 * DC * 128, DC * 128, 128);
           const uint64_t b_o = tc::sdesc(tc::smem_u32(sO) + k * 2 * DC * 128, DC * 128, 128);
-          tc::mma_bf16_ss(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
-          tc::mma_bf16_ss(tbase + C_DK, a_ds, b_q, id_kv, k > 0 ? 1u : 0u);
-          tc::mma_bf16_ss(tbase + C_DV, a_p, b_o, id_kv, k > 0 ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DK, a_ds, b_q, id_kv, k > 0 ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DV, a_p, b_o, id_kv, k > 0 ? 1u : 0u);
         }
-        tc::mma_commit(&bar[1]);
+        tc::mma_commit_w(&bar[1]);
       }
       tc::mbar_wait(&bar[1], ph1);
       ph1 ^= 1;

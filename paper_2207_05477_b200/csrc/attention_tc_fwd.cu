@@ -188,15 +188,15 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     const float* sMb = reinterpret_cast<const float*>(st + F::mb);
 
     // ---- S = Q K^T  (M=128, N=LP, K=D) ----
-    if (tid == 0) {
+    if (warp == 0) {  // warp-collective issue (uniform descriptors)
       const uint32_t idesc = tc::idesc_bf16(128, LP, false, false);
 #pragma unroll
       for (int k = 0; k < D / 16; ++k) {
         const uint64_t ad = tc::sdesc(tc::smem_u32(sQ) + k * 256, 128, DC * 128);
         const uint64_t bd = tc::sdesc(tc::smem_u32(sK) + k * 256, 128, DC * 128);
-        tc::mma_bf16_ss(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+        tc::mma_bf16_ss_w(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
       }
-      tc::mma_commit(bar);
+      tc::mma_commit_w(bar);
     }
     tc::mask_to_bias(const_cast<float*>(sMb), LP, L, tid, 256);
     __syncthreads();
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     __syncthreads();
 
     // ---- O = P V  (M=128, N=D, K=LP), A from TMEM ----
-    if (tid == 0) {
+    if (warp == 0) {  // warp-collective issue (uniform descriptors)
       tc::fence_after();
       const uint32_t idesc = tc::idesc_bf16(128, D, false, true);
 #pragma unroll 4
@@ -274,9 +274,9 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
         const int key0 = 16 * k;
         const uint32_t pcol = (key0 / HALF) * HALF + (key0 % HALF) / 2;
         const uint64_t bd = tc::sdesc(tc::smem_u32(sV) + k * 2 * DC * 128, DC * 128, 128);
-        tc::mma_bf16_ts(tbase + F::OC, tbase + pcol, bd, idesc, k > 0 ? 1u : 0u);
+        tc::mma_bf16_ts_w(tbase + F::OC, tbase + pcol, bd, idesc, k > 0 ? 1u : 0u);
       }
-      tc::mma_commit(bar);
+      tc::mma_commit_w(bar);
     }
     // gate = sigmoid(g + bg) while the tensor core runs P.V
     float gt[DH];
