@@ -369,8 +369,17 @@ def run_ours(args):
             ach = work / t / 1e9
             peak = peaks["hbm_gbs"]
             bound = "hbm"
+        traffic, traffic_src = None, None
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                tr = json.load(f).get(name)
+            if tr:
+                traffic = tr["traffic_bytes"]
+                traffic_src = f"profiles/r01_traffic.json ({tr['kernel']}, ncu --set full, per launch)"
         roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
-                    "frac": ach / peak, "traffic": None, "share_of_step": share,
+                    "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "share_of_step": share,
                     "peak_source": peaks["source"],
                     "candidates": {c[0]: {"us": c[1] * 1e6, "per_step": c[2],
                                           "achieved": (c[3] / c[1] / (1e12 if c[4] == "TFLOP/s" else 1e9)),
