@@ -61,26 +61,31 @@ struct BwdSmem {
   static constexpr int k = o + 128 * D * 2;
   static constexpr int v = k + LP * D * 2;
   static constexpr int mb = v + LP * D * 2;
-  static constexpr int NS = (D == 32 && LP == 256) ? 1 : 2;  // staging buffers (smem budget)
-  static constexpr int p = NS * STAGE;               // [128 x 128] bf16
+  static constexpr int p = 2 * STAGE;                // [128 x 128] bf16 (one 128-key chunk)
   static constexpr int ds = p + 128 * 128 * 2;
   static constexpr int bar = ds + 128 * 128 * 2;
-  static constexpr int slot = bar + 16;
-  static constexpr int BROW = LP + 8;                // padded bias row (bank spread)
-  static constexpr int bias = slot + 112;            // [128 x BROW] bf16, staged once
-  static constexpr int total = bias + 128 * BROW * 2;
+  static constexpr int bias = bar + 128;             // [128 x LP] bf16, 16-B chunks XOR-swizzled by row
+  static constexpr int total = bias + 128 * LP * 2;
 };
 
-// the CTA's bias rows nb[h, q0 + r, :] -> smem [128][LP + 8] (zero padded)
+// byte offset of (row r, 16-B chunk c) in the swizzled bias tile: the chunk
+// index is XORed with r & 7, so the 32 rows a warp reads at one column land in
+// 8 different bank groups (no padding needed, which keeps the D=32 / L=256
+// variant double-buffered inside 227 KB)
 template <int LP>
-__device__ __forceinline__ void stage_bias_tile(bf16* sB, const bf16* nb, int64_t h, int q0, int L,
+__device__ __forceinline__ int bias_off(int r, int c) {
+  return r * LP * 2 + ((c ^ (r & 7)) << 4);
+}
+
+// the CTA's bias rows nb[h, q0 + r, :] -> smem [128][LP] (zero padded)
+template <int LP>
+__device__ __forceinline__ void stage_bias_tile(uint8_t* sB, const bf16* nb, int64_t h, int q0, int L,
                                                 int tid, int nthreads) {
-  constexpr int BROW = LP + 8;
   constexpr int CPR = LP / 8;
   const bool vec_ok = (L % 8) == 0;
   for (int e = tid; e < 128 * CPR; e += nthreads) {
     const int r = e / CPR, c = e % CPR;
-    bf16* dst = sB + r * BROW + c * 8;
+    bf16* dst = reinterpret_cast<bf16*>(sB + bias_off<LP>(r, c));
     const int q = q0 + r;
     if (q < L && vec_ok && c * 8 + 8 <= L) {
       tc::cp_async16(dst, nb + ((size_t)h * L + q) * L + c * 8);
@@ -99,13 +104,7 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
                : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-      "r"(r[15]));
+  tc::tmem_st16u(taddr, reinterpret_cast<const uint32_t(&)[16]>(v));
 }
 __device__ __forceinline__ void tmem_zero(uint32_t taddr) {
   float z[16];
@@ -118,7 +117,7 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 template <int D, int LP>
 __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const bf16* dctx,
-                                          const float* mask, const AttnGeom& g, int64_t b,
+                                          const float* mbias, const AttnGeom& g, int64_t b,
                                           int64_t h, int q0, int tid) {
   using SM = BwdSmem<D, LP>;
   constexpr int DC = D / 8;
@@ -155,26 +154,71 @@ __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const b
   }
   for (int j = tid; j < LP; j += 512)
     if (j < L)
-      tc::cp_async4(sMb + j, mask + b * g.msb + (int64_t)j * g.msl);  // converted by mask_to_bias
+      tc::cp_async4(sMb + j, mbias + b * L + j);  // precomputed (m - 1) * 1e9 * log2(e)
     else
       sMb[j] = -INFINITY;
 }
 
+// advance a shared-memory descriptor by a byte offset (the start-address
+// field holds addr >> 4 in its low 14 bits; shared addresses stay < 256 KB)
+__device__ __forceinline__ uint64_t dadd(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
+
+// S = Q K^T and dP = dO V^T for the 64 keys at koff (one elected lane of the
+// calling warp issues; completion arrives on bar)
+template <int D>
+__device__ __forceinline__ void issue_sdp(uint32_t st, int koff, uint32_t tbase, uint32_t c_s, uint32_t c_dp,
+                                          uint64_t* bar, int q_off, int o_off, int k_off, int v_off) {
+  constexpr int DC = D / 8;
+  const uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
+  const uint64_t aq = tc::sdesc(st + q_off, 128, DC * 128);
+  const uint64_t ao = tc::sdesc(st + o_off, 128, DC * 128);
+  const uint64_t bk = tc::sdesc(st + k_off + (koff / 8) * DC * 128, 128, DC * 128);
+  const uint64_t bv = tc::sdesc(st + v_off + (koff / 8) * DC * 128, 128, DC * 128);
+#pragma unroll
+  for (int k = 0; k < D / 16; ++k) {
+    tc::mma_bf16_ss_w(tbase + c_s, dadd(aq, k * 256), dadd(bk, k * 256), idesc, k > 0 ? 1u : 0u);
+    tc::mma_bf16_ss_w(tbase + c_dp, dadd(ao, k * 256), dadd(bv, k * 256), idesc, k > 0 ? 1u : 0u);
+  }
+  tc::mma_commit_w(bar);
+}
+
+// Warp-specialised, software-pipelined backward (17 warps, one CTA per SM).
+//
+// Warp 16 issues every tcgen05.mma; warps 0..15 run the softmax backward
+// (TMEM lane quarter = warp & 3, 16-key column group = warp >> 2).  They talk
+// through four mbarriers only -- no CTA-wide barrier inside the batch loop:
+//   barS    (MMA -> softmax)  S/dP of sub-chunk j are in TMEM
+//   barSf   (softmax -> MMA)  all 16 warps copied S/dP(j) out (and, at a batch
+//                              boundary, the next batch's staging landed):
+//                              the MMA warp issues S/dP(j+1) into the same
+//                              columns, overlapping the softmax of j
+//   barPdS  (softmax -> MMA)  P/dS of a 128-key chunk are in shared memory and
+//                              the previous chunk's dK/dV/dQ are drained
+//   barKV   (MMA -> softmax)  dQ/dK/dV of the chunk are complete
+// The dQ/dK/dV MMAs of chunk c run while the softmax warps compute the first
+// sub-chunk of c+1; they are drained (and batch b-1's staging buffer is
+// refilled with batch b+1 by cp.async) just before P/dS of c+1 are stored.
+// The bias gradient is accumulated in TMEM across the whole batch group.
+// (A 32-key, double-buffered-S/dP variant with 8 or 16 softmax warps was
+// measured slower: its per-sub-chunk handshake latency dominates.)
 template <int D, int LP, bool BIAS>
-__global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
-    const bf16* __restrict__ qkvg, const bf16* __restrict__ dctx, const float* __restrict__ mask,
+__global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
+    const bf16* __restrict__ qkvg, const bf16* __restrict__ dctx, const float* __restrict__ mbias,
     const bf16* __restrict__ nb, const float* __restrict__ lse, const float* __restrict__ Dvec,
     bf16* __restrict__ dqkvg, bf16* __restrict__ kvpart, float* __restrict__ dnb_part,
     AttnGeom g, float scale, int NG) {
   using SM = BwdSmem<D, LP>;
   constexpr int DC = D / 8;
   constexpr int NKC = LP / 128;
+  constexpr int NSUB = LP / 64;
+  constexpr int NCW = 16;  // softmax warps
   constexpr uint32_t C_S = 0, C_DP = 64, C_DQ = 128, C_DK = 128 + D, C_DV = 128 + 2 * D, C_DB = 256;
   extern __shared__ __align__(128) uint8_t smem[];
   bf16* sP = reinterpret_cast<bf16*>(smem + SM::p);
   bf16* sdS = reinterpret_cast<bf16*>(smem + SM::ds);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + SM::slot);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);  // [0] S, [1] KV
+  uint64_t* bar2 = bar + 2;                                      // [0] Sf, [1] PdS
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = blockIdx.x;
@@ -185,185 +229,121 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
   const int64_t HD = g.H * D;
   const int64_t b_lo = (g.B * grp) / NG, b_hi = (g.B * (grp + 1)) / NG;
 
-  const int quarter = warp & 3, cg = warp >> 2;  // TMEM lane quarter, column group
+  const int quarter = warp & 3, cg = (warp >> 2) & 3;
   const int row = quarter * 32 + lane;
   const int i = q0 + row;
-  const bool valid = i < L;
-  const bf16* sBrow = reinterpret_cast<const bf16*>(smem + SM::bias) + row * SM::BROW;
+  const bool valid = i < L && warp < NCW;
 
-  if (warp == 0) tc::tmem_alloc<512>(slot);
-  if (tid == 32) {
+  if (warp == NCW) tc::tmem_alloc<512>(slot);
+  if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar2[0], NCW);
+    tc::mbar_init(&bar2[1], NCW);
+  }
+  if (warp < NCW) {
+    if (BIAS) stage_bias_tile<LP>(smem + SM::bias, nb, h, q0, L, tid, 512);
+    if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mbias, g, b_lo, h, q0, tid);
+    cp_async_commit();
+    cp_async_wait0();
+    tc::fence_proxy_async();
   }
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = *slot;
   const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
-  if (BIAS) {
-#pragma unroll
-    for (int c = 0; c < LP / 4; c += 16) tmem_zero(tl + C_DB + cg * (LP / 4) + c);
-  }
-  uint32_t ph0 = 0, ph1 = 0;
 
-  if (BIAS) stage_bias_tile<LP>(reinterpret_cast<bf16*>(smem + SM::bias), nb, h, q0, L, tid, 512);
-  if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mask, g, b_lo, h, q0, tid);
-  cp_async_commit();
-
-  for (int64_t b = b_lo; b < b_hi; ++b) {
-    const int buf = SM::NS == 2 ? (int)((b - b_lo) & 1) : 0;
-    uint8_t* st = smem + buf * SM::STAGE;
-    cp_async_wait0();
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (SM::NS == 2 && b + 1 < b_hi)
-      bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mask, g, b + 1, h, q0, tid);
-    cp_async_commit();
-    const bf16* sQ = reinterpret_cast<const bf16*>(st + SM::q);
-    const bf16* sO = reinterpret_cast<const bf16*>(st + SM::o);
-    const bf16* sK = reinterpret_cast<const bf16*>(st + SM::k);
-    const bf16* sV = reinterpret_cast<const bf16*>(st + SM::v);
-    const float* sMb = reinterpret_cast<const float*>(st + SM::mb);
-    const int64_t bh = b * g.H + h;
-    const float m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
-    const float rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
-    const float Dv = valid ? Dvec[g.tok(b, i) * g.H + h] : 0.f;
-    tc::mask_to_bias(const_cast<float*>(sMb), LP, L, tid, 512);
-    __syncthreads();
-
+  if (warp == NCW) {
+    // ======================= MMA issuer =======================
+    const int64_t nsub = (b_hi - b_lo) * NSUB;
+    const uint32_t s0 = tc::smem_u32(smem);
+    uint32_t phSf = 0, phP = 0;
+    const uint32_t id_q = tc::idesc_bf16(128, D, false, true);
+    const uint32_t id_kv = tc::idesc_bf16(128, D, true, true);
+    const uint64_t a_dq = tc::sdesc(tc::smem_u32(sdS), 128, 16 * 128);
+    const uint64_t a_ds = tc::sdesc(tc::smem_u32(sdS), 16 * 128, 128);
+    const uint64_t a_p = tc::sdesc(tc::smem_u32(sP), 16 * 128, 128);
+    if (nsub > 0) issue_sdp<D>(s0, 0, tbase, C_S, C_DP, &bar[0], SM::q, SM::o, SM::k, SM::v);
 #pragma unroll 1
-    for (int kc = 0; kc < NKC; ++kc) {
-#pragma unroll 1
-      for (int sub = 0; sub < 2; ++sub) {
-        const int koff = kc * 128 + sub * 64;
-        if (warp == 0) {  // warp-collective issue (uniform descriptors)
-          const uint32_t idesc = tc::idesc_bf16(128, 64, false, false);
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint64_t aq = tc::sdesc(tc::smem_u32(sQ) + k * 256, 128, DC * 128);
-            const uint64_t ao = tc::sdesc(tc::smem_u32(sO) + k * 256, 128, DC * 128);
-            const uint64_t bk = tc::sdesc(tc::smem_u32(sK) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
-            const uint64_t bv = tc::sdesc(tc::smem_u32(sV) + (koff / 8) * DC * 128 + k * 256, 128, DC * 128);
-            tc::mma_bf16_ss_w(tbase + C_S, aq, bk, idesc, k > 0 ? 1u : 0u);
-            tc::mma_bf16_ss_w(tbase + C_DP, ao, bv, idesc, k > 0 ? 1u : 0u);
-          }
-          tc::mma_commit_w(&bar[0]);
-        }
-        const int c0 = koff + cg * 16;  // this thread's 16 key columns
-        uint32_t braw[8];
-        if (BIAS) {
-          const uint4 u0 = *reinterpret_cast<const uint4*>(sBrow + c0);
-          const uint4 u1 = *reinterpret_cast<const uint4*>(sBrow + c0 + 8);
-          braw[0] = u0.x, braw[1] = u0.y, braw[2] = u0.z, braw[3] = u0.w;
-          braw[4] = u1.x, braw[5] = u1.y, braw[6] = u1.z, braw[7] = u1.w;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) braw[e] = 0u;
-        }
-        tc::mbar_wait(&bar[0], ph0);
-        ph0 ^= 1;
-        tc::fence_after();
-        float s[16], dp[16], acc[16];
-        tc::tmem_ld16(tl + C_S + cg * 16, s);
-        tc::tmem_ld16(tl + C_DP + cg * 16, dp);
-        if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
-        tc::wait_ld();
-        uint32_t pp[8], pd[8];
-        const float2 nm2 = make_float2(-m2, -m2), rl2 = make_float2(rl, rl), nD2 = make_float2(-Dv, -Dv);
-#pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          const float4 mb4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
-#pragma unroll
-          for (int u = 0; u < 4; u += 2) {
-            const float2 x = tc::logit2(make_float2(s[e + u], s[e + u + 1]), tc::bf16x2_f2(braw[(e + u) / 2]),
-                                        u == 0 ? make_float2(mb4.x, mb4.y) : make_float2(mb4.z, mb4.w), scale);
-            const float2 xd = __fadd2_rn(x, nm2);
-            const float2 p = __fmul2_rn(make_float2(tc::ex2(xd.x), tc::ex2(xd.y)), rl2);
-            const float2 d = __fmul2_rn(p, __fadd2_rn(make_float2(dp[e + u], dp[e + u + 1]), nD2));
-            if (BIAS) {
-              const float2 a = __fadd2_rn(make_float2(acc[e + u], acc[e + u + 1]), d);
-              acc[e + u] = a.x, acc[e + u + 1] = a.y;
-            }
-            pp[(e + u) / 2] = tc::pack_bf16(p.x, p.y);
-            pd[(e + u) / 2] = tc::pack_bf16(d.x, d.y);
-          }
-        }
-        if (BIAS) tmem_st16(tl + C_DB + c0, acc);
-        // P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B
-        const int kcol = sub * 64 + cg * 16;
-#pragma unroll
-        for (int qd = 0; qd < 2; ++qd) {
-          const int off = ((row >> 3) * 16 + (kcol >> 3) + qd) * 64 + (row & 7) * 8;
-          *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
-          *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
-        }
-        if (BIAS) tc::wait_st();
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
+    for (int64_t j = 0; j < nsub; ++j) {
+      const int sj = (int)(j % NSUB);
+      const uint32_t st = s0 + (uint32_t)((j / NSUB) & 1) * SM::STAGE;
+      tc::mbar_wait(&bar2[0], phSf);
+      phSf ^= 1;
+      tc::fence_after();
+      if (j + 1 < nsub) {
+        const int sj2 = (int)((j + 1) % NSUB);
+        const uint32_t st2 = s0 + (uint32_t)(((j + 1) / NSUB) & 1) * SM::STAGE;
+        issue_sdp<D>(st2, sj2 * 64, tbase, C_S, C_DP, &bar[0], SM::q, SM::o, SM::k, SM::v);
       }
-      // ---- dQ += dS Kc ; dK = dS^T Q ; dV = P^T dO  (chunk of 128 keys) ----
-      if (warp == 0) {  // warp-collective issue (uniform descriptors)
-        const uint32_t id_q = tc::idesc_bf16(128, D, false, true);
-        const uint32_t id_kv = tc::idesc_bf16(128, D, true, true);
-        const uint32_t kbase = tc::smem_u32(sK) + (kc * 16) * DC * 128;
-        // three independent accumulation chains, interleaved so the tensor
-        // pipe always has a ready MMA (N = D is small: latency, not FLOPs)
+      if (sj & 1) {
+        const int kc = sj >> 1;
+        tc::mbar_wait(&bar2[1], phP);
+        phP ^= 1;
+        tc::fence_after();
+        // dQ += dS Kc ; dK = dS^T Q ; dV = P^T dO   (chunk of 128 keys)
+        const uint64_t b_k = tc::sdesc(st + SM::k + (kc * 16) * DC * 128, DC * 128, 128);
+        const uint64_t b_q = tc::sdesc(st + SM::q, DC * 128, 128);
+        const uint64_t b_o = tc::sdesc(st + SM::o, DC * 128, 128);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const uint64_t a = tc::sdesc(tc::smem_u32(sdS) + k * 256, 128, 16 * 128);
-          const uint64_t bb = tc::sdesc(kbase + k * 2 * DC * 128, DC * 128, 128);
-          const uint64_t a_ds = tc::sdesc(tc::smem_u32(sdS) + k * 2 * 16 * 128, 16 * 128, 128);
-          const uint64_t a_p = tc::sdesc(tc::smem_u32(sP) + k * 2 * 16 * 128, 16 * 128, 128);
-          const uint64_t b_q = tc::sdesc(tc::smem_u32(sQ) + k * 2 * DC * 128, DC * 128, 128);
-          const uint64_t b_o = tc::sdesc(tc::smem_u32(sO) + k * 2 * DC * 128, DC * 128, 128);
-          tc::mma_bf16_ss_w(tbase + C_DQ, a, bb, id_q, (kc > 0 || k > 0) ? 1u : 0u);
-          tc::mma_bf16_ss_w(tbase + C_DK, a_ds, b_q, id_kv, k > 0 ? 1u : 0u);
-          tc::mma_bf16_ss_w(tbase + C_DV, a_p, b_o, id_kv, k > 0 ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DQ, dadd(a_dq, k * 256), dadd(b_k, k * 2 * DC * 128), id_q,
+                            (kc > 0 || k > 0) ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DK, dadd(a_ds, k * 4096), dadd(b_q, k * 2 * DC * 128), id_kv,
+                            k > 0 ? 1u : 0u);
+          tc::mma_bf16_ss_w(tbase + C_DV, dadd(a_p, k * 4096), dadd(b_o, k * 2 * DC * 128), id_kv,
+                            k > 0 ? 1u : 0u);
         }
         tc::mma_commit_w(&bar[1]);
       }
-      tc::mbar_wait(&bar[1], ph1);
-      ph1 ^= 1;
-      tc::fence_after();
-      // drain dK / dV of this chunk: lanes = keys, cg -> (dK|dV, column half)
-      {
-        const int key = kc * 128 + row;
-        const int region = cg >> 1, chalf = cg & 1;
-        constexpr int DH = D / 2;
-        float vv[DH];
-        const uint32_t col = (region ? C_DV : C_DK) + chalf * DH;
-        if constexpr (DH == 16) tc::tmem_ld16(tl + col, vv);
-        else tc::tmem_ld8(tl + col, vv);
-        tc::wait_ld();
-        if (key < L) {
-          const float sc = region ? 1.0f : scale;
-          uint32_t pk[DH / 2];
+    }
+  } else if (b_lo < b_hi) {
+    // ======================= softmax backward =======================
+    if (BIAS) {
 #pragma unroll
-          for (int e = 0; e < DH; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * sc, vv[e + 1] * sc);
-          const int64_t t = g.tok(b, key);
-          bf16* dst = (qt == 0) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
-                                : kvpart + t * 2 * HD + region * HD + h * D + chalf * DH;
+      for (int c = 0; c < LP / 4; c += 16) tmem_zero(tl + C_DB + cg * (LP / 4) + c);
+    }
+    uint32_t phS = 0, phKV = 0;
+    bool kv_pending = false;
+    int64_t pend_b = b_lo;
+    int pend_c = 0;
+    auto row_consts = [&](int64_t b, float& m2, float& rl, float& Dv) {
+      const int64_t bh = b * g.H + h;
+      m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
+      rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
+      Dv = valid ? Dvec[g.tok(b, i) * g.H + h] : 0.f;
+    };
+    float m2, rl, Dv, m2n = 0.f, rln = 0.f, Dvn = 0.f;
+    row_consts(b_lo, m2, rl, Dv);
+    // batch b_lo + 1 into the second buffer (nothing has read it yet)
+    if (b_lo + 1 < b_hi) bwd_stage<D, LP>(smem + SM::STAGE, qkvg, dctx, mbias, g, b_lo + 1, h, q0, tid);
+    cp_async_commit();
+
+    // drain dK / dV of chunk c of batch b: lanes = keys, cg -> (dK|dV, column half)
+    auto drain_kv = [&](int64_t b, int c) {
+      const int key = c * 128 + row;
+      const int region = cg >> 1, chalf = cg & 1;
+      constexpr int DH = D / 2;
+      float vv[DH];
+      const uint32_t col = (region ? C_DV : C_DK) + chalf * DH;
+      if constexpr (DH == 16) tc::tmem_ld16(tl + col, vv);
+      else tc::tmem_ld8(tl + col, vv);
+      tc::wait_ld();
+      if (key < L) {
+        const float sc = region ? 1.0f : scale;
+        uint32_t pk[DH / 2];
 #pragma unroll
-          for (int k = 0; k < DH / 8; ++k)
-            reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-        }
+        for (int e = 0; e < DH; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * sc, vv[e + 1] * sc);
+        const int64_t t = g.tok(b, key);
+        bf16* dst = (qt == 0) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
+                              : kvpart + t * 2 * HD + region * HD + h * D + chalf * DH;
+#pragma unroll
+        for (int k = 0; k < DH / 8; ++k)
+          reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
       }
-      tc::fence_before();
-      __syncthreads();
-      tc::fence_after();
-    }
-    // single staging buffer: every MMA of this batch has completed, prefetch the next
-    if (SM::NS == 1 && b + 1 < b_hi) {
-      bwd_stage<D, LP>(smem, qkvg, dctx, mask, g, b + 1, h, q0, tid);
-      cp_async_commit();
-    }
-    // ---- drain dQ ----
-    {
+    };
+    auto drain_dq = [&](int64_t b) {
       constexpr int DQ = D / 4;
       float vv[8];
       if constexpr (DQ == 8) {
@@ -386,13 +366,116 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
         else
           *reinterpret_cast<uint2*>(dst) = make_uint2(pk[0], pk[1]);
       }
+    };
+
+#pragma unroll 1
+    for (int64_t b = b_lo; b < b_hi; ++b) {
+      const int buf = (int)((b - b_lo) & 1);
+      const float* sMb = reinterpret_cast<const float*>(smem + buf * SM::STAGE + SM::mb);
+      const bool has_next = b + 1 < b_hi;
+      if (has_next) row_consts(b + 1, m2n, rln, Dvn);  // consumed at the next batch
+      const float2 nm2 = make_float2(-m2, -m2), rl2 = make_float2(rl, rl), nD2 = make_float2(-Dv, -Dv);
+#pragma unroll 1
+      for (int sj = 0; sj < NSUB; ++sj) {
+        const int kc = sj >> 1, sub = sj & 1;
+        const bool last_in_batch = sj == NSUB - 1;
+        const int c0 = sj * 64 + cg * 16;  // this thread's 16 key columns
+        uint32_t braw[8];
+        if (BIAS) {
+          const uint4 u0 = *reinterpret_cast<const uint4*>(smem + SM::bias + bias_off<LP>(row, c0 >> 3));
+          const uint4 u1 = *reinterpret_cast<const uint4*>(smem + SM::bias + bias_off<LP>(row, (c0 >> 3) + 1));
+          braw[0] = u0.x, braw[1] = u0.y, braw[2] = u0.z, braw[3] = u0.w;
+          braw[4] = u1.x, braw[5] = u1.y, braw[6] = u1.z, braw[7] = u1.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) braw[e] = 0u;
+        }
+        float mbv[16];
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(sMb + c0 + e);
+          mbv[e] = t4.x, mbv[e + 1] = t4.y, mbv[e + 2] = t4.z, mbv[e + 3] = t4.w;
+        }
+        // ---- S/dP(j) out of TMEM, then hand the columns back ----
+        tc::mbar_wait(&bar[0], phS);
+        phS ^= 1;
+        tc::fence_after();
+        float s[16], dp[16], acc[16];
+        tc::tmem_ld16(tl + C_S + cg * 16, s);
+        tc::tmem_ld16(tl + C_DP + cg * 16, dp);
+        if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
+        tc::wait_ld();
+        if (last_in_batch && has_next) {  // batch b+1's staging (own copies) has landed
+          cp_async_wait0();
+          tc::fence_proxy_async();
+        }
+        tc::fence_before();
+        tc::mbar_arrive_warp(&bar2[0]);
+        // ---- P, dS, bias gradient ----
+        uint32_t pp[8], pd[8];
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          const float2 x = tc::logit2(make_float2(s[e], s[e + 1]), tc::bf16x2_f2(braw[e / 2]),
+                                      make_float2(mbv[e], mbv[e + 1]), scale);
+          const float2 xd = __fadd2_rn(x, nm2);
+          const float2 p = __fmul2_rn(make_float2(tc::ex2(xd.x), tc::ex2(xd.y)), rl2);
+          const float2 d = __fmul2_rn(p, __fadd2_rn(make_float2(dp[e], dp[e + 1]), nD2));
+          if (BIAS) {
+            const float2 a = __fadd2_rn(make_float2(acc[e], acc[e + 1]), d);
+            acc[e] = a.x, acc[e + 1] = a.y;
+          }
+          pp[e / 2] = tc::pack_bf16(p.x, p.y);
+          pd[e / 2] = tc::pack_bf16(d.x, d.y);
+        }
+        if (BIAS) tmem_st16(tl + C_DB + c0, acc);
+        // ---- previous chunk's dQ/dK/dV: wait, drain, recycle its staging ----
+        if (sub == 0 && kv_pending) {
+          tc::mbar_wait(&bar[1], phKV);
+          phKV ^= 1;
+          tc::fence_after();
+          drain_kv(pend_b, pend_c);
+          if (pend_c == NKC - 1) {
+            drain_dq(pend_b);
+            // every MMA that read batch b-1's buffer is complete: prefetch b+1 into it
+            if (has_next) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mbias, g, b + 1, h, q0, tid);
+            cp_async_commit();
+          }
+          kv_pending = false;
+        }
+        // ---- P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B ----
+        const int kcol = sub * 64 + cg * 16;
+#pragma unroll
+        for (int qd = 0; qd < 2; ++qd) {
+          const int off = ((row >> 3) * 16 + (kcol >> 3) + qd) * 64 + (row & 7) * 8;
+          *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
+          *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
+        }
+        if (sub == 1) {
+          tc::fence_proxy_async();
+          tc::fence_before();
+          tc::mbar_arrive_warp(&bar2[1]);
+          kv_pending = true;
+          pend_b = b;
+          pend_c = kc;
+        }
+        if (BIAS) tc::wait_st();
+      }
+      m2 = m2n, rl = rln, Dv = Dvn;
     }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
+    // ---- last chunk's dQ/dK/dV ----
+    if (kv_pending) {
+      tc::mbar_wait(&bar[1], phKV);
+      tc::fence_after();
+      drain_kv(pend_b, pend_c);
+      drain_dq(pend_b);
+    }
+  } else if (BIAS) {  // empty batch group: zero bias-gradient partial
+#pragma unroll
+    for (int c = 0; c < LP / 4; c += 16) tmem_zero(tl + C_DB + cg * (LP / 4) + c);
+    tc::wait_st();
   }
   // ---- bias-gradient partial of this batch group ----
-  if (BIAS) {
+  if (BIAS && warp < NCW) {
     constexpr int PER = LP / 4;
 #pragma unroll 1
     for (int c = 0; c < PER; c += 16) {
@@ -416,7 +499,7 @@ __global__ void __launch_bounds__(512, 1) attn_bwd_tc_kernel(
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+  if (warp == NCW) tc::tmem_dealloc<512>(tbase);
 }
 
 // token-major, 8 channels per thread: dctx = dgated*gate (bf16, the dO the
@@ -425,7 +508,15 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
     const bf16* __restrict__ ctx, const bf16* __restrict__ gate, const bf16* __restrict__ dgated,
     bf16* __restrict__ dqkvg, bf16* __restrict__ dctx, float* __restrict__ Dvec, int64_t T, int H,
-    int64_t ld) {
+    int64_t ld, const float* __restrict__ mask, int64_t msb, int64_t msl, float* __restrict__ mbias,
+    int64_t B, int64_t L) {
+  // key-mask bias of every (batch, key), [b][l] contiguous, in the log2
+  // domain of the softmax: (m - 1) * 1e9 * log2(e)  (src/attention.py:151)
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * L;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / L, l = e % L;
+    mbias[e] = (mask[b * msb + l * msl] - 1.0f) * tc::MASK_BIAS_L2;
+  }
   constexpr int G = D / 8;  // threads per head
   const int64_t HD8 = (int64_t)H * D / 8;
   const int64_t n = T * HD8;
@@ -514,7 +605,7 @@ bool tc_disabled() {
 
 struct BwdPlan {
   int NQT, NG, LP;
-  int64_t off_dctx, off_dvec, off_kv, off_part, off_cols, total;
+  int64_t off_dctx, off_dvec, off_mb, off_kv, off_part, off_cols, total;
 };
 
 BwdPlan bwd_plan(const AttnGeom& g) {
@@ -531,7 +622,8 @@ BwdPlan bwd_plan(const AttnGeom& g) {
   auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
   p.off_dctx = 0;
   p.off_dvec = p.off_dctx + al(T * HD * 2);
-  p.off_kv = p.off_dvec + al(g.B * g.H * g.L * 4);
+  p.off_mb = p.off_dvec + al(g.B * g.H * g.L * 4);
+  p.off_kv = p.off_mb + al(g.B * g.L * 4);
   p.off_part = p.off_kv + (p.NQT > 1 ? al(T * 2 * HD * 2) : 0);
   p.off_cols = p.off_part + al((int64_t)p.NG * g.H * g.L * g.L * 4);
   p.total = p.off_cols + al((int64_t)(EVO_PARTIAL_BLOCKS > 8 * num_sms() ? EVO_PARTIAL_BLOCKS : 8 * num_sms()) * HD * 4);
@@ -558,7 +650,7 @@ void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const voi
   }
   dim3 grid((unsigned)p.NG, (unsigned)g.H, (unsigned)p.NQT);
   const float scale = (float)(1.0 / sqrt((double)D));
-  k<<<grid, 512, SM::total, s>>>((const bf16*)qkvg, dctx, mask, (const bf16*)nb, lse, Dvec,
+  k<<<grid, 544, SM::total, s>>>((const bf16*)qkvg, dctx, mask, (const bf16*)nb, lse, Dvec,
                                  (bf16*)dqkvg, kvpart, part, g, scale, p.NG);
   EVO_LAUNCH_CHECK();
   count_launch(1);
@@ -598,6 +690,7 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   bf16* kvpart = (bf16*)(w + p.off_kv);
   float* part = (float*)(w + p.off_part);
   float* cols = (float*)(w + p.off_cols);
+  float* mbias = (float*)(w + p.off_mb);
   const int64_t T = g.B * g.L, HD = g.H * g.D;
   {
     const int64_t nthr = T * HD / 8;
@@ -605,18 +698,20 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
     if (g.D == 16)
       attn_bwd_prep_tc_kernel<16><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
-                                                         Dvec, T, (int)g.H, g.ld);
+                                                         Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
+                                                         mbias, g.B, g.L);
     else
       attn_bwd_prep_tc_kernel<32><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
-                                                         Dvec, T, (int)g.H, g.ld);
+                                                         Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
+                                                         mbias, g.B, g.L);
     EVO_LAUNCH_CHECK();
   }
   const bool bias = nb != nullptr && dnb != nullptr;
   if (g.D == 16)
-    launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
   else
-    launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
   if (p.NQT > 1) {
     attn_kv_combine_kernel<<<cdiv(T * 2 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, kvpart, T, g.ld, HD);
     EVO_LAUNCH_CHECK();
