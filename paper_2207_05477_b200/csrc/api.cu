@@ -69,6 +69,9 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
                int sdt, int ddt, int unpack, cudaStream_t s);
 
 // tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
+bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
+             int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
+             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s);
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
                  int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
@@ -236,6 +239,9 @@ int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int tr
   cudaStream_t s = (cudaStream_t)stream;
   if (gemm_tc_try(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, ldc, stride_c,
                   batch, alpha, beta, ab_dtype, c_dtype, s))
+    return EVO_OK;
+  if (gemm_lt(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, C, ldc, stride_c, batch,
+              alpha, beta, ab_dtype, c_dtype, 0, nullptr, s))
     return EVO_OK;
   cublasHandle_t h = blas_handle(s);
   // row-major C = op(A) op(B)  <=>  column-major C^T = op(B)^T op(A)^T

@@ -1,0 +1,74 @@
+"""Record every evo_gemm call of one block fwd+bwd at the bench shape, then
+time each distinct (M, N, K, ta, tb, dtypes) in isolation with CUDA events.
+
+    python tools/gemm_shapes.py
+"""
+import os
+import sys
+from collections import Counter
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2207_05477_b200 import ops  # noqa: E402
+from paper_2207_05477_b200.model import ModelConfig  # noqa: E402
+from paper_2207_05477_b200.trainer import ExecutionPlan, Trainer  # noqa: E402
+
+
+def main():
+    cfg = ModelConfig(n_blocks=1, n_seq=128, n_res=256, c_m=256, c_z=128, heads=8, opm_dim=32)
+    tr = Trainer.create(cfg, ExecutionPlan(act_dtype="bf16", fixed_recycles=1))
+    tr.engine.forward_backward(tr.feats, 1)
+    torch.cuda.synchronize()
+    calls = []
+    orig = ops.call
+
+    def rec(name, *args):
+        if name == "evo_gemm":
+            M, N, K = args[0], args[1], args[2]
+            ta, tb, batch = args[5], args[9], args[14]
+            ad, cd = args[17], args[18]
+            calls.append((M, N, K, ta, tb, batch, ad, cd))
+        return orig(name, *args)
+
+    ops.call = rec
+    tr.engine.forward_backward(tr.feats, 1)
+    ops.call = orig
+    torch.cuda.synchronize()
+    cnt = Counter(calls)
+    dt = {0: torch.float32, 1: torch.bfloat16}
+    tot_t = tot_f = 0.0
+    rows = []
+    for (M, N, K, ta, tb, batch, ad, cd), n in cnt.items():
+        a = torch.randn((K, M) if ta else (M, K), device="cuda").to(dt.get(ad, torch.bfloat16))
+        b = torch.randn((N, K) if tb else (K, N), device="cuda").to(dt.get(ad, torch.bfloat16))
+        c = torch.empty((M, N), device="cuda", dtype=dt.get(cd, torch.float32))
+        if batch != 1:
+            continue
+        for _ in range(3):
+            ops.gemm(a, b, c, ta=bool(ta), tb=bool(tb))
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            for _ in range(20):
+                ops.gemm(a, b, c, ta=bool(ta), tb=bool(tb))
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        fl = 2.0 * M * N * K
+        tot_t += us * n
+        tot_f += fl * n
+        rows.append((us * n, M, N, K, ta, tb, ad, cd, n, us, fl / us / 1e6))
+    for r in sorted(rows, reverse=True):
+        print(f"M={r[1]:6d} N={r[2]:6d} K={r[3]:6d} ta={r[4]} tb={r[5]} a{r[6]} c{r[7]} x{r[8]}  "
+              f"{r[9]:8.1f} us  {r[10]:7.1f} TF/s  total {r[0]:8.1f} us")
+    print(f"per block: {tot_t:.1f} us, {tot_f / tot_t / 1e6:.1f} TF/s")
+
+
+if __name__ == "__main__":
+    main()
