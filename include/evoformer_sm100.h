@@ -74,6 +74,17 @@ int evo_gemm(int64_t M, int64_t N, int64_t K,
              void* C, int64_t ldc, int64_t stride_c, int batch,
              float alpha, float beta, int ab_dtype, int c_dtype, void* stream);
 
+/* Projection with its module epilogue fused (replaces the np.matmul + bias +
+ * residual of src/attention.py:173 / src/model.py:346-348, 378 and the
+ * matmul + bias + relu of src/model.py:346):
+ *   out[M,N] = op(A) . op(B) + bias[N] (+ res[M,N])      relu == 0
+ *   out[M,N] = relu(op(A) . op(B) + bias[N])              relu == 1, res == NULL
+ * res may alias nothing else; res_dtype is its storage dtype. */
+int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
+                  const void* B, int64_t ldb, int trans_b, const void* res, int res_dtype,
+                  const float* bias, int relu, void* out, int64_t ldo, int ab_dtype, int c_dtype,
+                  void* stream);
+
 /* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
  * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */
 int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const float* beta,

@@ -262,6 +262,41 @@ int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int tr
   EVO_API_END
 }
 
+int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
+                  int64_t ldb, int trans_b, const void* res, int res_dtype, const float* bias, int relu,
+                  void* out, int64_t ldo, int ab_dtype, int c_dtype, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0, EVO_ERR_ARG, "gemm_bias: bad extents");
+  EVO_REQUIRE(!(relu && res), EVO_ERR_ARG, "gemm_bias: relu with a residual is not a module of the path");
+  if (M == 0 || N == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool fuse_res = res != nullptr && res_dtype == c_dtype;
+  if (gemm_lt(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, fuse_res ? res : out, out, ldo, 0, 1, 1.0f,
+              fuse_res ? 1.0f : 0.0f, ab_dtype, c_dtype, relu ? 2 : 1, bias, s)) {
+    if (res && !fuse_res) {  // residual of another dtype: add it after the fused bias
+      EVO_REQUIRE(ldo == N, EVO_ERR_ARG, "gemm_bias: strided output with a mixed-dtype residual");
+      static float* zero = nullptr;
+      static int64_t zn = 0;
+      if (zn < N) {
+        if (zero) EVO_CUDA(cudaFree(zero));
+        EVO_CUDA(cudaMalloc(&zero, N * sizeof(float)));
+        EVO_CUDA(cudaMemset(zero, 0, N * sizeof(float)));
+        zn = N;
+      }
+      return evo_bias_residual(res, res_dtype, out, c_dtype, zero, out, c_dtype, M, N, stream);
+    }
+    return EVO_OK;
+  }
+  // library fallback: plain GEMM, then the glue kernel
+  const int rc = evo_gemm(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, out, ldo, 0, 1, 1.0f, 0.0f, ab_dtype,
+                          c_dtype, stream);
+  if (rc != EVO_OK) return rc;
+  EVO_REQUIRE(ldo == N, EVO_ERR_ARG, "gemm_bias: strided output needs the fused path");
+  if (relu) return evo_bias_relu(out, c_dtype, bias, M, N, stream);
+  return evo_bias_residual(res, res ? res_dtype : EVO_F32, out, c_dtype, bias, out, c_dtype, M, N, stream);
+  EVO_API_END
+}
+
 int evo_bias_residual(const void* res, int res_dtype, const void* y, int y_dtype, const float* bias,
                       void* out, int out_dtype, int64_t rows, int64_t C, void* stream) {
   EVO_API_BEGIN

@@ -172,10 +172,8 @@ class BlockEngine:
         mask = self.mask(feats, v.mask)
         ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, v.msb, v.msl, nb,
                                              self.P(f"{prefix}.attn.bg"), v.B, v.L, H, D, v.sb, v.sl)
-        y = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.gemm(gated, self.W(f"{prefix}.attn.wo", HD), y)
         out = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.bias_residual(x, y, self.P(f"{prefix}.attn.bo"), out)
+        ops.gemm_bias(gated, self.W(f"{prefix}.attn.wo", HD), out, self.P(f"{prefix}.attn.bo"), res=x)
         saved = dict(x=x, xl=xl, mu=mu, rs=rs, qkvg=qkvg, ctx=ctx, gate=gate, gated=gated, lse=lse,
                      nb=nb, pmu=pmu, prs=prs, pair=pair if pair is not None else x)
         return out, saved
@@ -226,12 +224,9 @@ class BlockEngine:
         xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
         w1 = self.W(f"{prefix}.w1", C)
         h = torch.empty((T, w1.shape[1]), dtype=dt, device=x.device)
-        ops.gemm(xl, w1, h)
-        ops.bias_relu_(h, self.P(f"{prefix}.b1"))
-        y = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.gemm(h, self.W(f"{prefix}.w2", w1.shape[1]), y)
+        ops.gemm_bias(xl, w1, h, self.P(f"{prefix}.b1"), relu=True)
         out = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.bias_residual(x, y, self.P(f"{prefix}.b2"), out)
+        ops.gemm_bias(h, self.W(f"{prefix}.w2", w1.shape[1]), out, self.P(f"{prefix}.b2"), res=x)
         return out, dict(x=x, xl=xl, mu=mu, rs=rs, h=h)
 
     def trans_bwd(self, d, sv, prefix):
@@ -271,10 +266,8 @@ class BlockEngine:
         ops.gemm(a.view(S, R * k), c.view(S, R * k), num, ta=True)
         rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt)
         del num
-        y = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
-        ops.gemm(outn, self.W(f"{prefix}.w_out", k * k), y)
-        out = torch.empty_like(y)
-        ops.bias_residual(pair_res, y, self.P(f"{prefix}.b_out"), out)
+        out = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
+        ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res)
         return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
 
     def opm_bwd_core(self, d, sv, prefix, feats):

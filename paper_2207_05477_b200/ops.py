@@ -68,6 +68,25 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, ta: bool = False, tb
          ptr(c), c.stride(0), 0, 1, alpha, beta, dcode(a), dcode(c), stream())
 
 
+def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.Tensor,
+              res: torch.Tensor | None = None, relu: bool = False, ta: bool = False, tb: bool = False):
+    """out = op(a) @ op(b) + bias (+ res), or relu(op(a) @ op(b) + bias): the
+    projection with its module epilogue fused (one kernel on the Lt path)."""
+    for t in (a, b, out):
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("gemm operands must be 2-D with unit inner stride")
+    M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
+    Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
+    if K != Kb or tuple(out.shape) != (M, N) or bias.numel() != N:
+        raise ValueError(f"gemm_bias shape mismatch: op(a)={M}x{K} op(b)={Kb}x{N} out={tuple(out.shape)}")
+    if res is not None and (tuple(res.shape) != (M, N) or not res.is_contiguous() or not out.is_contiguous()):
+        raise ValueError("gemm_bias: residual must be a contiguous [M, N] like out")
+    call("evo_gemm_bias", M, N, K, ptr(a), a.stride(0), int(ta), ptr(b), b.stride(0), int(tb), ptr(res),
+         dcode(res) if res is not None else F32, ptr(bias), int(relu), ptr(out), out.stride(0), dcode(a),
+         dcode(out), stream())
+    return out
+
+
 def gemm_batched(a, b, c, batch, sa, sb, sc, ta=False, tb=False, alpha=1.0, beta=0.0):
     """Strided-batched row-major GEMM on flat buffers: operand k of batch i is
     the matrix at data_ptr + i*s (elements); a, b, c are 2-D views of batch 0."""
