@@ -66,43 +66,71 @@ struct Fwd {
   static constexpr int total = slot + 8;
 };
 
+// Per-thread staging plan: the (row, 16-B column chunk) pairs of the Q, K, V
+// tiles a thread copies are the same for every batch, so their global offsets
+// (minus the batch term) and shared-memory offsets are computed once; a batch
+// then costs one add and one cp.async per chunk.
 template <int D, int LP>
-__device__ __forceinline__ void fwd_stage(uint8_t* st, const bf16* qkvg, const float* mask,
-                                          const AttnGeom& g, int64_t b, int64_t h, int q0, int tid) {
+struct FwdStager {
   using F = Fwd<D, LP>;
-  constexpr int DC = F::DC;
-  const int L = (int)g.L;
-  const int64_t HD = g.H * D;
-  bf16* sQ = reinterpret_cast<bf16*>(st + F::q);
-  bf16* sK = reinterpret_cast<bf16*>(st + F::k);
-  bf16* sV = reinterpret_cast<bf16*>(st + F::v);
-  float* sMb = reinterpret_cast<float*>(st + F::mb);
-  for (int e = tid; e < 128 * DC; e += 256) {
-    const int r = e / DC, c = e % DC;
-    bf16* dst = sQ + ((r >> 3) * DC + c) * 64 + (r & 7) * 8;
-    if (q0 + r < L)
-      tc::cp_async16(dst, qkvg + g.tok(b, q0 + r) * g.ld + h * D + c * 8);
-    else
-      st_zero16(dst);
+  static constexpr int DC = F::DC;
+  static constexpr int NQ = (128 * DC + 255) / 256;
+  static constexpr int NK = (LP * DC + 255) / 256;
+  int qoff[NQ], koff[NK];      // element offsets from the batch's token-row base; -1 = zero-fill
+  int qdst[NQ], kdst[NK];      // byte offsets inside a stage
+  int moff;                    // mask element offset (-1: none / beyond L)
+  int mdst;
+  __device__ __forceinline__ void init(const AttnGeom& g, int64_t h, int q0, int tid) {
+    const int L = (int)g.L;
+    const int64_t HD = g.H * D;
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int e = tid + u * 256;
+      const int r = e / DC, c = e % DC;
+      qdst[u] = e < 128 * DC ? F::q + (((r >> 3) * DC + c) * 64 + (r & 7) * 8) * 2 : -1;
+      qoff[u] = (e < 128 * DC && q0 + r < L) ? (int)((q0 + r) * g.sl * g.ld + h * D + c * 8) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < NK; ++u) {
+      const int e = tid + u * 256;
+      const int j = e / DC, c = e % DC;
+      kdst[u] = e < LP * DC ? (((j >> 3) * DC + c) * 64 + (j & 7) * 8) * 2 : -1;
+      koff[u] = (e < LP * DC && j < L) ? (int)(j * g.sl * g.ld + HD + h * D + c * 8) : -1;
+    }
+    mdst = tid < LP ? F::mb + tid * 4 : -1;
+    moff = tid < L ? (int)(tid * g.msl) : -1;
   }
-  for (int e = tid; e < LP * DC; e += 256) {
-    const int j = e / DC, c = e % DC;
-    const int off = ((j >> 3) * DC + c) * 64 + (j & 7) * 8;
-    if (j < L) {
-      const bf16* src = qkvg + g.tok(b, j) * g.ld + HD + h * D + c * 8;
-      tc::cp_async16(sK + off, src);
-      tc::cp_async16(sV + off, src + HD);
-    } else {
-      st_zero16(sK + off);
-      st_zero16(sV + off);
+  // Q, K and the key mask of batch b
+  __device__ __forceinline__ void qkm(uint8_t* st, const bf16* qkvg, const float* mask, const AttnGeom& g,
+                                      int64_t b) const {
+    const bf16* base = qkvg + b * g.sb * g.ld;
+#pragma unroll
+    for (int u = 0; u < NQ; ++u)
+      if (qdst[u] >= 0) {
+        if (qoff[u] >= 0) tc::cp_async16(st + qdst[u], base + qoff[u]);
+        else st_zero16(st + qdst[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < NK; ++u)
+      if (kdst[u] >= 0) {
+        if (koff[u] >= 0) tc::cp_async16(st + F::k + kdst[u], base + koff[u]);
+        else st_zero16(st + F::k + kdst[u]);
+      }
+    if (mdst >= 0) {
+      if (moff >= 0) tc::cp_async4(st + mdst, mask + b * g.msb + moff);  // converted by mask_to_bias
+      else *reinterpret_cast<float*>(st + mdst) = -INFINITY;
     }
   }
-  for (int j = tid; j < LP; j += 256)
-    if (j < L)
-      tc::cp_async4(sMb + j, mask + b * g.msb + (int64_t)j * g.msl);  // converted by mask_to_bias
-    else
-      sMb[j] = -INFINITY;
-}
+  __device__ __forceinline__ void v(uint8_t* st, const bf16* qkvg, const AttnGeom& g, int64_t b) const {
+    const bf16* base = qkvg + b * g.sb * g.ld + g.H * D;
+#pragma unroll
+    for (int u = 0; u < NK; ++u)
+      if (kdst[u] >= 0) {
+        if (koff[u] >= 0) tc::cp_async16(st + F::v + kdst[u], base + koff[u]);
+        else st_zero16(st + F::v + kdst[u]);
+      }
+  }
+};
 
 template <int LP>
 __device__ __forceinline__ void stage_bias_rows(bf16* sB, const bf16* nb, int64_t h, int q0, int L,
@@ -126,7 +154,7 @@ __device__ __forceinline__ void stage_bias_rows(bf16* sB, const bf16* nb, int64_
 }
 
 template <int D, int LP, bool BIAS>
-__global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
+__global__ void __launch_bounds__(256, 2) attn_fwd_tc_kernel(
     const bf16* __restrict__ qkvg, const float* __restrict__ mask, const bf16* __restrict__ nb,
     const float* __restrict__ bg, bf16* __restrict__ ctx, bf16* __restrict__ gate,
     bf16* __restrict__ gated, float* __restrict__ lse, AttnGeom g, float scale, int NG) {
@@ -153,7 +181,12 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
   if (warp == 0) tc::tmem_alloc<F::TCOLS>(slot);
   if (tid == 32) tc::mbar_init(bar, 1);
   if (BIAS) stage_bias_rows<LP>(reinterpret_cast<bf16*>(smem + F::bias), nb, h, q0, L, tid);
-  if (b_lo < b_hi) fwd_stage<D, LP>(smem, qkvg, mask, g, b_lo, h, q0, tid);
+  FwdStager<D, LP> stg;
+  stg.init(g, h, q0, tid);
+  if (b_lo < b_hi) {
+    stg.qkm(smem, qkvg, mask, g, b_lo);
+    stg.v(smem, qkvg, g, b_lo);
+  }
   tc::cp_async_commit();
   uint32_t phase = 0;
   constexpr int DH = D / 2;  // output channels of this thread (its half of the head)
@@ -180,7 +213,10 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     tc::fence_after();
     const uint32_t tbase = *slot;
     const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
-    if (F::NS == 2 && b + 1 < b_hi) fwd_stage<D, LP>(smem + (buf ^ 1) * F::STAGE, qkvg, mask, g, b + 1, h, q0, tid);
+    if (F::NS == 2 && b + 1 < b_hi) {
+      stg.qkm(smem + (buf ^ 1) * F::STAGE, qkvg, mask, g, b + 1);
+      stg.v(smem + (buf ^ 1) * F::STAGE, qkvg, g, b + 1);
+    }
     tc::cp_async_commit();
     const bf16* sQ = reinterpret_cast<const bf16*>(st + F::q);
     const bf16* sK = reinterpret_cast<const bf16*>(st + F::k);
@@ -239,6 +275,10 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     sEx[half * 128 + row] = mx;
     __syncthreads();
     const float m = fmaxf(sEx[row], sEx[128 + row]);
+    if (F::NS == 1 && b + 1 < b_hi) {  // Q, K (S is done) and the mask (pass 1 is done) are free
+      stg.qkm(smem, qkvg, mask, g, b + 1);
+      tc::cp_async_commit();
+    }
 
     // ---- pass 2: P = exp2(logits - m), packed bf16 pairs back into TMEM ----
     float2 sum2 = make_float2(0.f, 0.f);
@@ -287,8 +327,8 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float2 gp = tc::bf16x2_f2(w4[q]);
-          gt[8 * k + 2 * q] = 1.0f / (1.0f + __expf(-(gp.x + bgv[8 * k + 2 * q])));
-          gt[8 * k + 2 * q + 1] = 1.0f / (1.0f + __expf(-(gp.y + bgv[8 * k + 2 * q + 1])));
+          gt[8 * k + 2 * q] = __fdividef(1.0f, 1.0f + __expf(-(gp.x + bgv[8 * k + 2 * q])));
+          gt[8 * k + 2 * q + 1] = __fdividef(1.0f, 1.0f + __expf(-(gp.y + bgv[8 * k + 2 * q + 1])));
         }
       }
     }
@@ -297,8 +337,8 @@ __global__ void __launch_bounds__(256) attn_fwd_tc_kernel(
     tc::mbar_wait(bar, phase);
     phase ^= 1;
     tc::fence_after();
-    if (F::NS == 1 && b + 1 < b_hi) {  // all MMAs of this batch are done with smem
-      fwd_stage<D, LP>(smem, qkvg, mask, g, b + 1, h, q0, tid);
+    if (F::NS == 1 && b + 1 < b_hi) {  // P.V is done with V
+      stg.v(smem, qkvg, g, b + 1);
       tc::cp_async_commit();
     }
 
