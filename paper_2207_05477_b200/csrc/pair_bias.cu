@@ -8,6 +8,8 @@
 // Backward fuses dP -> dLN -> LayerNorm backward -> dz (+=) with the
 // w_bias / LN-affine gradient partials in one pass over the pair.
 #include "common.cuh"
+#include "vec.cuh"
+#include <type_traits>
 #include "reduce.cuh"
 
 namespace evo {
@@ -162,6 +164,131 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
 bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
                        float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap,
                        cudaStream_t s);
+
+// Thread-per-token forward: each thread owns one token row (no cross-lane
+// reductions at all), reads it three times from L1 (sum, squared deviation,
+// projection), and keeps the 8 head accumulators in registers; LN affine and
+// w_bias are broadcast from shared memory.  Threads walk the tokens in output
+// order -- for the transposed triangle-end layout (swap) thread i handles token
+// (i % R, i / R) -- so the 8 head planes of nb are written coalesced.
+__device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int C, typename T>
+__global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
+    const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
+    const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
+    float* __restrict__ rstd, int64_t R, int H, int swap) {
+  __shared__ float4 sw[C][2];   // w[c, 0..7] (zero beyond H)
+  __shared__ float2 sgb[C];     // (gamma, beta)
+  for (int e = threadIdx.x; e < C; e += blockDim.x) {
+    float t[8];
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh) t[hh] = hh < H ? w[e * H + hh] : 0.f;
+    sw[e][0] = make_float4(t[0], t[1], t[2], t[3]);
+    sw[e][1] = make_float4(t[4], t[5], t[6], t[7]);
+    sgb[e] = make_float2(g[e], b[e]);
+  }
+  __syncthreads();
+  const int64_t RR = R * R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < RR; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tok = swap ? (i % R) * R + i / R : i;
+    const T* row = z + tok * C;
+    constexpr bool IN_REGS = C * sizeof(T) <= 256;  // whole row in registers: every load in flight at once
+    constexpr int NV = IN_REGS ? C / 8 : 1;
+    Vec8<T> rv[NV];
+    if constexpr (IN_REGS) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) ldv8(row + 8 * k, rv[k]);
+    }
+    auto chunk = [&](int c, float (&f)[8]) {
+      if constexpr (IN_REGS) {
+        cvt8(rv[c / 8], f);
+      } else {
+        Vec8<T> v;
+        ldv8(row + c, v);
+        cvt8(v, f);
+      }
+    };
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; c += 8) {
+      float f[8];
+      chunk(c, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += f[e];
+    }
+    const float mu = s / (float)C;
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; c += 8) {
+      float f[8];
+      chunk(c, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = f[e] - mu;
+        q += d * d;
+      }
+    }
+    const float inv = rsqrtf(q / (float)C + 1e-5f);
+    float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int c = 0; c < C; c += 8) {
+      float f[8];
+      chunk(c, f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        // volatile shared loads: keeps the compiler from hoisting all C x 10
+        // broadcast weights into registers (the row already holds C/2 of them)
+        float2 gb;
+        float4 w0, w1;
+        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(gb.x), "=f"(gb.y) : "r"(tc_smem_u32(&sgb[c + e])));
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w0.x), "=f"(w0.y), "=f"(w0.z), "=f"(w0.w)
+                     : "r"(tc_smem_u32(&sw[c + e][0])));
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w1.x), "=f"(w1.y), "=f"(w1.z), "=f"(w1.w)
+                     : "r"(tc_smem_u32(&sw[c + e][1])));
+        const float zl = (f[e] - mu) * inv * gb.x + gb.y;
+        const float2 z2 = make_float2(zl, zl);
+        p[0] = __ffma2_rn(z2, make_float2(w0.x, w0.y), p[0]);
+        p[1] = __ffma2_rn(z2, make_float2(w0.z, w0.w), p[1]);
+        p[2] = __ffma2_rn(z2, make_float2(w1.x, w1.y), p[2]);
+        p[3] = __ffma2_rn(z2, make_float2(w1.z, w1.w), p[3]);
+      }
+    }
+    const float ph[8] = {p[0].x, p[0].y, p[1].x, p[1].y, p[2].x, p[2].y, p[3].x, p[3].y};
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh)
+      if (hh < H) nb[hh * RR + i] = from_f<T>(ph[hh]);
+    mean[tok] = mu;
+    rstd[tok] = inv;
+  }
+}
+
+bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
+                       float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap, cudaStream_t s) {
+  if (H > 8 || (C % 8) != 0 || (((uintptr_t)z) & 15) != 0) return false;
+  const int64_t RR = R * R;
+  const unsigned grid = (unsigned)((RR + 127) / 128);
+  bool done = true;
+  auto go = [&](auto cc) {
+    constexpr int CC = decltype(cc)::value;
+    EVO_DISPATCH_T(dt, T, {
+      pair_bias_fwd_tpt_kernel<CC, T><<<grid, 128, 0, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd, R,
+                                                           (int)H, swap);
+    });
+  };
+  if (C == 32) go(std::integral_constant<int, 32>{});
+  else if (C == 64) go(std::integral_constant<int, 64>{});
+  else if (C == 128) go(std::integral_constant<int, 128>{});
+  else if (C == 256) go(std::integral_constant<int, 256>{});
+  else done = false;
+  if (done) {
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+  }
+  return done;
+}
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
@@ -181,6 +308,8 @@ int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* 
   EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
   if (R == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pair_bias_fwd_tpt(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, C, H, swap_xy, s))
+    return EVO_OK;
   if (pair_bias_fwd_vec(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, C, H, swap_xy, s))
     return EVO_OK;
   unsigned grid = cdiv(R * R, PB_WARPS);

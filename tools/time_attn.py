@@ -14,11 +14,17 @@ from paper_2207_05477_b200 import ops  # noqa: E402
 def timeit(fn, reps=20):
     for _ in range(3):
         fn()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(reps):
+            fn()
+    gr.replay()
+    torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(reps):
-        fn()
+    gr.replay()
     e1.record(s)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps * 1e3
