@@ -14,6 +14,7 @@
 //   EPI_RELU_BIAS   D = relu(op(A) op(B) + bias[col])
 // and C may differ from D (D = AB + bias + C: the residual add of a module).
 #include <cublasLt.h>
+#include <cstdio>
 
 #include <map>
 #include <mutex>
@@ -28,6 +29,8 @@ namespace {
 
 struct LtState {
   cublasLtHandle_t h = nullptr;
+  __nv_bfloat16* bias16 = nullptr;  // bf16 copy of an epilogue bias (Lt wants Dtype biases)
+  int64_t bias16_n = 0;
   void* ws = nullptr;
   size_t ws_bytes = 0;
   void* scratch = nullptr;
@@ -43,8 +46,15 @@ LtState& lt_state() {
     if (cublasLtCreate(&s.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasLtCreate failed");
     s.ws_bytes = size_t(32) << 20;
     EVO_CUDA(cudaMalloc(&s.ws, s.ws_bytes));
+    s.bias16_n = 1 << 16;
+    EVO_CUDA(cudaMalloc(&s.bias16, s.bias16_n * sizeof(__nv_bfloat16)));
   }
   return s;
+}
+
+__global__ void bias_to_bf16_kernel(const float* __restrict__ b, __nv_bfloat16* __restrict__ o, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __float2bfloat16_rn(b[i]);
 }
 
 cudaDataType_t lt_dt(int d) { return d == EVO_F32 ? CUDA_R_32F : CUDA_R_16BF; }
@@ -98,7 +108,9 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   if (env_off()) return false;
   // small problems are launch-bound: keep them on the default cuBLAS path
   // (no timing-dependent algorithm choice where it cannot pay)
-  if (epi == 0 && (double)M * N * K * batch < (double)(1 << 28)) return false;
+  // (fused epilogues included: Lt wants a bf16 bias for bf16 outputs, a rounding
+  // that is only worth paying where the fused kernel saves a pass over HBM)
+  if ((double)M * N * K * batch < (double)(1 << 28)) return false;
   LtState& st = lt_state();
   // column-major view: D^T[N, M] = op(B)^T op(A)^T  ->  Lt A := B, Lt B := A
   const cublasOperation_t opA = tb ? CUBLAS_OP_T : CUBLAS_OP_N;
@@ -111,10 +123,16 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   if (epi == 1) e = CUBLASLT_EPILOGUE_BIAS;
   if (epi == 2) e = CUBLASLT_EPILOGUE_RELU_BIAS;
   if (epi) {
+    // the bias must have the output's dtype: bf16 outputs get a bf16 copy
+    const void* bptr = bias;
+    if (c_dtype == EVO_BF16) {
+      if (N > st.bias16_n) return false;
+      bias_to_bf16_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(bias, st.bias16, N);
+      EVO_LAUNCH_CHECK();
+      bptr = st.bias16;
+    }
     LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &e, sizeof(e)));
-    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias)));
-    const cudaDataType_t bdt = CUDA_R_32F;
-    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bdt, sizeof(bdt)));
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bptr, sizeof(bptr)));
   }
   const cudaDataType_t abt = lt_dt(ab_dtype), ct = lt_dt(c_dtype);
   // Lt A = our B: stored [K x N] row-major (op N) == col-major N x K with ld ldb
@@ -148,7 +166,12 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
     const cublasStatus_t hs =
         cublasLtMatmulAlgoGetHeuristic(st.h, ds.op, ds.a, ds.b, ds.c, ds.d, pref, 16, res, &nres);
     cublasLtMatmulPreferenceDestroy(pref);
-    if (hs != CUBLAS_STATUS_SUCCESS || nres == 0) return false;
+    if (hs != CUBLAS_STATUS_SUCCESS || nres == 0) {
+      if (getenv("EVO_GEMM_DEBUG"))
+        fprintf(stderr, "gemm_lt heuristic: M=%lld N=%lld K=%lld epi=%d status=%d nres=%d\n", (long long)M,
+                (long long)N, (long long)K, epi, (int)hs, nres);
+      return false;
+    }
     Choice ch{res[0].algo, false};
     if (!capturing && nres > 1) {
       // time every candidate into a scratch D (C untouched)
@@ -193,6 +216,9 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   }
   const cublasStatus_t rs = cublasLtMatmul(st.h, ds.op, &alpha, B, ds.a, A, ds.b, &beta, Cin, ds.c, D, ds.d,
                                            &it->second.algo, st.ws, st.ws_bytes, s);
+  if (rs != CUBLAS_STATUS_SUCCESS && getenv("EVO_GEMM_DEBUG"))
+    fprintf(stderr, "gemm_lt: M=%lld N=%lld K=%lld epi=%d status=%d\n", (long long)M, (long long)N, (long long)K,
+            epi, (int)rs);
   return rs == CUBLAS_STATUS_SUCCESS;
 }
 

@@ -248,3 +248,25 @@ def test_layernorm_bwd_ex_fused_outputs():
     assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
     assert torch.equal(dx16, dx.to(torch.bfloat16))
     assert rel(dxs, dx.double().sum(0).float()) <= 1e-5
+
+
+@pytest.mark.parametrize("relu,with_res", [(False, True), (False, False), (True, False)])
+@pytest.mark.parametrize("T,K,N", [(32768, 256, 256), (65536, 128, 512), (8192, 1024, 128)])
+def test_gemm_bias_fused_epilogue_vs_torch(relu, with_res, T, K, N):
+    """Projection + module epilogue (bias [+ residual] or bias + ReLU) in one
+    kernel (evo_gemm_bias, cuBLASLt epilogue) against fp32 torch, at the
+    bench shapes where the fused path is taken."""
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(T + K + N)
+    a = (torch.randn(T, K, device="cuda") * 0.5).bfloat16()
+    w = (torch.randn(K, N, device="cuda") / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda") * 0.1
+    res = torch.randn(T, N, device="cuda").bfloat16() if with_res else None
+    out = torch.empty(T, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm_bias(a, w, out, bias, res=res, relu=relu)
+    ref = a.float() @ w.float() + bias
+    if with_res:
+        ref = ref + res.float()
+    if relu:
+        ref = ref.clamp_min(0)
+    assert rel(out.float(), ref) <= 1e-2
