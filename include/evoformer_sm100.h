@@ -85,6 +85,22 @@ int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
                   const float* bias, int relu, void* out, int64_t ldo, int ab_dtype, int c_dtype,
                   void* stream);
 
+/* Projection with a training epilogue, for the transition's ReLU and the
+ * bias gradients (replaces the np.maximum / np.sum steps of src/model.py:346
+ * and their tape backward):
+ *   epi 3  D = relu(op(A).op(B) + vec[N]); aux <- ReLU bit mask (aux_ld bits/row, %128)
+ *   epi 4  D = op(A).op(B) * relu'(aux)                    (dReLU with that mask)
+ *   epi 5  D = op(A).op(B) + beta*D; vec[N] (+)= ... column sums of op(B)  (fp32 D)
+ *   epi 6  as 5 with the row sums of op(A) (length M)
+ * Returns EVO_ERR_UNSUPPORTED when no fused kernel exists for the problem; the
+ * caller then runs the unfused sequence.  (Measured on B200, tools/epi_time.py:
+ * the library's dReLU / bias-gradient epilogues are 2-4x slower than the
+ * unfused GEMM + relu_bwd_colsum, so the engine does not route through them.) */
+int evo_gemm_epilogue(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
+                      const void* B, int64_t ldb, int trans_b, void* D, int64_t ldd, float beta,
+                      int epi, float* vec, void* aux, int64_t aux_ld, int ab_dtype, int c_dtype,
+                      void* stream);
+
 /* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
  * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */
 int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const float* beta,

@@ -71,7 +71,8 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
 // tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
 bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
-             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s);
+             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s,
+             void* aux = nullptr, int64_t aux_ld = 0);
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
                  int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
@@ -259,6 +260,18 @@ int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int tr
                                     CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
   EVO_REQUIRE(st == CUBLAS_STATUS_SUCCESS, EVO_ERR_CUDA,
               "cublasGemmEx failed with status " + std::to_string((int)st));
+  EVO_API_END
+}
+
+int evo_gemm_epilogue(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
+                      int64_t ldb, int trans_b, void* D, int64_t ldd, float beta, int epi, float* vec, void* aux,
+                      int64_t aux_ld, int ab_dtype, int c_dtype, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0 && epi >= 3 && epi <= 6, EVO_ERR_ARG, "gemm_epilogue: bad arguments");
+  if (M == 0 || N == 0) return EVO_OK;
+  if (!gemm_lt(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, D, D, ldd, 0, 1, 1.0f, beta, ab_dtype, c_dtype,
+               epi, vec, (cudaStream_t)stream, aux, aux_ld))
+    return EVO_ERR_UNSUPPORTED;
   EVO_API_END
 }
 

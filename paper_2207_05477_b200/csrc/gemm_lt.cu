@@ -93,6 +93,13 @@ struct Descs {
   }
 };
 
+}  // namespace
+
+enum { EPI_NONE = 0, EPI_BIAS = 1, EPI_RELU_BIAS = 2, EPI_RELU_AUX_BIAS = 3, EPI_DRELU = 4, EPI_BGRADA = 5,
+       EPI_BGRADB = 6 };
+
+namespace {
+
 #define LT_OK(x)                                   \
   do {                                             \
     if ((x) != CUBLAS_STATUS_SUCCESS) return false; \
@@ -104,7 +111,8 @@ struct Descs {
 // Returns false (caller falls back) when Lt rejects the problem.
 bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
-             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s) {
+             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s,
+             void* aux, int64_t aux_ld) {
   if (env_off()) return false;
   // small problems are launch-bound: keep them on the default cuBLAS path
   // (no timing-dependent algorithm choice where it cannot pay)
@@ -120,9 +128,26 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_TRANSA, &opA, sizeof(opA)));
   LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_TRANSB, &opB, sizeof(opB)));
   cublasLtEpilogue_t e = CUBLASLT_EPILOGUE_DEFAULT;
-  if (epi == 1) e = CUBLASLT_EPILOGUE_BIAS;
-  if (epi == 2) e = CUBLASLT_EPILOGUE_RELU_BIAS;
-  if (epi) {
+  if (epi == EPI_BIAS) e = CUBLASLT_EPILOGUE_BIAS;
+  if (epi == EPI_RELU_BIAS) e = CUBLASLT_EPILOGUE_RELU_BIAS;
+  if (epi == EPI_RELU_AUX_BIAS) e = CUBLASLT_EPILOGUE_RELU_AUX_BIAS;
+  if (epi == EPI_DRELU) e = CUBLASLT_EPILOGUE_DRELU;
+  if (epi == EPI_BGRADA) e = CUBLASLT_EPILOGUE_BGRADA;
+  if (epi == EPI_BGRADB) e = CUBLASLT_EPILOGUE_BGRADB;
+  if (epi == EPI_RELU_AUX_BIAS || epi == EPI_DRELU) {
+    if (!aux || (aux_ld % 128) != 0 || aux_ld < N) return false;
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_POINTER, &aux, sizeof(aux)));
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_LD, &aux_ld, sizeof(aux_ld)));
+  }
+  if (epi == EPI_DRELU) {
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &e, sizeof(e)));
+  } else if (epi == EPI_BGRADA || epi == EPI_BGRADB) {
+    // bias-gradient output has the output's dtype: only fp32 outputs keep fp32 sums
+    if (c_dtype != EVO_F32) return false;
+    void* gptr = const_cast<float*>(bias);
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &e, sizeof(e)));
+    LT_OK(cublasLtMatmulDescSetAttribute(ds.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &gptr, sizeof(gptr)));
+  } else if (epi) {
     // the bias must have the output's dtype: bf16 outputs get a bf16 copy
     const void* bptr = bias;
     if (c_dtype == EVO_BF16) {
