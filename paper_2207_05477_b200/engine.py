@@ -152,6 +152,20 @@ class BlockEngine:
     def mask(self, feats: DeviceFeatures, which: str):
         return feats.msa_mask if which == "msa" else feats.pair_mask
 
+    def _ln_bwd_chain(self, x, dxl, mu, rs, prefix, d, nxt):
+        """LayerNorm backward into the residual gradient d (in place).  With
+        ``nxt`` (the output-bias gradient slot of the module that runs next in
+        the backward) it also returns that module's bf16 operand d_act and
+        writes the bias gradient, so the module skips its colsum/cast pass."""
+        if nxt is None or self.dt != torch.bfloat16:
+            ops.layernorm_bwd(x, dxl, mu, rs, self.P(f"{prefix}.ln_g"), d, d, self.G(f"{prefix}.ln_g"),
+                              self.G(f"{prefix}.ln_b"))
+            return None
+        d_act = torch.empty(d.shape, dtype=self.dt, device=d.device)
+        ops.layernorm_bwd_ex(x, dxl, mu, rs, self.P(f"{prefix}.ln_g"), d, d, self.G(f"{prefix}.ln_g"),
+                             self.G(f"{prefix}.ln_b"), d_act, nxt)
+        return d_act
+
     # -- gated attention module (LN -> [pair bias] -> fused attention -> residual)
 
     def attn_fwd(self, x, prefix, v: Variant, feats, pair=None):
@@ -178,17 +192,20 @@ class BlockEngine:
                      nb=nb, pmu=pmu, prs=prs, pair=pair if pair is not None else x)
         return out, saved
 
-    def attn_bwd(self, d, sv, prefix, v: Variant, feats, dpair=None):
+    def attn_bwd(self, d, sv, prefix, v: Variant, feats, dpair=None, d_act=None, nxt=None):
         """``d`` (fp32 [T, C]) is d(out) on entry and d(x) on exit.  The
         pair-bias gradient is added into ``dpair`` (or ``d`` for triangle
-        attention, whose bias comes from its own input)."""
+        attention, whose bias comes from its own input).  ``d_act``: bf16 d(out)
+        with the output-bias gradient already taken (from the previous LN
+        backward); returns the next module's d_act when ``nxt`` is given."""
         cfg, dt = self.cfg, self.dt
         T, C = d.shape
         H = cfg.heads
         D = C // H
         HD = H * D
-        d_act = torch.empty((T, C), dtype=dt, device=d.device)
-        ops.colsum_cast(d, self.G(f"{prefix}.attn.bo"), y=d_act)
+        if d_act is None:
+            d_act = torch.empty((T, C), dtype=dt, device=d.device)
+            ops.colsum_cast(d, self.G(f"{prefix}.attn.bo"), y=d_act)
         ops.gemm(sv["gated"], d_act, self.Gm(f"{prefix}.attn.wo", HD), ta=True)
         dgated = torch.empty((T, HD), dtype=dt, device=d.device)
         ops.gemm(d_act, self.W(f"{prefix}.attn.wo", HD), dgated, tb=True)
@@ -206,15 +223,14 @@ class BlockEngine:
         dxl = torch.empty((T, C), dtype=F32, device=d.device)
         ops.gemm(dqkvg, self.wcat[prefix], dxl, tb=True)
         del dqkvg, dwcat
-        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d, d,
-                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
-        if v.bias:
+        if v.bias:  # before the LN backward, so d is final when that pass reads it
             target = dpair if dpair is not None else d
             ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
                               self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
                               v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
                               self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
                               cfg.n_res, H)
+        return self._ln_bwd_chain(sv["x"], dxl, sv["mu"], sv["rs"], prefix, d, nxt)
 
     # -- transition (src/model.py:344-348) ------------------------------------------
 
@@ -229,7 +245,7 @@ class BlockEngine:
         ops.gemm_bias(h, self.W(f"{prefix}.w2", w1.shape[1]), out, self.P(f"{prefix}.b2"), res=x)
         return out, dict(x=x, xl=xl, mu=mu, rs=rs, h=h)
 
-    def trans_bwd(self, d, sv, prefix):
+    def trans_bwd(self, d, sv, prefix, nxt=None):
         dt = self.dt
         T, C = d.shape
         h = sv["h"]
@@ -245,8 +261,7 @@ class BlockEngine:
         dxl = torch.empty((T, C), dtype=F32, device=d.device)
         ops.gemm(dh, self.W(f"{prefix}.w1", C), dxl, tb=True)
         del dh
-        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d, d,
-                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+        return self._ln_bwd_chain(sv["x"], dxl, sv["mu"], sv["rs"], prefix, d, nxt)
 
     # -- outer product mean (src/model.py:351-378) -----------------------------------
 
@@ -397,9 +412,10 @@ class BlockEngine:
         d(pair_in) into d_pair_acc."""
         p = f"block{i}"
         s1, s2, s3 = saved
-        self.trans_bwd(d_msa, s3, f"{p}.msa_trans")
-        self.attn_bwd(d_msa, s2, f"{p}.col_attn", self.var["col_attn"], feats)
-        self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc)
+        a = self.trans_bwd(d_msa, s3, f"{p}.msa_trans", nxt=self.G(f"{p}.col_attn.attn.bo"))
+        a = self.attn_bwd(d_msa, s2, f"{p}.col_attn", self.var["col_attn"], feats, d_act=a,
+                          nxt=self.G(f"{p}.row_attn.attn.bo"))
+        self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc, d_act=a)
 
     def pair_branch_fwd(self, i, pair_mid, feats):
         p = f"block{i}"
@@ -418,9 +434,10 @@ class BlockEngine:
         """d(pair_out) -> d(pair_mid) in place."""
         p = f"block{i}"
         tm, s1, s2, s3 = saved
-        self.trans_bwd(d_pair, s3, f"{p}.pair_trans")
-        self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats)
-        self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats)
+        a = self.trans_bwd(d_pair, s3, f"{p}.pair_trans", nxt=self.G(f"{p}.tri_end.attn.bo"))
+        a = self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats, d_act=a,
+                          nxt=self.G(f"{p}.tri_start.attn.bo"))
+        self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats, d_act=a)
         if tm:
             self.trimul_bwd(d_pair, tm[1], f"{p}.tri_mul_in", feats)
             self.trimul_bwd(d_pair, tm[0], f"{p}.tri_mul_out", feats)

@@ -189,6 +189,16 @@ def layernorm_bwd(x, dy, mean, rstd, g, dres, dx, dgamma, dbeta, accumulate=Fals
          ptr(dres), ptr(dx), ptr(dgamma), ptr(dbeta), int(accumulate), ptr(ws), rows, C, stream())
 
 
+def layernorm_bwd_ex(x, dy, mean, rstd, g, dres, dx, dgamma, dbeta, dx16, dxsum, accumulate=False):
+    """layernorm_bwd that also emits a bf16 copy of dx and its column sums:
+    the next module's GEMM operand and output-bias gradient in the same pass."""
+    rows, C = x.shape
+    ws = _ws(_lib.load().evo_layernorm_bwd_workspace(rows, C), x.device)
+    call("evo_layernorm_bwd_ex", ptr(x), dcode(x), ptr(dy), dcode(dy), ptr(mean), ptr(rstd), ptr(g),
+         ptr(dres), ptr(dx), ptr(dx16), ptr(dxsum), ptr(dgamma), ptr(dbeta), int(accumulate), ptr(ws), rows,
+         C, stream())
+
+
 def bias_residual(res, y, bias, out):
     rows, C = y.shape
     call("evo_bias_residual", ptr(res), dcode(res) if res is not None else F32, ptr(y), dcode(y),
