@@ -191,14 +191,30 @@ def kernel_candidates(trainer):
     out = []
     nblk = cfg.n_blocks
 
-    def timeit(fn, reps=20):
+    def timeit(fn, reps=20, graph=True):
+        """Device seconds per call (CUDA events on the launching stream); the
+        calls are replayed from a CUDA graph so host overhead cannot floor
+        short kernels."""
         s = torch.cuda.current_stream()
         for _ in range(3):
             fn()
+        torch.cuda.synchronize()
+        if graph:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for _ in range(reps):
+                    fn()
+            gr.replay()
+            torch.cuda.synchronize()
+            run = gr.replay
+        else:
+            def run():
+                for _ in range(reps):
+                    fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.current_stream()
         e0.record(s)
-        for _ in range(reps):
-            fn()
+        run()
         e1.record(s)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps / 1e3
@@ -237,7 +253,7 @@ def kernel_candidates(trainer):
 
     def opt():
         st.step()
-    t = timeit(opt, reps=5)
+    t = timeit(opt, reps=5, graph=False)
     out.append(("adam_clip_ema+sumsq", t, 1, n * 40 + (n * 2 if st.shadow is not None else 0), "GB/s"))
     return out
 
@@ -377,8 +393,20 @@ def run_ours(args):
             if tr:
                 traffic = tr["traffic_bytes"]
                 traffic_src = f"profiles/r01_traffic.json ({tr['kernel']}, ncu --set full, per launch)"
+        # the attention cores at head dims 16/32 are bound by the softmax exps
+        # (MUFU ex2, 16/clk/SM) and small-N tcgen05 issue, not by tensor FLOPs:
+        # report the ex2 roofline beside the tensor one
+        cfg_ = trainer.cfg
+        exps = {"attn_fwd[tri]": cfg_.n_res ** 3 * cfg_.heads, "attn_bwd[tri]": cfg_.n_res ** 3 * cfg_.heads,
+                "attn_fwd[row]": cfg_.n_seq * cfg_.n_res ** 2 * cfg_.heads}
+        ex2_peak = 148 * 16 * 1.965e9
+        ex2 = None
+        if name in exps:
+            ex2 = {"ex2_per_launch": exps[name], "achieved_per_s": exps[name] / t, "peak_per_s": ex2_peak,
+                   "frac": exps[name] / t / ex2_peak, "peak_source": "148 SMs x 16 MUFU.EX2/clk x 1965 MHz"}
         roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "ex2_roofline": ex2,
                     "share_of_step": share,
                     "peak_source": peaks["source"],
                     "candidates": {c[0]: {"us": c[1] * 1e6, "per_step": c[2],
