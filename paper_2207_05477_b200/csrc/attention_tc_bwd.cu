@@ -308,14 +308,14 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     bool kv_pending = false;
     int64_t pend_b = b_lo;
     int pend_c = 0;
-    auto row_consts = [&](int64_t b, float& m2, float& rl, float& Dv) {
+    // (1/rowsum is folded into dO' and D' by the prep kernel)
+    auto row_consts = [&](int64_t b, float& m2, float& Dv) {
       const int64_t bh = b * g.H + h;
-      m2 = valid ? lse[2 * (bh * L + i)] : 0.f;
-      rl = valid ? lse[2 * (bh * L + i) + 1] : 0.f;
+      m2 = valid ? lse[2 * (bh * L + i)] : INFINITY;  // P' = 0 on rows beyond L
       Dv = valid ? Dvec[g.tok(b, i) * g.H + h] : 0.f;
     };
-    float m2, rl, Dv, m2n = 0.f, rln = 0.f, Dvn = 0.f;
-    row_consts(b_lo, m2, rl, Dv);
+    float m2, Dv, m2n = 0.f, Dvn = 0.f;
+    row_consts(b_lo, m2, Dv);
     // batch b_lo + 1 into the second buffer (nothing has read it yet)
     if (b_lo + 1 < b_hi) bwd_stage<D, LP>(smem + SM::STAGE, qkvg, dctx, mbias, g, b_lo + 1, h, q0, tid);
     cp_async_commit();
@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
       const int buf = (int)((b - b_lo) & 1);
       const float* sMb = reinterpret_cast<const float*>(smem + buf * SM::STAGE + SM::mb);
       const bool has_next = b + 1 < b_hi;
-      if (has_next) row_consts(b + 1, m2n, rln, Dvn);  // consumed at the next batch
-      const float2 nm2 = make_float2(-m2, -m2), rl2 = make_float2(rl, rl), nD2 = make_float2(-Dv, -Dv);
+      if (has_next) row_consts(b + 1, m2n, Dvn);  // consumed at the next batch
+      const float2 nm2 = make_float2(-m2, -m2), nD2 = make_float2(-Dv, -Dv);
 #pragma unroll 1
       for (int sj = 0; sj < NSUB; ++sj) {
         const int kc = sj >> 1, sub = sj & 1;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           const float2 x = tc::logit2(make_float2(s[e], s[e + 1]), tc::bf16x2_f2(braw[e / 2]),
                                       make_float2(mbv[e], mbv[e + 1]), scale);
           const float2 xd = __fadd2_rn(x, nm2);
-          const float2 p = __fmul2_rn(make_float2(tc::ex2(xd.x), tc::ex2(xd.y)), rl2);
+          const float2 p = make_float2(tc::ex2(xd.x), tc::ex2(xd.y));
           const float2 d = __fmul2_rn(p, __fadd2_rn(make_float2(dp[e], dp[e + 1]), nD2));
           if (BIAS) {
             const float2 a = __fadd2_rn(make_float2(acc[e], acc[e + 1]), d);
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         }
         if (BIAS) tc::wait_st();
       }
-      m2 = m2n, rl = rln, Dv = Dvn;
+      m2 = m2n, Dv = Dvn;
     }
     // ---- last chunk's dQ/dK/dV ----
     if (kv_pending) {
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
     const bf16* __restrict__ ctx, const bf16* __restrict__ gate, const bf16* __restrict__ dgated,
     bf16* __restrict__ dqkvg, bf16* __restrict__ dctx, float* __restrict__ Dvec, int64_t T, int H,
     int64_t ld, const float* __restrict__ mask, int64_t msb, int64_t msl, float* __restrict__ mbias,
-    int64_t B, int64_t L) {
+    int64_t B, int64_t L, int64_t sb, int64_t sl, const float* __restrict__ lse) {
   // key-mask bias of every (batch, key), [b][l] contiguous, in the log2
   // domain of the softmax: (m - 1) * 1e9 * log2(e)  (src/attention.py:151)
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * L;
@@ -528,6 +528,12 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
     const int c8 = act ? (int)(e % HD8) : 0;
     float dsum = 0.f;
     if (act) {
+      // dO is pre-scaled by this row's 1/rowsum (the backward kernel then
+      // works with the unnormalised P' = exp2(x - m):  dS = P' (dP' - D'),
+      // dV = P'^T dO' -- one multiply per score fewer; fully-masked rows stay
+      // uniform since P' = 1 there and 1/l = 1/L)
+      const int64_t bq = sl == 1 ? t / sb : t % sl, lq = sl == 1 ? t % sb : t / sl;
+      const float rl = lse[2 * ((bq * H + c8 / G) * L + lq) + 1];
       const int64_t c = t * (HD8 * 8) + c8 * 8;
       float dg[8], gv[8], cv[8];
       bf16x8_to_f(*reinterpret_cast<const uint4*>(dgated + c), dg);
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
       uint32_t pc[4], pg[4];
 #pragma unroll
       for (int u = 0; u < 8; u += 2) {
-        const float d0 = dg[u] * gv[u], d1 = dg[u + 1] * gv[u + 1];
+        const float d0 = dg[u] * gv[u] * rl, d1 = dg[u + 1] * gv[u + 1] * rl;
         const float g0 = dg[u] * cv[u] * gv[u] * (1.0f - gv[u]);
         const float g1 = dg[u + 1] * cv[u + 1] * gv[u + 1] * (1.0f - gv[u + 1]);
         const __nv_bfloat162 dq = __floats2bfloat162_rn(d0, d1);
@@ -699,12 +705,12 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
       attn_bwd_prep_tc_kernel<16><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse);
     else
       attn_bwd_prep_tc_kernel<32><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse);
     EVO_LAUNCH_CHECK();
   }
   const bool bias = nb != nullptr && dnb != nullptr;
