@@ -31,23 +31,44 @@ static __global__ void __launch_bounds__(256) finalize_batch_kernel(const __grid
 // cuBLAS handle per (thread, device); a fixed workspace so the handle is
 // usable inside CUDA-graph capture.
 
+// Streams map to one of EVO_STREAM_SLOTS slots; every per-stream scratch
+// (cuBLAS handle + workspace, cuBLASLt workspace, epilogue bias copy) is
+// indexed by slot, so kernels on concurrently running streams (the two branch
+// streams of the engine) never share a workspace.  Slots are assigned on first
+// sight and their buffers allocated when a slot's owner first needs them --
+// before CUDA-graph capture, since the eager warm-up step touches every stream.
+int stream_slot(cudaStream_t s) {
+  static thread_local cudaStream_t seen[EVO_STREAM_SLOTS] = {};
+  static thread_local int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (seen[i] == s) return i;
+  if (n < EVO_STREAM_SLOTS) {
+    seen[n] = s;
+    return n++;
+  }
+  return (int)(((uintptr_t)s >> 4) % EVO_STREAM_SLOTS);
+}
+
 struct BlasState {
   cublasHandle_t h = nullptr;
   void* ws = nullptr;
 };
 
 static cublasHandle_t blas_handle(cudaStream_t s) {
-  static thread_local BlasState st[16];
+  static thread_local BlasState st[16][EVO_STREAM_SLOTS];
   int dev = 0;
   EVO_CUDA(cudaGetDevice(&dev));
-  BlasState& b = st[dev & 15];
-  if (!b.h) {
-    if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasCreate failed");
-    const size_t ws = size_t(32) << 20;
-    EVO_CUDA(cudaMalloc(&b.ws, ws));
-    cublasSetWorkspace(b.h, b.ws, ws);
-    cublasSetMathMode(b.h, CUBLAS_DEFAULT_MATH);  // never TF32
+  if (!st[dev & 15][0].h) {  // every slot at once (no allocation inside graph capture)
+    for (int k = 0; k < EVO_STREAM_SLOTS; ++k) {
+      BlasState& b = st[dev & 15][k];
+      if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasCreate failed");
+      const size_t ws = size_t(32) << 20;
+      EVO_CUDA(cudaMalloc(&b.ws, ws));
+      cublasSetWorkspace(b.h, b.ws, ws);
+      cublasSetMathMode(b.h, CUBLAS_DEFAULT_MATH);  // never TF32
+    }
   }
+  BlasState& b = st[dev & 15][stream_slot(s)];
   cublasSetStream(b.h, s);
   return b.h;
 }

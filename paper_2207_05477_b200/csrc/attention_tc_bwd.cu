@@ -405,9 +405,13 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         tc::tmem_ld16(tl + C_DP + cg * 16, dp);
         if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
         tc::wait_ld();
-        if (last_in_batch && has_next) {  // batch b+1's staging (own copies) has landed
+        if (last_in_batch && has_next) {
+          // batch b+1's staging: each thread waits for its own copies, then a
+          // barrier over the 16 softmax warps makes every thread's copies (the
+          // key-mask row is read by all of them) visible before batch b+1 starts
           cp_async_wait0();
           tc::fence_proxy_async();
+          asm volatile("bar.sync 1, 512;" ::: "memory");
         }
         tc::fence_before();
         tc::mbar_arrive_warp(&bar2[0]);

@@ -20,6 +20,9 @@
 
 namespace evo {
 
+constexpr int EVO_STREAM_SLOTS = 8;
+int stream_slot(cudaStream_t s);  // api.cu
+
 void set_error(const std::string& msg);
 
 struct Error : std::runtime_error {

@@ -37,19 +37,23 @@ struct LtState {
   size_t scratch_bytes = 0;
 };
 
-LtState& lt_state() {
-  static thread_local LtState st[16];
+LtState& lt_state(cudaStream_t stream) {
+  static thread_local LtState st[16][EVO_STREAM_SLOTS];
   int dev = 0;
   EVO_CUDA(cudaGetDevice(&dev));
-  LtState& s = st[dev & 15];
-  if (!s.h) {
-    if (cublasLtCreate(&s.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasLtCreate failed");
-    s.ws_bytes = size_t(32) << 20;
-    EVO_CUDA(cudaMalloc(&s.ws, s.ws_bytes));
-    s.bias16_n = 1 << 16;
-    EVO_CUDA(cudaMalloc(&s.bias16, s.bias16_n * sizeof(__nv_bfloat16)));
+  if (!st[dev & 15][0].h) {
+    // every slot at once: a stream first seen inside CUDA-graph capture (the
+    // capture stream) must not allocate
+    for (int k = 0; k < EVO_STREAM_SLOTS; ++k) {
+      LtState& s = st[dev & 15][k];
+      if (cublasLtCreate(&s.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasLtCreate failed");
+      s.ws_bytes = size_t(32) << 20;
+      EVO_CUDA(cudaMalloc(&s.ws, s.ws_bytes));
+      s.bias16_n = 1 << 16;
+      EVO_CUDA(cudaMalloc(&s.bias16, s.bias16_n * sizeof(__nv_bfloat16)));
+    }
   }
-  return s;
+  return st[dev & 15][stream_slot(stream)];
 }
 
 __global__ void bias_to_bf16_kernel(const float* __restrict__ b, __nv_bfloat16* __restrict__ o, int64_t n) {
@@ -119,7 +123,7 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   // (fused epilogues included: Lt wants a bf16 bias for bf16 outputs, a rounding
   // that is only worth paying where the fused kernel saves a pass over HBM)
   if ((double)M * N * K * batch < (double)(1 << 28)) return false;
-  LtState& st = lt_state();
+  LtState& st = lt_state(s);
   // column-major view: D^T[N, M] = op(B)^T op(A)^T  ->  Lt A := B, Lt B := A
   const cublasOperation_t opA = tb ? CUBLAS_OP_T : CUBLAS_OP_N;
   const cublasOperation_t opB = ta ? CUBLAS_OP_T : CUBLAS_OP_N;

@@ -91,6 +91,11 @@ class BlockEngine:
         self.st = store
         self.dt = act_dtype
         self.var = variants(cfg)
+        # MSA branch on a second stream (EVO_BRANCH_STREAMS=0 disables)
+        import os
+        self.branch_streams = (torch.device(store.device).type == "cuda"
+                               and os.environ.get("EVO_BRANCH_STREAMS", "1") != "0")
+        self._s2 = None
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
         # merged Q|K|V|G projection weights [C, 4*H*c] per attention module (the
@@ -192,7 +197,7 @@ class BlockEngine:
                      nb=nb, pmu=pmu, prs=prs, pair=pair if pair is not None else x)
         return out, saved
 
-    def attn_bwd(self, d, sv, prefix, v: Variant, feats, dpair=None, d_act=None, nxt=None):
+    def attn_bwd(self, d, sv, prefix, v: Variant, feats, dpair=None, d_act=None, nxt=None, late=None):
         """``d`` (fp32 [T, C]) is d(out) on entry and d(x) on exit.  The
         pair-bias gradient is added into ``dpair`` (or ``d`` for triangle
         attention, whose bias comes from its own input).  ``d_act``: bf16 d(out)
@@ -223,13 +228,19 @@ class BlockEngine:
         dxl = torch.empty((T, C), dtype=F32, device=d.device)
         ops.gemm(dqkvg, self.wcat[prefix], dxl, tb=True)
         del dqkvg, dwcat
-        if v.bias:  # before the LN backward, so d is final when that pass reads it
+        if v.bias:
             target = dpair if dpair is not None else d
-            ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
-                              self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
-                              v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
-                              self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
-                              cfg.n_res, H)
+
+            def pair_bias_bwd():
+                ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
+                                  self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
+                                  v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
+                                  self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
+                                  cfg.n_res, H)
+            if dpair is not None and late is not None:
+                late.append(pair_bias_bwd)  # into the pair gradient: run by the caller after its join
+            else:
+                pair_bias_bwd()  # before the LN backward, so d is final when that pass reads it
         return self._ln_bwd_chain(sv["x"], dxl, sv["mu"], sv["rs"], prefix, d, nxt)
 
     # -- transition (src/model.py:344-348) ------------------------------------------
@@ -407,15 +418,16 @@ class BlockEngine:
         msa, s3 = self.trans_fwd(msa, f"{p}.msa_trans")
         return msa, (s1, s2, s3)
 
-    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats):
+    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats, late=None):
         """d_msa: d(msa_out) -> d(msa_in) in place; the pair-bias path adds
-        d(pair_in) into d_pair_acc."""
+        d(pair_in) into d_pair_acc (appended to ``late`` instead when given)."""
         p = f"block{i}"
         s1, s2, s3 = saved
         a = self.trans_bwd(d_msa, s3, f"{p}.msa_trans", nxt=self.G(f"{p}.col_attn.attn.bo"))
         a = self.attn_bwd(d_msa, s2, f"{p}.col_attn", self.var["col_attn"], feats, d_act=a,
                           nxt=self.G(f"{p}.row_attn.attn.bo"))
-        self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc, d_act=a)
+        self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc, d_act=a,
+                      late=late)
 
     def pair_branch_fwd(self, i, pair_mid, feats):
         p = f"block{i}"
@@ -444,19 +456,53 @@ class BlockEngine:
 
     # -- whole block (src/model.py:431-445) -------------------------------------------
 
+    # Branch concurrency on one GPU: given the block inputs, the MSA stack and
+    # the OPM + pair stack are independent (the split Branch Parallelism puts on
+    # two GPUs, src/harness.py:447-486).  On one GPU the MSA branch runs on a
+    # second CUDA stream, forked at the block start and joined at its end, so
+    # its kernels fill the SMs the pair branch's kernels leave idle.  Nothing
+    # allocated on one stream is freed by the host between fork and join.
+
+    def _side_stream(self):
+        if self._s2 is None:
+            self._s2 = torch.cuda.Stream(device=self.st.device)
+        return self._s2
+
     def block_fwd(self, i, msa_in, pair_in, feats):
-        msa, sm = self.msa_branch_fwd(i, msa_in, pair_in, feats)
+        if not self.branch_streams:
+            msa, sm = self.msa_branch_fwd(i, msa_in, pair_in, feats)
+            pair_mid, so = self.opm_fwd(msa_in, f"block{i}.opm", feats, pair_res=pair_in)
+            pair, sp = self.pair_branch_fwd(i, pair_mid, feats)
+            return msa, pair, (sm, so, sp)
+        main, side = torch.cuda.current_stream(), self._side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            msa, sm = self.msa_branch_fwd(i, msa_in, pair_in, feats)
         pair_mid, so = self.opm_fwd(msa_in, f"block{i}.opm", feats, pair_res=pair_in)
         pair, sp = self.pair_branch_fwd(i, pair_mid, feats)
+        main.wait_stream(side)
         return msa, pair, (sm, so, sp)
 
     def block_bwd(self, i, d_msa, d_pair, saved, feats):
         """In place: (d msa_out, d pair_out) -> (d msa_in, d pair_in)."""
         sm, so, sp = saved
-        self.pair_branch_bwd(i, d_pair, sp, feats)            # d_pair = d(pair_mid)
+        if not self.branch_streams:
+            self.pair_branch_bwd(i, d_pair, sp, feats)            # d_pair = d(pair_mid)
+            dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats)
+            self.msa_branch_bwd(i, d_msa, d_pair, sm, feats)      # d_pair += bias path
+            self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)      # d_msa += OPM path
+            return
+        main, side = torch.cuda.current_stream(), self._side_stream()
+        late = []
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.msa_branch_bwd(i, d_msa, d_pair, sm, feats, late=late)
+        self.pair_branch_bwd(i, d_pair, sp, feats)                # d_pair = d(pair_mid)
         dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats)
-        self.msa_branch_bwd(i, d_msa, d_pair, sm, feats)      # d_pair += bias path
-        self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)      # d_msa += OPM path
+        main.wait_stream(side)
+        for fn in late:                                           # d_pair += bias path
+            fn()
+        self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)          # d_msa += OPM path
 
     # -- embedding, recycling, loss (src/model.py:448-478, src/harness.py:313-320) ----
 

@@ -153,3 +153,20 @@ def test_block_with_trimul_matches_oracle(dtype):
     worst = max(errs, key=errs.get)
     assert errs[worst] <= tol_g, (worst, errs[worst])
     assert any("tri_mul" in n and np.abs(grads[n]).max() > 0 for n in grads)
+
+
+def test_bench_shape_step_gradients_finite():
+    """Two Evoformer blocks at the bench shape (N_seq=128, N_res=256, bf16,
+    padded residues): one fwd+bwd gives a finite loss and finite gradients in
+    every parameter slot (the small-shape parity tests cannot reach the
+    many-batches-per-CTA attention paths this exercises)."""
+    import torch
+    from paper_2207_05477_b200.model import ModelConfig
+    from paper_2207_05477_b200.trainer import ExecutionPlan, Trainer
+    cfg = ModelConfig(n_blocks=2, n_seq=128, n_res=256, c_m=256, c_z=128, heads=8, opm_dim=32)
+    tr = Trainer.create(cfg, ExecutionPlan(act_dtype="bf16", fixed_recycles=1))
+    loss, _ = tr.engine.forward_backward(tr.feats, 1)
+    torch.cuda.synchronize()
+    assert np.isfinite(float(loss))
+    bad = [n for n in tr.store.names if not bool(torch.isfinite(tr.store.grad(n)).all())]
+    assert not bad, bad[:5]
