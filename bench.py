@@ -435,7 +435,10 @@ def run_ours(args):
                         "d2h_bytes_per_step": 4},
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu_baseline,
-                "loss_last": losses[-1] if losses else None}
+                "loss_last": losses[-1] if losses else None,
+                "loss_finite": bool(losses) and all(np.isfinite(losses))}
+        if not line["loss_finite"]:
+            print("bench: WARNING non-finite training loss", losses, file=sys.stderr)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
