@@ -276,8 +276,9 @@ class BlockEngine:
 
     # -- outer product mean (src/model.py:351-378) -----------------------------------
 
-    def opm_fwd(self, msa_in, prefix, feats, pair_res=None):
-        """Returns pair_res + OPM(msa_in) (or OPM alone when pair_res is None)."""
+    def opm_fwd(self, msa_in, prefix, feats, pair_res=None, out=None):
+        """Returns pair_res + OPM(msa_in) (or OPM alone when pair_res is None),
+        written into ``out`` when given."""
         cfg, dt = self.cfg, self.dt
         S, R, k = cfg.n_seq, cfg.n_res, cfg.opm_dim
         SR, Cm = msa_in.shape
@@ -292,7 +293,8 @@ class BlockEngine:
         ops.gemm(a.view(S, R * k), c.view(S, R * k), num, ta=True)
         rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt)
         del num
-        out = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
+        if out is None:
+            out = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
         ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res)
         return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
 
@@ -575,11 +577,55 @@ class BlockEngine:
 
     # -- whole model ---------------------------------------------------------------------
 
+    def blocks_fwd(self, msa, pair, feats, saved=None):
+        """All blocks forward; appends each block's saved tensors to ``saved``.
+
+        With branch streams the OPM of block i+1 (which needs only block i's
+        MSA output) is computed on the side stream right after block i's MSA
+        branch, i.e. while the main stream runs block i's pair branch; the main
+        stream then only adds it onto the pair activations (event-ordered).  Its
+        output buffers are allocated on the main stream, which consumes them."""
+        n = self.cfg.n_blocks
+        if not self.branch_streams or n == 0:
+            for i in range(n):
+                msa, pair, sv = self.block_fwd(i, msa, pair, feats)
+                if saved is not None:
+                    saved.append(sv)
+            return msa, pair
+        main, side = torch.cuda.current_stream(), self._side_stream()
+        RR, Cz = pair.shape
+
+        def opm_on_side(i, msa_i):
+            y = torch.empty((RR, Cz), dtype=self.dt, device=pair.device)  # main-stream allocation
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(side):
+                _, so = self.opm_fwd(msa_i, f"block{i}.opm", feats, pair_res=None, out=y)
+                ev.record(side)
+            return y, so, ev
+
+        side.wait_stream(main)
+        nxt = opm_on_side(0, msa)
+        for i in range(n):
+            y, so, ev = nxt
+            side.wait_stream(main)                   # pair (row-attention bias) is final
+            with torch.cuda.stream(side):
+                msa_new, sm = self.msa_branch_fwd(i, msa, pair, feats)
+            if i + 1 < n:
+                nxt = opm_on_side(i + 1, msa_new)
+            main.wait_event(ev)                      # OPM(block i) done on the side stream
+            pair_mid = torch.empty_like(pair)
+            ops.bias_residual(pair, y, None, pair_mid)
+            del y
+            pair, sp = self.pair_branch_fwd(i, pair_mid, feats)
+            msa = msa_new
+            if saved is not None:
+                saved.append((sm, so, sp))
+        main.wait_stream(side)
+        return msa, pair
+
     def forward_only(self, feats, prev=None):
         msa, pair, _ = self.embed_fwd(feats, prev)
-        for i in range(self.cfg.n_blocks):
-            msa, pair, _ = self.block_fwd(i, msa, pair, feats)
-        return msa, pair
+        return self.blocks_fwd(msa, pair, feats)
 
     def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1):
         """``_serial_grads`` (src/harness.py:327-352): n-1 untaped recycling
@@ -592,9 +638,7 @@ class BlockEngine:
             prev = self.forward_only(feats, prev)
         msa, pair, rec = self.embed_fwd(feats, prev)
         saved = []
-        for i in range(self.cfg.n_blocks):
-            msa, pair, sv = self.block_fwd(i, msa, pair, feats)
-            saved.append(sv)
+        msa, pair = self.blocks_fwd(msa, pair, feats, saved)
         loss, d_msa, d_pair = self.loss(msa, pair)
         for i in reversed(range(self.cfg.n_blocks)):
             with self.deferred():
