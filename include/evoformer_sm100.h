@@ -79,11 +79,12 @@ int evo_gemm(int64_t M, int64_t N, int64_t K,
  * matmul + bias + relu of src/model.py:346):
  *   out[M,N] = op(A) . op(B) + bias[N] (+ res[M,N])      relu == 0
  *   out[M,N] = relu(op(A) . op(B) + bias[N])              relu == 1, res == NULL
- * res may alias nothing else; res_dtype is its storage dtype. */
+ * res may alias nothing else; res_dtype is its storage dtype.  bias_bf16 (nullable):
+ * a bf16 copy of bias (the parameter store's shadow) used by bf16 fused epilogues. */
 int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
                   const void* B, int64_t ldb, int trans_b, const void* res, int res_dtype,
-                  const float* bias, int relu, void* out, int64_t ldo, int ab_dtype, int c_dtype,
-                  void* stream);
+                  const float* bias, const void* bias_bf16, int relu, void* out, int64_t ldo,
+                  int ab_dtype, int c_dtype, void* stream);
 
 /* Projection with a training epilogue, for the transition's ReLU and the
  * bias gradients (replaces the np.maximum / np.sum steps of src/model.py:346

@@ -35,8 +35,8 @@ SIGNATURES = {
                       _i, _f, _f, _i, _i, _p]),
     "evo_gemm_epilogue": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _i64, _f, _i, _p, _p, _i64,
                                _i, _i, _p]),
-    "evo_gemm_bias": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _i, _p, _i, _p, _i64, _i, _i,
-                           _p]),
+    "evo_gemm_bias": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _i, _p, _p, _i, _p, _i64, _i,
+                           _i, _p]),
     "evo_layernorm_fwd": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i64, _i64, _f, _p]),
     "evo_layernorm_bwd_workspace": (_i64, [_i64, _i64]),
     "evo_layernorm_bwd": (_i, [_p, _i, _p, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _i64, _i64, _p]),

@@ -93,7 +93,7 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
 bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
              float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s,
-             void* aux = nullptr, int64_t aux_ld = 0);
+             void* aux = nullptr, int64_t aux_ld = 0, const void* bias16 = nullptr);
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
                  int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
@@ -297,8 +297,9 @@ int evo_gemm_epilogue(int64_t M, int64_t N, int64_t K, const void* A, int64_t ld
 }
 
 int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
-                  int64_t ldb, int trans_b, const void* res, int res_dtype, const float* bias, int relu,
-                  void* out, int64_t ldo, int ab_dtype, int c_dtype, void* stream) {
+                  int64_t ldb, int trans_b, const void* res, int res_dtype, const float* bias,
+                  const void* bias_bf16, int relu, void* out, int64_t ldo, int ab_dtype, int c_dtype,
+                  void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0, EVO_ERR_ARG, "gemm_bias: bad extents");
   EVO_REQUIRE(!(relu && res), EVO_ERR_ARG, "gemm_bias: relu with a residual is not a module of the path");
@@ -306,7 +307,7 @@ int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
   cudaStream_t s = (cudaStream_t)stream;
   const bool fuse_res = res != nullptr && res_dtype == c_dtype;
   if (gemm_lt(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, fuse_res ? res : out, out, ldo, 0, 1, 1.0f,
-              fuse_res ? 1.0f : 0.0f, ab_dtype, c_dtype, relu ? 2 : 1, bias, s)) {
+              fuse_res ? 1.0f : 0.0f, ab_dtype, c_dtype, relu ? 2 : 1, bias, s, nullptr, 0, bias_bf16)) {
     if (res && !fuse_res) {  // residual of another dtype: add it after the fused bias
       EVO_REQUIRE(ldo == N, EVO_ERR_ARG, "gemm_bias: strided output with a mixed-dtype residual");
       static float* zero = nullptr;

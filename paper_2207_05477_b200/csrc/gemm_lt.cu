@@ -116,7 +116,7 @@ namespace {
 bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
              float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s,
-             void* aux, int64_t aux_ld) {
+             void* aux, int64_t aux_ld, const void* bias16) {
   if (env_off()) return false;
   // small problems are launch-bound: keep them on the default cuBLAS path
   // (no timing-dependent algorithm choice where it cannot pay)
@@ -154,7 +154,9 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   } else if (epi) {
     // the bias must have the output's dtype: bf16 outputs get a bf16 copy
     const void* bptr = bias;
-    if (c_dtype == EVO_BF16) {
+    if (c_dtype == EVO_BF16 && bias16) {
+      bptr = bias16;  // the caller's bf16 copy (the parameter store's shadow)
+    } else if (c_dtype == EVO_BF16) {
       if (N > st.bias16_n) return false;
       bias_to_bf16_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(bias, st.bias16, N);
       EVO_LAUNCH_CHECK();

@@ -192,7 +192,8 @@ class BlockEngine:
         ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, v.msb, v.msl, nb,
                                              self.P(f"{prefix}.attn.bg"), v.B, v.L, H, D, v.sb, v.sl)
         out = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.gemm_bias(gated, self.W(f"{prefix}.attn.wo", HD), out, self.P(f"{prefix}.attn.bo"), res=x)
+        ops.gemm_bias(gated, self.W(f"{prefix}.attn.wo", HD), out, self.P(f"{prefix}.attn.bo"), res=x,
+                      bias16=self.st.weight(f"{prefix}.attn.bo"))
         saved = dict(x=x, xl=xl, mu=mu, rs=rs, qkvg=qkvg, ctx=ctx, gate=gate, gated=gated, lse=lse,
                      nb=nb, pmu=pmu, prs=prs, pair=pair if pair is not None else x)
         return out, saved
@@ -251,9 +252,10 @@ class BlockEngine:
         xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
         w1 = self.W(f"{prefix}.w1", C)
         h = torch.empty((T, w1.shape[1]), dtype=dt, device=x.device)
-        ops.gemm_bias(xl, w1, h, self.P(f"{prefix}.b1"), relu=True)
+        ops.gemm_bias(xl, w1, h, self.P(f"{prefix}.b1"), relu=True, bias16=self.st.weight(f"{prefix}.b1"))
         out = torch.empty((T, C), dtype=dt, device=x.device)
-        ops.gemm_bias(h, self.W(f"{prefix}.w2", w1.shape[1]), out, self.P(f"{prefix}.b2"), res=x)
+        ops.gemm_bias(h, self.W(f"{prefix}.w2", w1.shape[1]), out, self.P(f"{prefix}.b2"), res=x,
+                      bias16=self.st.weight(f"{prefix}.b2"))
         return out, dict(x=x, xl=xl, mu=mu, rs=rs, h=h)
 
     def trans_bwd(self, d, sv, prefix, nxt=None):
@@ -295,7 +297,8 @@ class BlockEngine:
         del num
         if out is None:
             out = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
-        ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res)
+        ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res,
+                      bias16=self.st.weight(f"{prefix}.b_out"))
         return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
 
     def opm_bwd_core(self, d, sv, prefix, feats):

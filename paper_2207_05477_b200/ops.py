@@ -69,7 +69,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, ta: bool = False, tb
 
 
 def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.Tensor,
-              res: torch.Tensor | None = None, relu: bool = False, ta: bool = False, tb: bool = False):
+              res: torch.Tensor | None = None, relu: bool = False, ta: bool = False, tb: bool = False,
+              bias16: torch.Tensor | None = None):
     """out = op(a) @ op(b) + bias (+ res), or relu(op(a) @ op(b) + bias): the
     projection with its module epilogue fused (one kernel on the Lt path)."""
     for t in (a, b, out):
@@ -81,9 +82,11 @@ def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.T
         raise ValueError(f"gemm_bias shape mismatch: op(a)={M}x{K} op(b)={Kb}x{N} out={tuple(out.shape)}")
     if res is not None and (tuple(res.shape) != (M, N) or not res.is_contiguous() or not out.is_contiguous()):
         raise ValueError("gemm_bias: residual must be a contiguous [M, N] like out")
+    if bias16 is not None and bias16.dtype != torch.bfloat16:
+        bias16 = None
     call("evo_gemm_bias", M, N, K, ptr(a), a.stride(0), int(ta), ptr(b), b.stride(0), int(tb), ptr(res),
-         dcode(res) if res is not None else F32, ptr(bias), int(relu), ptr(out), out.stride(0), dcode(a),
-         dcode(out), stream())
+         dcode(res) if res is not None else F32, ptr(bias), ptr(bias16), int(relu), ptr(out), out.stride(0),
+         dcode(a), dcode(out), stream())
     return out
 
 
