@@ -98,6 +98,8 @@ class BlockEngine:
         self._s2 = None
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
+        # two arenas for the block-pipelined backward (blocks_bwd), alternating by block
+        self.arenas = (self.arena, torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device))
         # merged Q|K|V|G projection weights [C, 4*H*c] per attention module (the
         # reference concatenates Wq|Wk|Wv the same way, src/attention.py:133-141),
         # refreshed from the (bf16 shadow of the) pooled params every step
@@ -301,24 +303,27 @@ class BlockEngine:
                       bias16=self.st.weight(f"{prefix}.b_out"))
         return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
 
-    def opm_bwd_core(self, d, sv, prefix, feats):
+    def opm_bwd_core(self, d, sv, prefix, feats, d_act=None):
         """d(pair_mid) (fp32) -> dxl (fp32 [S*R, c_m]); the LayerNorm backward is
-        applied later by opm_ln_bwd so it can accumulate into d(msa_in)."""
+        applied later by opm_ln_bwd so it can accumulate into d(msa_in).  With
+        ``d_act`` (bf16 d(pair_mid), b_out gradient already taken) ``d`` is not read."""
         cfg, dt = self.cfg, self.dt
         S, R, k = cfg.n_seq, cfg.n_res, cfg.opm_dim
-        RR, Cz = d.shape
+        RR, Cz = (d if d is not None else d_act).shape
         SR, Cm = sv["x"].shape
-        d_act = torch.empty((RR, Cz), dtype=dt, device=d.device)
-        ops.colsum_cast(d, self.G(f"{prefix}.b_out"), y=d_act)
+        dev = sv["x"].device
+        if d_act is None:
+            d_act = torch.empty((RR, Cz), dtype=dt, device=dev)
+            ops.colsum_cast(d, self.G(f"{prefix}.b_out"), y=d_act)
         ops.gemm(sv["outn"], d_act, self.Gm(f"{prefix}.w_out", k * k), ta=True)
-        doutn = torch.empty((RR, k * k), dtype=dt, device=d.device)
+        doutn = torch.empty((RR, k * k), dtype=dt, device=dev)
         ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
         del d_act
         dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt)
         del doutn
         a2, c2 = sv["a"].view(S, R * k), sv["c"].view(S, R * k)
-        da = torch.empty((S, R * k), dtype=dt, device=d.device)
-        dc = torch.empty((S, R * k), dtype=dt, device=d.device)
+        da = torch.empty((S, R * k), dtype=dt, device=dev)
+        dc = torch.empty((S, R * k), dtype=dt, device=dev)
         ops.gemm(c2, dnum, da, tb=True)
         ops.gemm(a2, dnum, dc)
         del dnum
@@ -327,7 +332,7 @@ class BlockEngine:
         xl = sv["xl"]
         ops.gemm(xl, d_ab[:, :k], self.Gm(f"{prefix}.w_left", Cm), ta=True)
         ops.gemm(xl, d_ab[:, k:], self.Gm(f"{prefix}.w_right", Cm), ta=True)
-        dxl = torch.empty((SR, Cm), dtype=F32, device=d.device)
+        dxl = torch.empty((SR, Cm), dtype=F32, device=dev)
         ops.gemm(d_ab[:, :k], self.W(f"{prefix}.w_left", Cm), dxl, tb=True)
         ops.gemm(d_ab[:, k:], self.W(f"{prefix}.w_right", Cm), dxl, tb=True, beta=1.0)
         return dxl
@@ -626,6 +631,53 @@ class BlockEngine:
         main.wait_stream(side)
         return msa, pair
 
+    def blocks_bwd(self, d_msa, d_pair, saved, feats):
+        """All blocks backward, in place on (d_msa, d_pair); frees ``saved``.
+
+        With branch streams the MSA branch runs on the side stream as in
+        ``block_bwd``, and the OPM backward of block i -- which needs only a bf16
+        copy of d(pair_mid) -- also moves to the side stream, where it overlaps
+        the main stream's pair-branch backward of block i-1.  The per-block
+        deferred reductions then alternate between two arenas and are finalised
+        on the side stream once both streams' kernels of the block are done."""
+        n = self.cfg.n_blocks
+        if not self.branch_streams:
+            for i in reversed(range(n)):
+                with self.deferred():
+                    self.block_bwd(i, d_msa, d_pair, saved[i], feats)
+                saved[i] = None
+            return
+        main, side = torch.cuda.current_stream(), self._side_stream()
+        keep = []  # main-stream tensors read by the side stream: alive until the final join
+        side.wait_stream(main)
+        for i in reversed(range(n)):
+            sm, so, sp = saved[i]
+            ops.defer_begin(self.arenas[i % 2])
+            late = []
+            with torch.cuda.stream(side):
+                self.msa_branch_bwd(i, d_msa, d_pair, sm, feats, late=late)
+                ev_msa = torch.cuda.Event()
+                ev_msa.record(side)
+            self.pair_branch_bwd(i, d_pair, sp, feats)          # d_pair = d(pair_mid)
+            d_act = torch.empty(d_pair.shape, dtype=self.dt, device=d_pair.device)
+            ops.colsum_cast(d_pair, self.G(f"block{i}.opm.b_out"), y=d_act)
+            ev_pair = torch.cuda.Event()
+            ev_pair.record(main)
+            main.wait_event(ev_msa)
+            for fn in late:                                     # d_pair += bias path
+                fn()
+            with torch.cuda.stream(side):
+                side.wait_event(ev_pair)
+                dxl = self.opm_bwd_core(None, so, f"block{i}.opm", feats, d_act=d_act)
+                self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)  # d_msa += OPM path
+                del dxl
+                side.wait_stream(main)                          # every partial of block i written
+                ops.defer_end(side)
+            keep.append(d_act)
+            saved[i] = None
+        main.wait_stream(side)
+        keep.clear()
+
     def forward_only(self, feats, prev=None):
         msa, pair, _ = self.embed_fwd(feats, prev)
         return self.blocks_fwd(msa, pair, feats)
@@ -643,10 +695,7 @@ class BlockEngine:
         saved = []
         msa, pair = self.blocks_fwd(msa, pair, feats, saved)
         loss, d_msa, d_pair = self.loss(msa, pair)
-        for i in reversed(range(self.cfg.n_blocks)):
-            with self.deferred():
-                self.block_bwd(i, d_msa, d_pair, saved[i], feats)
-            saved[i] = None
+        self.blocks_bwd(d_msa, d_pair, saved, feats)
         with self.deferred():
             self.embed_bwd(d_msa, d_pair, feats, rec)
         return loss, (msa, pair)

@@ -31,6 +31,14 @@ def _ws(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
 
 
+def defer_begin(arena: torch.Tensor):
+    call("evo_defer_begin", ptr(arena), arena.numel() * arena.element_size())
+
+
+def defer_end(stream_obj=None):
+    call("evo_defer_end", stream_obj.cuda_stream if stream_obj is not None else stream())
+
+
 class deferred_reductions:
     """Context manager: batch the finalisation of every column reduction
     issued inside into one launch at exit (evo_defer_begin / evo_defer_end)."""
