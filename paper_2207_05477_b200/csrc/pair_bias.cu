@@ -9,6 +9,7 @@
 // w_bias / LN-affine gradient partials in one pass over the pair.
 #include "common.cuh"
 #include "vec.cuh"
+#include "tc_common.cuh"
 #include <type_traits>
 #include "reduce.cuh"
 
@@ -176,12 +177,36 @@ __device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
 }
 
 template <int C, typename T>
+struct PbTile {
+  static constexpr int ROWB = C * (int)sizeof(T) + 16;  // padded row: 16-B chunk index 17t+k spreads banks
+  static constexpr int CPR = C * (int)sizeof(T) / 16;   // 16-B chunks per row
+  static constexpr int bytes = 128 * ROWB;
+};
+
+// A block owns 128 consecutive output positions: their token rows are staged
+// into shared memory with coalesced 16-B cp.async (CPR threads per row), then
+// each thread reduces and projects one row from the padded tile.
+template <int C, typename T>
 __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
     const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
     float* __restrict__ rstd, int64_t R, int H, int swap) {
+  using TL = PbTile<C, T>;
+  extern __shared__ __align__(16) uint8_t tile[];
   __shared__ float4 sw[C][2];   // w[c, 0..7] (zero beyond H)
   __shared__ float2 sgb[C];     // (gamma, beta)
+  const int64_t RR = R * R;
+  const int64_t i0 = blockIdx.x * (int64_t)128;
+  // stage: chunk k of row r by thread (r * CPR + k) % 128
+  for (int e = threadIdx.x; e < 128 * TL::CPR; e += 128) {
+    const int r = e / TL::CPR, k = e % TL::CPR;
+    const int64_t i = i0 + r;
+    if (i < RR) {
+      const int64_t tok = swap ? (i % R) * R + i / R : i;
+      tc::cp_async16(tile + r * TL::ROWB + k * 16, reinterpret_cast<const uint8_t*>(z + tok * C) + k * 16);
+    }
+  }
+  tc::cp_async_commit();
   for (int e = threadIdx.x; e < C; e += blockDim.x) {
     float t[8];
 #pragma unroll
@@ -190,79 +215,66 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
     sw[e][1] = make_float4(t[4], t[5], t[6], t[7]);
     sgb[e] = make_float2(g[e], b[e]);
   }
+  tc::cp_async_wait0();
   __syncthreads();
-  const int64_t RR = R * R;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < RR; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tok = swap ? (i % R) * R + i / R : i;
-    const T* row = z + tok * C;
-    constexpr bool IN_REGS = C * sizeof(T) <= 256;  // whole row in registers: every load in flight at once
-    constexpr int NV = IN_REGS ? C / 8 : 1;
-    Vec8<T> rv[NV];
-    if constexpr (IN_REGS) {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) ldv8(row + 8 * k, rv[k]);
+  const int64_t i = i0 + threadIdx.x;
+  if (i >= RR) return;
+  const int64_t tok = swap ? (i % R) * R + i / R : i;
+  const uint8_t* row = tile + threadIdx.x * TL::ROWB;
+  auto chunk = [&](int c, float (&f)[8]) {
+    Vec8<T> v;
+    if constexpr (sizeof(T) == 2) {
+      v.u = *reinterpret_cast<const uint4*>(row + c * 2);
+    } else {
+      v.a = *reinterpret_cast<const float4*>(row + c * 4);
+      v.b = *reinterpret_cast<const float4*>(row + c * 4 + 16);
     }
-    auto chunk = [&](int c, float (&f)[8]) {
-      if constexpr (IN_REGS) {
-        cvt8(rv[c / 8], f);
-      } else {
-        Vec8<T> v;
-        ldv8(row + c, v);
-        cvt8(v, f);
-      }
-    };
-    float s = 0.f;
+    cvt8(v, f);
+  };
+  float s = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < C; c += 8) {
+    float f[8];
+    chunk(c, f);
 #pragma unroll
-    for (int c = 0; c < C; c += 8) {
-      float f[8];
-      chunk(c, f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s += f[e];
-    }
-    const float mu = s / (float)C;
-    float q = 0.f;
-#pragma unroll
-    for (int c = 0; c < C; c += 8) {
-      float f[8];
-      chunk(c, f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float d = f[e] - mu;
-        q += d * d;
-      }
-    }
-    const float inv = rsqrtf(q / (float)C + 1e-5f);
-    float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-    for (int c = 0; c < C; c += 8) {
-      float f[8];
-      chunk(c, f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        // volatile shared loads: keeps the compiler from hoisting all C x 10
-        // broadcast weights into registers (the row already holds C/2 of them)
-        float2 gb;
-        float4 w0, w1;
-        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(gb.x), "=f"(gb.y) : "r"(tc_smem_u32(&sgb[c + e])));
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w0.x), "=f"(w0.y), "=f"(w0.z), "=f"(w0.w)
-                     : "r"(tc_smem_u32(&sw[c + e][0])));
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(w1.x), "=f"(w1.y), "=f"(w1.z), "=f"(w1.w)
-                     : "r"(tc_smem_u32(&sw[c + e][1])));
-        const float zl = (f[e] - mu) * inv * gb.x + gb.y;
-        const float2 z2 = make_float2(zl, zl);
-        p[0] = __ffma2_rn(z2, make_float2(w0.x, w0.y), p[0]);
-        p[1] = __ffma2_rn(z2, make_float2(w0.z, w0.w), p[1]);
-        p[2] = __ffma2_rn(z2, make_float2(w1.x, w1.y), p[2]);
-        p[3] = __ffma2_rn(z2, make_float2(w1.z, w1.w), p[3]);
-      }
-    }
-    const float ph[8] = {p[0].x, p[0].y, p[1].x, p[1].y, p[2].x, p[2].y, p[3].x, p[3].y};
-#pragma unroll
-    for (int hh = 0; hh < 8; ++hh)
-      if (hh < H) nb[hh * RR + i] = from_f<T>(ph[hh]);
-    mean[tok] = mu;
-    rstd[tok] = inv;
+    for (int e = 0; e < 8; ++e) s += f[e];
   }
+  const float mu = s / (float)C;
+  float q = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < C; c += 8) {
+    float f[8];
+    chunk(c, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = f[e] - mu;
+      q += d * d;
+    }
+  }
+  const float inv = rsqrtf(q / (float)C + 1e-5f);
+  float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll 1
+  for (int c = 0; c < C; c += 8) {
+    float f[8];
+    chunk(c, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 gb = sgb[c + e];
+      const float4 w0 = sw[c + e][0], w1 = sw[c + e][1];
+      const float zl = (f[e] - mu) * inv * gb.x + gb.y;
+      const float2 z2 = make_float2(zl, zl);
+      p[0] = __ffma2_rn(z2, make_float2(w0.x, w0.y), p[0]);
+      p[1] = __ffma2_rn(z2, make_float2(w0.z, w0.w), p[1]);
+      p[2] = __ffma2_rn(z2, make_float2(w1.x, w1.y), p[2]);
+      p[3] = __ffma2_rn(z2, make_float2(w1.z, w1.w), p[3]);
+    }
+  }
+  const float ph[8] = {p[0].x, p[0].y, p[1].x, p[1].y, p[2].x, p[2].y, p[3].x, p[3].y};
+#pragma unroll
+  for (int hh = 0; hh < 8; ++hh)
+    if (hh < H) nb[hh * RR + i] = from_f<T>(ph[hh]);
+  mean[tok] = mu;
+  rstd[tok] = inv;
 }
 
 bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
@@ -274,8 +286,14 @@ bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, co
   auto go = [&](auto cc) {
     constexpr int CC = decltype(cc)::value;
     EVO_DISPATCH_T(dt, T, {
-      pair_bias_fwd_tpt_kernel<CC, T><<<grid, 128, 0, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd, R,
-                                                           (int)H, swap);
+      auto k = pair_bias_fwd_tpt_kernel<CC, T>;
+      constexpr int SMEM = PbTile<CC, T>::bytes;
+      static bool attr = false;
+      if (!attr) {
+        EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        attr = true;
+      }
+      k<<<grid, 128, SMEM, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd, R, (int)H, swap);
     });
   };
   if (C == 32) go(std::integral_constant<int, 32>{});
