@@ -435,7 +435,11 @@ bool attn_fwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
                      void* ctx, void* gate, void* gated, float* lse, const AttnGeom& g, int dtype,
                      cudaStream_t s) {
   if (fwd_tc_disabled() || dtype != EVO_BF16) return false;
-  if (!(g.D == 16 || g.D == 32) || g.L > 256 || g.L < 1) return false;
+  // same L range as the tcgen05 backward (attention_tc_bwd.cu): a problem's
+  // forward and backward must form the logits with the same operation order,
+  // or a fully-masked row's recomputed logits could round one ulp (128 at the
+  // -1e9 mask) away from the saved row max
+  if (!(g.D == 16 || g.D == 32) || g.L > 256 || g.L < 65) return false;
   if ((g.ld % 8) != 0 || (((uintptr_t)qkvg) & 15) != 0) return false;
   if (((uintptr_t)ctx | (uintptr_t)gate | (uintptr_t)gated) & 15) return false;
   const bool bias = nb != nullptr;
