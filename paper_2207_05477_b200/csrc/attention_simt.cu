@@ -24,6 +24,7 @@ namespace evo {
 constexpr int SIMT_QT = 64;  // query rows (threads) per CTA
 constexpr int SIMT_KC = 32;  // keys per shared-memory chunk
 constexpr float LOG2E = 1.4426950408889634f;
+constexpr float MASK_BIAS_L2 = 1.4426950408889634e9f;  // = tc::MASK_BIAS_L2 (tc_common.cuh)
 
 
 template <typename T, int DM>
@@ -60,7 +61,8 @@ __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(
       Vs[jj][k] = vv;
     }
     for (int jj = threadIdx.x; jj < SIMT_KC; jj += SIMT_QT)
-      Mb[jj] = jj < nk ? (mask[b * g.msb + (j0 + jj) * g.msl] - 1.0f) * 1e9f : 0.f;
+      Mb[jj] = jj < nk ? (mask[b * g.msb + (j0 + jj) * g.msl] - 1.0f) * (sizeof(T) == 2 ? MASK_BIAS_L2 : 1e9f)
+                       : 0.f;
     __syncthreads();
     if (!active) continue;
     float s[SIMT_KC];
@@ -71,10 +73,18 @@ __global__ void __launch_bounds__(SIMT_QT) attn_fwd_simt_kernel(
         float d = 0.f;
 #pragma unroll
         for (int k = 0; k < DM; ++k) d = fmaf(q[k], Ks[jj][k], d);
-        float v = __fmul_rn(d, scale);
-        v = v + Mb[jj];
-        if (nb) v = v + to_f(nb[(h * g.L + i) * g.L + j0 + jj]);
-        v = __fmul_rn(v, LOG2E);  // softmax in the log2 domain (shared with the tcgen05 path)
+        const float nbv = nb ? to_f(nb[(h * g.L + i) * g.L + j0 + jj]) : 0.f;
+        float v;
+        if constexpr (sizeof(T) == 2) {
+          // bf16: the fused order of the tcgen05 kernels, (s c + nb) log2e + mask bias, so
+          // a problem's forward and backward form the same logits whichever path runs them
+          v = fmaf(fmaf(d, scale, nbv), LOG2E, Mb[jj]);  // Mb already (m - 1) 1e9 log2e
+        } else {
+          v = __fmul_rn(d, scale);  // fp32 parity path: the reference's order (src/attention.py:151-156)
+          v = v + Mb[jj];
+          if (nb) v = v + nbv;
+          v = __fmul_rn(v, LOG2E);  // softmax in the log2 domain
+        }
         s[jj] = v;
         cmax = fmaxf(cmax, v);
       } else {
@@ -184,7 +194,8 @@ __global__ void __launch_bounds__(SIMT_QT) attn_bwd_rows_kernel(
       Vs[jj][k] = vv;
     }
     for (int jj = threadIdx.x; jj < SIMT_KC; jj += SIMT_QT)
-      Mb[jj] = jj < nk ? (mask[b * g.msb + (j0 + jj) * g.msl] - 1.0f) * 1e9f : 0.f;
+      Mb[jj] = jj < nk ? (mask[b * g.msb + (j0 + jj) * g.msl] - 1.0f) * (sizeof(T) == 2 ? MASK_BIAS_L2 : 1e9f)
+                       : 0.f;
     __syncthreads();
     if (!active) continue;
     for (int jj = 0; jj < nk; ++jj) {
@@ -194,10 +205,19 @@ __global__ void __launch_bounds__(SIMT_QT) attn_bwd_rows_kernel(
         d = fmaf(q[k], Ks[jj][k], d);
         dp = fmaf(dc[k], Vs[jj][k], dp);
       }
-      float s = __fmul_rn(d, scale);
-      s = s + Mb[jj];
-      if (nb) s = s + to_f(nb[(h * g.L + i) * g.L + j0 + jj]);
-      float p = exp2f(__fmul_rn(s, LOG2E) - ls) * rl;
+      const float nbv = nb ? to_f(nb[(h * g.L + i) * g.L + j0 + jj]) : 0.f;
+      float p;
+      if constexpr (sizeof(T) == 2) {
+        // fused order (see the forward); x - m is clamped at 0: the saved row max may
+        // come from the tcgen05 forward, whose MMA sums the dot products in another order
+        const float x = fmaf(fmaf(d, scale, nbv), LOG2E, Mb[jj]);
+        p = exp2f(fminf(x - ls, 0.f)) * rl;
+      } else {
+        float s = __fmul_rn(d, scale);
+        s = s + Mb[jj];
+        if (nb) s = s + nbv;
+        p = exp2f(__fmul_rn(s, LOG2E) - ls) * rl;
+      }
       float ds = p * (dp - Dv);
       const int64_t o = (bh * g.L + j0 + jj) * g.L + i;
       Pt[o] = p;
@@ -308,11 +328,17 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
                      float* dnb, float* dbg, int accumulate, void* ws, size_t ws_bytes,
                      const AttnGeom& g, int dtype, cudaStream_t s);
 int64_t attn_bwd_tc_workspace(const AttnGeom& g, int dtype);
+bool attn_fwd_tc_kb_try(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
+                        void* gate, void* gated, float* lse, const AttnGeom& g, int dtype, cudaStream_t s);
 
 static AttnGeom make_geom(int64_t B, int64_t L, int64_t H, int64_t D, int64_t sb, int64_t sl,
                           int64_t ld, int64_t msb, int64_t msl) {
   EVO_REQUIRE(B > 0 && L > 0 && H > 0 && D > 0, EVO_ERR_ARG, "attention: non-positive extent");
   EVO_REQUIRE(ld >= 4 * H * D, EVO_ERR_ARG, "attention: ld_qkvg < 4*H*D");
+  // the (batch, position) -> token-row map must cover rows 0..B*L-1 exactly (row-major
+  // [B, L] or its transpose): the kernels' per-token workspaces are indexed by token row
+  EVO_REQUIRE((sb == L && sl == 1) || (sb == 1 && sl == B), EVO_ERR_ARG,
+              "attention: token strides must map (b, l) onto rows 0..B*L-1 (sb=L,sl=1 or sb=1,sl=B)");
   AttnGeom g{B, L, H, D, sb, sl, ld, msb, msl};
   return g;
 }
@@ -338,6 +364,7 @@ int evo_attn_fwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t m
   AttnGeom g = make_geom(B, L, H, D, tok_sb, tok_sl, ld_qkvg, mask_sb, mask_sl);
   cudaStream_t s = (cudaStream_t)stream;
   if (attn_fwd_tc_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
+  if (attn_fwd_tc_kb_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
   const float scale = (float)(1.0 / sqrt((double)D));
   dim3 grid(cdiv(L, SIMT_QT), (unsigned)H, (unsigned)B);
   ATTN_DM_DISPATCH(D, DM, EVO_DISPATCH_T(dtype, T, {

@@ -342,3 +342,47 @@ def test_attention_bench_geometry_padded_mask(geom):
     if n32 is not None:
         assert torch.isfinite(n16).all()
         assert rel(n16, n32) <= 3e-2
+
+
+@pytest.mark.parametrize("name,S,R,H,D,geom", [("F_row", 512, 384, 8, 32, "row"), ("F_col", 512, 384, 8, 32, "col"),
+                                                ("F_tri_end", 8, 384, 8, 16, "tri_end"),
+                                                ("X_tri", 8, 1024, 4, 32, "tri_start")])
+@pytest.mark.timeout(600)
+def test_attention_long_rows_vs_fp32(name, S, R, H, D, geom):
+    """L > 256 (fine-tune shape F, stress shape X): the key-blocked tcgen05
+    forward against the fp32 path on the same inputs (padded masks, fully-masked
+    batches included); for F also the backward (bf16 SIMT, fused logit order)."""
+    from paper_2207_05477_b200 import ops
+    B, L, sb, sl, msb, msl = GEOMS[geom](S, R)
+    T = S * R if geom in ("row", "col") else R * R
+    torch.manual_seed(5)
+    q32 = torch.randn(T, 4 * H * D, device="cuda") * 0.5
+    mask = torch.ones(T, device="cuda")
+    nv = R - R // 10
+    mv = mask.view(S, R) if geom in ("row", "col") else mask.view(R, R)
+    mv[:, nv:] = 0.0
+    if geom.startswith("tri"):
+        mv[nv:, :] = 0.0
+        mv[:3, :] = 0.0  # more fully-masked rows / masked keys
+    bias32 = torch.randn(H, L, L, device="cuda") * 0.1 if geom != "col" else None
+    bg = torch.randn(H * D, device="cuda") * 0.1
+    dg32 = torch.randn(T, H * D, device="cuda")
+    out = {}
+    for dt in (torch.float32, torch.bfloat16):
+        q = q32.to(dt)
+        bias = bias32.to(dt) if bias32 is not None else None
+        ctx, gate, gated, lse = ops.attn_fwd(q, mask, msb, msl, bias, bg, B, L, H, D, sb, sl)
+        dq = None
+        if name.startswith("F"):
+            dbg = torch.empty(H * D, device="cuda")
+            dq, _ = ops.attn_bwd(q, mask, msb, msl, bias, ctx, gate, dg32.to(dt), lse, dbg, B, L, H, D, sb, sl,
+                                 want_dbias=bias is not None)
+            dq = dq.float()
+        out[dt] = (ctx.float(), dq)
+    c32, d32 = out[torch.float32]
+    c16, d16 = out[torch.bfloat16]
+    assert torch.isfinite(c16).all()
+    assert rel(c16, c32) <= 2e-2
+    if d16 is not None:
+        assert torch.isfinite(d16).all()
+        assert rel(d16, d32) <= 3e-2
