@@ -79,20 +79,20 @@ __device__ __forceinline__ int bias_off(int r, int c) {
 
 // the CTA's bias rows nb[h, q0 + r, :] -> smem [128][LP] (zero padded)
 template <int LP>
-__device__ __forceinline__ void stage_bias_tile(uint8_t* sB, const bf16* nb, int64_t h, int q0, int L,
+__device__ __forceinline__ void stage_bias_tile(uint8_t* sB, const bf16* nb, int64_t h, int q0, int k0, int L,
                                                 int tid, int nthreads) {
   constexpr int CPR = LP / 8;
   const bool vec_ok = (L % 8) == 0;
   for (int e = tid; e < 128 * CPR; e += nthreads) {
     const int r = e / CPR, c = e % CPR;
     bf16* dst = reinterpret_cast<bf16*>(sB + bias_off<LP>(r, c));
-    const int q = q0 + r;
-    if (q < L && vec_ok && c * 8 + 8 <= L) {
-      tc::cp_async16(dst, nb + ((size_t)h * L + q) * L + c * 8);
+    const int q = q0 + r, kk = k0 + c * 8;
+    if (q < L && vec_ok && kk + 8 <= L) {
+      tc::cp_async16(dst, nb + ((size_t)h * L + q) * L + kk);
     } else {
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        dst[u] = (q < L && c * 8 + u < L) ? nb[((size_t)h * L + q) * L + c * 8 + u] : __float2bfloat16(0.f);
+        dst[u] = (q < L && kk + u < L) ? nb[((size_t)h * L + q) * L + kk + u] : __float2bfloat16(0.f);
     }
   }
 }
@@ -118,7 +118,7 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 template <int D, int LP>
 __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const bf16* dctx,
                                           const float* mbias, const AttnGeom& g, int64_t b,
-                                          int64_t h, int q0, int tid) {
+                                          int64_t h, int q0, int tid, int k0 = 0) {
   using SM = BwdSmem<D, LP>;
   constexpr int DC = D / 8;
   const int L = (int)g.L;
@@ -143,8 +143,8 @@ __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const b
   for (int e = tid; e < LP * DC; e += 512) {
     const int j = e / DC, c = e % DC;
     const int off = ((j >> 3) * DC + c) * 64 + (j & 7) * 8;
-    if (j < L) {
-      const bf16* src = qkvg + g.tok(b, j) * g.ld + HD + h * D + c * 8;
+    if (k0 + j < L) {
+      const bf16* src = qkvg + g.tok(b, k0 + j) * g.ld + HD + h * D + c * 8;
       tc::cp_async16(sK + off, src);
       tc::cp_async16(sV + off, src + HD);
     } else {
@@ -153,8 +153,8 @@ __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const b
     }
   }
   for (int j = tid; j < LP; j += 512)
-    if (j < L)
-      tc::cp_async4(sMb + j, mbias + b * L + j);  // precomputed (m - 1) * 1e9 * log2(e)
+    if (k0 + j < L)
+      tc::cp_async4(sMb + j, mbias + b * L + k0 + j);  // precomputed (m - 1) * 1e9 * log2(e)
     else
       sMb[j] = -INFINITY;
 }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     const bf16* __restrict__ qkvg, const bf16* __restrict__ dctx, const float* __restrict__ mbias,
     const bf16* __restrict__ nb, const float* __restrict__ lse, const float* __restrict__ Dvec,
     bf16* __restrict__ dqkvg, bf16* __restrict__ kvpart, float* __restrict__ dnb_part,
-    AttnGeom g, float scale, int NG) {
+    AttnGeom g, float scale, int NG, bf16* __restrict__ qpart, int NKW) {
   using SM = BwdSmem<D, LP>;
   constexpr int DC = D / 8;
   constexpr int NKC = LP / 128;
@@ -223,8 +223,12 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int grp = blockIdx.x;
   const int64_t h = blockIdx.y;
-  const int qt = blockIdx.z;
-  const int q0 = qt * 128;
+  // CTA = (batch group, head, query tile, key window of LP keys); rows longer than
+  // 256 keys use several windows, whose dQ partials (and the dK/dV partials of
+  // query tiles > 0) are combined afterwards in fixed order
+  const int qt = blockIdx.z / NKW, kw = blockIdx.z % NKW;
+  const int q0 = qt * 128, k0 = kw * LP;
+  const int64_t Ttok = g.B * g.L;
   const int L = (int)g.L;
   const int64_t HD = g.H * D;
   const int64_t b_lo = (g.B * grp) / NG, b_hi = (g.B * (grp + 1)) / NG;
@@ -242,8 +246,8 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     tc::mbar_init(&bar2[1], NCW);
   }
   if (warp < NCW) {
-    if (BIAS) stage_bias_tile<LP>(smem + SM::bias, nb, h, q0, L, tid, 512);
-    if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mbias, g, b_lo, h, q0, tid);
+    if (BIAS) stage_bias_tile<LP>(smem + SM::bias, nb, h, q0, k0, L, tid, 512);
+    if (b_lo < b_hi) bwd_stage<D, LP>(smem, qkvg, dctx, mbias, g, b_lo, h, q0, tid, k0);
     cp_async_commit();
     cp_async_wait0();
     tc::fence_proxy_async();
@@ -317,12 +321,12 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     float m2, Dv, m2n = 0.f, Dvn = 0.f;
     row_consts(b_lo, m2, Dv);
     // batch b_lo + 1 into the second buffer (nothing has read it yet)
-    if (b_lo + 1 < b_hi) bwd_stage<D, LP>(smem + SM::STAGE, qkvg, dctx, mbias, g, b_lo + 1, h, q0, tid);
+    if (b_lo + 1 < b_hi) bwd_stage<D, LP>(smem + SM::STAGE, qkvg, dctx, mbias, g, b_lo + 1, h, q0, tid, k0);
     cp_async_commit();
 
     // drain dK / dV of chunk c of batch b: lanes = keys, cg -> (dK|dV, column half)
     auto drain_kv = [&](int64_t b, int c) {
-      const int key = c * 128 + row;
+      const int key = k0 + c * 128 + row;
       const int region = cg >> 1, chalf = cg & 1;
       constexpr int DH = D / 2;
       float vv[DH];
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         for (int e = 0; e < DH; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * sc, vv[e + 1] * sc);
         const int64_t t = g.tok(b, key);
         bf16* dst = (qt == 0) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
-                              : kvpart + t * 2 * HD + region * HD + h * D + chalf * DH;
+                              : kvpart + (qt - 1) * Ttok * 2 * HD + t * 2 * HD + region * HD + h * D + chalf * DH;
 #pragma unroll
         for (int k = 0; k < DH / 8; ++k)
           reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
@@ -357,7 +361,8 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
       tc::wait_ld();
       if (valid) {
         const int64_t t = g.tok(b, i);
-        bf16* dst = dqkvg + t * g.ld + h * D + cg * DQ;
+        bf16* dst = (kw == 0) ? dqkvg + t * g.ld + h * D + cg * DQ
+                              : qpart + (kw - 1) * Ttok * HD + t * HD + h * D + cg * DQ;
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < DQ; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * scale, vv[e + 1] * scale);
@@ -441,7 +446,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           if (pend_c == NKC - 1) {
             drain_dq(pend_b);
             // every MMA that read batch b-1's buffer is complete: prefetch b+1 into it
-            if (has_next) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mbias, g, b + 1, h, q0, tid);
+            if (has_next) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mbias, g, b + 1, h, q0, tid, k0);
             cp_async_commit();
           }
           kv_pending = false;
@@ -487,8 +492,8 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
       tc::tmem_ld16(tl + C_DB + cg * PER + c, vv);
       tc::wait_ld();
       if (valid) {
-        float* dst = dnb_part + (((size_t)grp * g.H + h) * L + i) * L + cg * PER + c;
-        const int j0 = cg * PER + c;
+        float* dst = dnb_part + (((size_t)grp * g.H + h) * L + i) * L + k0 + cg * PER + c;
+        const int j0 = k0 + cg * PER + c;
         if ((L % 4) == 0 && j0 + 16 <= L) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -563,6 +568,36 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
   }
 }
 
+// dqkvg[:, 0:HD] += sum_w qpart[w] (key windows > 0), dqkvg[:, HD:3HD] += sum_q kvpart[q]
+// (query tiles > 0); fixed addend order
+__global__ void attn_part_combine_kernel(bf16* __restrict__ dqkvg, const bf16* __restrict__ qpart, int nq,
+                                         const bf16* __restrict__ kvpart, int nkv, int64_t T, int64_t ld,
+                                         int64_t HD) {
+  const int64_t per_row = 3 * HD / 8;
+  const int64_t n = T * per_row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / per_row, c = (e % per_row) * 8;
+    const bool isq = c < HD;
+    if (isq ? nq == 0 : nkv == 0) continue;
+    uint4* d = reinterpret_cast<uint4*>(dqkvg + t * ld + c);
+    float a[8], bq[8];
+    bf16x8_to_f(*d, a);
+    const int np = isq ? nq : nkv;
+    for (int k = 0; k < np; ++k) {
+      const uint4 p = isq ? *reinterpret_cast<const uint4*>(qpart + ((int64_t)k * T + t) * HD + c)
+                          : *reinterpret_cast<const uint4*>(kvpart + ((int64_t)k * T + t) * 2 * HD + c - HD);
+      bf16x8_to_f(p, bq);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += bq[u];
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) o[u / 2] = tc::pack_bf16(a[u], a[u + 1]);
+    *d = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // dqkvg[:, HD:3HD] += kvpart   (query tile 1's dK/dV partial)
 __global__ void attn_kv_combine_kernel(bf16* __restrict__ dqkvg, const bf16* __restrict__ kvpart,
                                        int64_t T, int64_t ld, int64_t HD) {
@@ -614,15 +649,16 @@ bool tc_disabled() {
 }
 
 struct BwdPlan {
-  int NQT, NG, LP;
-  int64_t off_dctx, off_dvec, off_mb, off_kv, off_part, off_cols, total;
+  int NQT, NG, LP, NKW;
+  int64_t off_dctx, off_dvec, off_mb, off_kv, off_q, off_part, off_cols, total;
 };
 
 BwdPlan bwd_plan(const AttnGeom& g) {
   BwdPlan p{};
   p.LP = g.L <= 128 ? 128 : 256;
   p.NQT = (int)((g.L + 127) / 128);
-  int per = (int)(g.H * p.NQT);
+  p.NKW = (int)((g.L + p.LP - 1) / p.LP);
+  int per = (int)(g.H * p.NQT * p.NKW);
   int ng = num_sms() / (per > 0 ? per : 1);
   if (ng < 1) ng = 1;
   if (ng > g.B) ng = (int)g.B;
@@ -634,7 +670,8 @@ BwdPlan bwd_plan(const AttnGeom& g) {
   p.off_dvec = p.off_dctx + al(T * HD * 2);
   p.off_mb = p.off_dvec + al(g.B * g.H * g.L * 4);
   p.off_kv = p.off_mb + al(g.B * g.L * 4);
-  p.off_part = p.off_kv + (p.NQT > 1 ? al(T * 2 * HD * 2) : 0);
+  p.off_q = p.off_kv + (int64_t)(p.NQT - 1) * al(T * 2 * HD * 2);
+  p.off_part = p.off_q + (int64_t)(p.NKW - 1) * al(T * HD * 2);
   p.off_cols = p.off_part + al((int64_t)p.NG * g.H * g.L * g.L * 4);
   p.total = p.off_cols + al((int64_t)(EVO_PARTIAL_BLOCKS > 8 * num_sms() ? EVO_PARTIAL_BLOCKS : 8 * num_sms()) * HD * 4);
   return p;
@@ -642,7 +679,7 @@ BwdPlan bwd_plan(const AttnGeom& g) {
 
 bool bwd_supported(const AttnGeom& g, int dtype) {
   if (tc_disabled() || dtype != EVO_BF16) return false;
-  if (!(g.D == 16 || g.D == 32) || g.L > 256 || g.L < 65) return false;
+  if (!(g.D == 16 || g.D == 32) || g.L > 1024 || g.L < 65) return false;
   if ((g.ld % 8) != 0) return false;
   return true;
 }
@@ -650,7 +687,7 @@ bool bwd_supported(const AttnGeom& g, int dtype) {
 template <int D, int LP, bool BIAS>
 void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const void* nb,
                 const float* lse, const float* Dvec, void* dqkvg, bf16* kvpart, float* part,
-                const AttnGeom& g, const BwdPlan& p, cudaStream_t s) {
+                const AttnGeom& g, const BwdPlan& p, cudaStream_t s, bf16* qpart) {
   using SM = BwdSmem<D, LP>;
   auto k = attn_bwd_tc_kernel<D, LP, BIAS>;
   static bool attr = false;
@@ -658,10 +695,10 @@ void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const voi
     EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::total));
     attr = true;
   }
-  dim3 grid((unsigned)p.NG, (unsigned)g.H, (unsigned)p.NQT);
+  dim3 grid((unsigned)p.NG, (unsigned)g.H, (unsigned)(p.NQT * p.NKW));
   const float scale = (float)(1.0 / sqrt((double)D));
   k<<<grid, 544, SM::total, s>>>((const bf16*)qkvg, dctx, mask, (const bf16*)nb, lse, Dvec,
-                                 (bf16*)dqkvg, kvpart, part, g, scale, p.NG);
+                                 (bf16*)dqkvg, kvpart, part, g, scale, p.NG, qpart, p.NKW);
   EVO_LAUNCH_CHECK();
   count_launch(1);
 }
@@ -669,13 +706,13 @@ void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const voi
 template <int D>
 void launch_bwd_d(bool bias, int LP, const void* qkvg, const bf16* dctx, const float* mask,
                   const void* nb, const float* lse, const float* Dvec, void* dqkvg, bf16* kvpart,
-                  float* part, const AttnGeom& g, const BwdPlan& p, cudaStream_t s) {
+                  float* part, const AttnGeom& g, const BwdPlan& p, cudaStream_t s, bf16* qpart) {
   if (LP == 128) {
-    if (bias) launch_bwd<D, 128, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
-    else launch_bwd<D, 128, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    if (bias) launch_bwd<D, 128, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
+    else launch_bwd<D, 128, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
   } else {
-    if (bias) launch_bwd<D, 256, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
-    else launch_bwd<D, 256, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    if (bias) launch_bwd<D, 256, true>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
+    else launch_bwd<D, 256, false>(qkvg, dctx, mask, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
   }
 }
 
@@ -698,6 +735,7 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   bf16* dctx = (bf16*)(w + p.off_dctx);
   float* Dvec = (float*)(w + p.off_dvec);
   bf16* kvpart = (bf16*)(w + p.off_kv);
+  bf16* qpart = (bf16*)(w + p.off_q);
   float* part = (float*)(w + p.off_part);
   float* cols = (float*)(w + p.off_cols);
   float* mbias = (float*)(w + p.off_mb);
@@ -719,10 +757,14 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   }
   const bool bias = nb != nullptr && dnb != nullptr;
   if (g.D == 16)
-    launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
+    launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
   else
-    launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s);
-  if (p.NQT > 1) {
+    launch_bwd_d<32>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
+  if (p.NKW > 1 || p.NQT > 2) {
+    attn_part_combine_kernel<<<cdiv(T * 3 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, qpart, p.NKW - 1, kvpart,
+                                                                        p.NQT - 1, T, g.ld, HD);
+    EVO_LAUNCH_CHECK();
+  } else if (p.NQT > 1) {
     attn_kv_combine_kernel<<<cdiv(T * 2 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, kvpart, T, g.ld, HD);
     EVO_LAUNCH_CHECK();
   }
