@@ -585,8 +585,9 @@ class BlockEngine:
 
     # -- whole model ---------------------------------------------------------------------
 
-    def blocks_fwd(self, msa, pair, feats, saved=None):
-        """All blocks forward; appends each block's saved tensors to ``saved``.
+    def blocks_fwd(self, msa, pair, feats, saved=None, inputs=None):
+        """All blocks forward; appends each block's saved tensors to ``saved``
+        and, for recompute, each block's (msa, pair) input to ``inputs``.
 
         With branch streams the OPM of block i+1 (which needs only block i's
         MSA output) is computed on the side stream right after block i's MSA
@@ -596,6 +597,8 @@ class BlockEngine:
         n = self.cfg.n_blocks
         if not self.branch_streams or n == 0:
             for i in range(n):
+                if inputs is not None:
+                    inputs.append((msa, pair))
                 msa, pair, sv = self.block_fwd(i, msa, pair, feats)
                 if saved is not None:
                     saved.append(sv)
@@ -614,6 +617,8 @@ class BlockEngine:
         side.wait_stream(main)
         nxt = opm_on_side(0, msa)
         for i in range(n):
+            if inputs is not None:
+                inputs.append((msa, pair))
             y, so, ev = nxt
             side.wait_stream(main)                   # pair (row-attention bias) is final
             with torch.cuda.stream(side):
@@ -631,8 +636,35 @@ class BlockEngine:
         main.wait_stream(side)
         return msa, pair
 
-    def blocks_bwd(self, d_msa, d_pair, saved, feats):
+    def block_refwd(self, i, msa_in, pair_in, feats):
+        """Recompute block i's saved tensors from its inputs
+        (src/trainer.py:108-179 ``recompute_grads``): same kernels, same op
+        order and the same stream placement as ``blocks_fwd`` -- the OPM
+        output is added onto the pair activations as a separate bf16 tensor
+        there, so it is here too -- so the recomputed tensors, and therefore
+        the gradients, are bitwise those of the stored-activation pass."""
+        if not self.branch_streams:
+            return self.block_fwd(i, msa_in, pair_in, feats)[2]
+        main, side = torch.cuda.current_stream(), self._side_stream()
+        y = torch.empty(pair_in.shape, dtype=self.dt, device=pair_in.device)  # main-stream allocation
+        ev = torch.cuda.Event()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            _, so = self.opm_fwd(msa_in, f"block{i}.opm", feats, pair_res=None, out=y)
+            ev.record(side)
+            _, sm = self.msa_branch_fwd(i, msa_in, pair_in, feats)
+        main.wait_event(ev)
+        pair_mid = torch.empty_like(pair_in)
+        ops.bias_residual(pair_in, y, None, pair_mid)
+        del y
+        _, sp = self.pair_branch_fwd(i, pair_mid, feats)
+        return sm, so, sp
+
+    def blocks_bwd(self, d_msa, d_pair, saved, feats, inputs=None):
         """All blocks backward, in place on (d_msa, d_pair); frees ``saved``.
+
+        With ``inputs`` (recompute) ``saved`` is unused: block i's saved tensors are recomputed from ``inputs[i]`` right before its
+        backward, so at most one block's activations are alive at a time.
 
         With branch streams the MSA branch runs on the side stream as in
         ``block_bwd``, and the OPM backward of block i -- which needs only a bf16
@@ -641,8 +673,12 @@ class BlockEngine:
         deferred reductions then alternate between two arenas and are finalised
         on the side stream once both streams' kernels of the block are done."""
         n = self.cfg.n_blocks
+        if inputs is not None:
+            saved = [None] * n
         if not self.branch_streams:
             for i in reversed(range(n)):
+                if inputs is not None:
+                    saved[i] = self.block_refwd(i, *inputs[i], feats)
                 with self.deferred():
                     self.block_bwd(i, d_msa, d_pair, saved[i], feats)
                 saved[i] = None
@@ -651,6 +687,8 @@ class BlockEngine:
         keep = []  # main-stream tensors read by the side stream: alive until the final join
         side.wait_stream(main)
         for i in reversed(range(n)):
+            if inputs is not None:
+                saved[i] = self.block_refwd(i, *inputs[i], feats)
             sm, so, sp = saved[i]
             ops.defer_begin(self.arenas[i % 2])
             late = []
@@ -682,20 +720,28 @@ class BlockEngine:
         msa, pair, _ = self.embed_fwd(feats, prev)
         return self.blocks_fwd(msa, pair, feats)
 
-    def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1):
+    def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1, recompute: bool = False):
         """``_serial_grads`` (src/harness.py:327-352): n-1 untaped recycling
         passes, one differentiated pass; grads land in the pooled region.
-        Returns (loss device tensor [1], (msa, pair))."""
+        ``recompute`` keeps only each block's inputs through the forward and
+        recomputes its activations during the backward
+        (src/trainer.py:108-179).  Returns (loss device tensor [1], (msa, pair))."""
         self.refresh_weights()
         self.st.zero_grads()
         prev = None
         for _ in range(max(0, n_cycles - 1)):
             prev = self.forward_only(feats, prev)
         msa, pair, rec = self.embed_fwd(feats, prev)
-        saved = []
-        msa, pair = self.blocks_fwd(msa, pair, feats, saved)
+        if recompute:
+            saved, inputs = None, []
+            msa, pair = self.blocks_fwd(msa, pair, feats, None, inputs)
+        else:
+            saved, inputs = [], None
+            msa, pair = self.blocks_fwd(msa, pair, feats, saved)
         loss, d_msa, d_pair = self.loss(msa, pair)
-        self.blocks_bwd(d_msa, d_pair, saved, feats)
+        self.blocks_bwd(d_msa, d_pair, saved, feats, inputs)
+        if inputs is not None:
+            inputs.clear()                       # blocks_bwd joined the side stream
         with self.deferred():
             self.embed_bwd(d_msa, d_pair, feats, rec)
         return loss, (msa, pair)

@@ -32,7 +32,7 @@ class ExecutionPlan:
     dap: int = 1
     fuse_ops: bool = True
     fuse_tensors: bool = True
-    recompute: tuple = ()
+    recompute: tuple = ()  # subset of {"evoformer"}
     act_dtype: str = "bf16"
     chunk: int = 0
     seed: int = 32
@@ -46,6 +46,15 @@ class ExecutionPlan:
             raise ContractError(f"act_dtype must be f32 or bf16, got {self.act_dtype!r}")
         if self.chunk < 0:
             raise ContractError("chunk must be >= 0")
+        unknown = set(self.recompute) - {"evoformer"}
+        if unknown:
+            raise ContractError(f"unknown recompute stacks {sorted(unknown)}")
+        if self.recompute_on and self.dp * self.bp * self.dap > 1:
+            raise ContractError("recompute is supported on single-worker plans")
+
+    @property
+    def recompute_on(self) -> bool:
+        return "evoformer" in self.recompute
 
     @property
     def torch_dtype(self):
@@ -113,7 +122,8 @@ class Trainer:
         """H2D of the staged features, fwd+bwd, optimizer; returns the
         device loss tensor (no host sync)."""
         self.feats.copy_from_host(self.host)
-        loss, _ = self.engine.forward_backward(self.feats, n_cycles)
+        loss, _ = self.engine.forward_backward(self.feats, n_cycles,
+                                               recompute=self.plan.recompute_on)
         self.store.grad_sync(None)
         self.store.step()
         return loss

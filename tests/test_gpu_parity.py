@@ -170,3 +170,31 @@ def test_bench_shape_step_gradients_finite():
     assert np.isfinite(float(loss))
     bad = [n for n in tr.store.names if not bool(torch.isfinite(tr.store.grad(n)).all())]
     assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("dtype,streams,nb,s,r", [
+    ("f32", True, 3, 16, 32), ("bf16", True, 3, 16, 32), ("bf16", False, 3, 16, 32),
+    ("bf16", True, 2, 128, 256)])
+def test_recompute_grads_bitwise_equal_direct(dtype, streams, nb, s, r):
+    """src/trainer.py:108-179: storing only block inputs and recomputing each
+    block's forward during the backward gives bitwise the loss and gradients
+    of the stored-activation pass (two recycles: the untaped pass feeds in)."""
+    from paper_2207_05477_b200.model import ModelConfig
+    from paper_2207_05477_b200.trainer import ExecutionPlan, Trainer
+    if r == 256:
+        cfg = ModelConfig(n_blocks=nb, n_seq=s, n_res=r, c_m=256, c_z=128, heads=8, opm_dim=32)
+    else:
+        cfg = ModelConfig(n_blocks=nb, n_seq=s, n_res=r, c_m=64, c_z=32, heads=2, opm_dim=8)
+    out = []
+    for rc in ((), ("evoformer",)):
+        tr = Trainer.create(cfg, ExecutionPlan(act_dtype=dtype, recompute=rc, fixed_recycles=2))
+        tr.engine.branch_streams = streams
+        loss, (msa, pair) = tr.engine.forward_backward(tr.feats, 2, recompute=tr.plan.recompute_on)
+        torch.cuda.synchronize()
+        out.append((loss.cpu(), msa.cpu(), pair.cpu(),
+                    {n: tr.store.grad(n).cpu() for n in tr.store.names}))
+    (l0, m0, p0, g0), (l1, m1, p1, g1) = out
+    assert torch.equal(l0, l1) and torch.equal(m0, m1) and torch.equal(p0, p1)
+    diff = [n for n in g0 if not torch.equal(g0[n], g1[n])]
+    assert not diff, diff[:5]
+    assert any(bool(g.abs().max() > 0) for g in g0.values())

@@ -201,3 +201,17 @@ def test_grid_config_rules():
     for bad in (dict(bp=3), dict(bp=2, dap=2), dict(dp=0)):
         with pytest.raises(ContractError):
             GridConfig(**bad)
+
+
+def test_recompute_plan_rules():
+    """src/trainer.py:44-68: only the 'evoformer' stack recomputes, on
+    single-worker plans only."""
+    from paper_2207_05477_b200.errors import ContractError
+    from paper_2207_05477_b200.trainer import ExecutionPlan
+    ExecutionPlan(recompute=("evoformer",)).validate()
+    assert ExecutionPlan(recompute=("evoformer",)).recompute_on
+    assert not ExecutionPlan().recompute_on
+    for bad in (dict(recompute=("msa",)), dict(recompute=("evoformer",), dp=2),
+                dict(recompute=("evoformer",), bp=2)):
+        with pytest.raises(ContractError):
+            ExecutionPlan(**bad).validate()
