@@ -197,6 +197,17 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
                       int swap_xy, float* dz, float* dln_g, float* dln_b,
                       float* dw_bias, int accumulate, void* ws,
                       int64_t R, int64_t C, int64_t H, void* stream);
+/* Rectangular forms for one DAP shard: z holds NI x NJ tokens (x, y) at row
+ * x*NJ + y; nb is [H, NI, NJ] (swap_xy=0) or [H, NJ, NI] (swap_xy=1).  The
+ * square entry points above are these with NI = NJ = R. */
+int evo_pair_bias_fwd_rect(const void* z, int dtype, const float* ln_g, const float* ln_b,
+                           const float* w_bias, void* nb, float* mean, float* rstd,
+                           int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap_xy, void* stream);
+int evo_pair_bias_bwd_rect(const void* z, int dtype, const float* mean, const float* rstd,
+                           const float* ln_g, const float* ln_b, const float* w_bias, const float* dnb,
+                           int swap_xy, float* dz, float* dln_g, float* dln_b,
+                           float* dw_bias, int accumulate, void* ws,
+                           int64_t NI, int64_t NJ, int64_t C, int64_t H, void* stream);
 
 /* ---- outer product mean (src/model.py:351-378) ---------------------------
  * ab: [S*R, 2k] = LN(m).[Wl|Wr]; a = (ab[:, :k]+bl)*mask, c = (ab[:, k:]+br)*mask
@@ -213,6 +224,19 @@ int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* r
 /* dnum[i*k+p, j*k+q] = doutn[i,j,p*k+q] * rec[i,j] */
 int evo_opm_norm_bwd(const void* doutn, int in_dtype, const float* rec, void* dnum,
                      int out_dtype, int64_t R, int64_t k, void* stream);
+/* Row-shard forms (DAP, src/model.py:375 reduce-scatter): num / dnum hold the
+ * NI rows i0..i0+NI-1 ([NI*k, R*k]); rec and outn / doutn are [NI*R, ...];
+ * the mask is the full [S, R] one. */
+int evo_opm_norm_fwd_rows(const void* num, int num_dtype, const float* mask, float* rec,
+                          void* outn, int out_dtype, int64_t S, int64_t R, int64_t k,
+                          int64_t i0, int64_t NI, void* stream);
+int evo_opm_norm_bwd_rows(const void* doutn, int in_dtype, const float* rec, void* dnum,
+                          int out_dtype, int64_t R, int64_t k, int64_t NI, void* stream);
+
+/* ---- DAP re-layout (src/harness.py:262-293) ------------------------------
+ * dst[b, a, :] = src[a, b, :] for src [A, B, elem_bytes]: the outer-axis swap
+ * that brackets every DAP all-to-all / all-gather / reduce-scatter. */
+int evo_swap01(const void* src, void* dst, int64_t A, int64_t B, int64_t elem_bytes, void* stream);
 
 /* ---- loss (src/harness.py:313-320) ---------------------------------------
  * loss = km*sum(msa^2) + kz*sum(pair^2);  dmsa = 2*km*msa, dpair = 2*kz*pair (fp32). */

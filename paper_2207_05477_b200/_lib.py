@@ -58,6 +58,12 @@ SIGNATURES = {
     "evo_attn_bwd": (_i, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _sz,
                           _i64, _i64, _i64, _i64, _i64, _i64, _i, _p]),
     "evo_pair_bias_fwd": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i, _p]),
+    "evo_pair_bias_fwd_rect": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _p]),
+    "evo_pair_bias_bwd_rect": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _i, _p,
+                                    _i64, _i64, _i64, _i64, _p]),
+    "evo_opm_norm_fwd_rows": (_i, [_p, _i, _p, _p, _p, _i, _i64, _i64, _i64, _i64, _i64, _p]),
+    "evo_opm_norm_bwd_rows": (_i, [_p, _i, _p, _p, _i, _i64, _i64, _i64, _p]),
+    "evo_swap01": (_i, [_p, _p, _i64, _i64, _i64, _p]),
     "evo_pair_bias_bwd_workspace": (_i64, [_i64, _i64]),
     "evo_pair_bias_bwd": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _i, _p,
                                _i64, _i64, _i64, _p]),

@@ -414,7 +414,7 @@ template <int C, typename T>
 __global__ void __launch_bounds__(GT) pair_bias_fwd_vec_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
     const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
-    float* __restrict__ rstd, int64_t R, int H, int swap_xy) {
+    float* __restrict__ rstd, int64_t NI, int64_t NJ, int H, int swap_xy) {
   using M = PbMap<C>;
   constexpr int U = M::U;
   const int l = threadIdx.x % M::LANES;
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(GT) pair_bias_fwd_vec_kernel(
     }
   const int hme = pb_head<M::LANES>(l);
   const bool writer = (l & (M::LANES / 8 - 1)) == 0 && hme < H;
-  const int64_t NT = R * R;
+  const int64_t NT = NI * NJ;
   for (int64_t tb = blockIdx.x * (int64_t)(M::GROUPS * U); tb < NT; tb += (int64_t)gridDim.x * M::GROUPS * U) {
     float v[U][M::CH][4];
     int64_t t[U];
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(GT) pair_bias_fwd_vec_kernel(
       const float mine = head_reduce8<M::LANES>(p, l);
       const bool act = tb + u * M::GROUPS + grp < NT;
       if (act && writer) {
-        const int64_t x = t[u] / R, y = t[u] % R;
-        const int64_t o = swap_xy ? ((int64_t)hme * R + y) * R + x : ((int64_t)hme * R + x) * R + y;
+        const int64_t x = t[u] / NJ, y = t[u] % NJ;
+        const int64_t o = swap_xy ? ((int64_t)hme * NJ + y) * NI + x : ((int64_t)hme * NI + x) * NJ + y;
         nb[o] = from_f<T>(mine);
       }
       if (act && l == 0) {
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(GT) pair_bias_bwd_vec_kernel(
     const T* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
     const float* __restrict__ dnb, int swap_xy, float* __restrict__ dz,
-    float* __restrict__ partials, int64_t R, int H) {
+    float* __restrict__ partials, int64_t NI, int64_t NJ, int H) {
   using M = PbMap<C>;
   constexpr int U = M::U;
   extern __shared__ float red[];  // [GROUPS][C*H + 2C]
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(GT) pair_bias_bwd_vec_kernel(
       }
     }
   const int base = (threadIdx.x & 31) - l;  // first lane of this row group
-  const int64_t NT = R * R;
+  const int64_t NT = NI * NJ;
   const int64_t t0 = (NT * blockIdx.x) / gridDim.x, t1 = (NT * (blockIdx.x + 1)) / gridDim.x;
   for (int64_t tb = t0; tb < t1; tb += M::GROUPS * U) {
     int64_t t[U];
@@ -526,10 +526,10 @@ __global__ void __launch_bounds__(GT) pair_bias_bwd_vec_kernel(
     for (int u = 0; u < U; ++u) {
       act[u] = tb + u * M::GROUPS + grp < t1;
       t[u] = act[u] ? tb + u * M::GROUPS + grp : t1 - 1;
-      const int64_t x = t[u] / R, y = t[u] % R;
+      const int64_t x = t[u] / NJ, y = t[u] % NJ;
       dpm[u] = 0.f;
       if (act[u] && l < H) {  // inactive groups carry dP = 0: no contribution anywhere
-        const int64_t od = swap_xy ? ((int64_t)l * R + y) * R + x : ((int64_t)l * R + x) * R + y;
+        const int64_t od = swap_xy ? ((int64_t)l * NJ + y) * NI + x : ((int64_t)l * NI + x) * NJ + y;
         dpm[u] = dnb[od];
       }
       mu[u] = mean[t[u]];
@@ -692,12 +692,14 @@ __global__ void __launch_bounds__(GT) pack_cols_kernel(const __grid_constant__ P
   }
 }
 
-// rec[i, j] = 1 / (sum_s m[s, i] m[s, j] + 1e-3)   (block per i; exact integer sums)
+// rec[i, j] = 1 / (sum_s m[s, i0 + i] m[s, j] + 1e-3)   (block per local row i; exact
+// integer sums).  i0 > 0: the rows of one DAP shard (src/model.py:351-378 sharded)
 __global__ void __launch_bounds__(GT) opm_rec_vec_kernel(const float* __restrict__ mask,
-                                                         float* __restrict__ rec, int64_t S, int64_t R) {
+                                                         float* __restrict__ rec, int64_t S, int64_t R,
+                                                         int64_t i0) {
   extern __shared__ float mi[];  // [S]
   const int64_t i = blockIdx.x;
-  for (int64_t s = threadIdx.x; s < S; s += GT) mi[s] = mask[s * R + i];
+  for (int64_t s = threadIdx.x; s < S; s += GT) mi[s] = mask[s * R + i0 + i];
   __syncthreads();
   for (int64_t j = threadIdx.x; j < R; j += GT) {
     float acc = 0.f;
@@ -856,17 +858,17 @@ bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, 
 }
 
 bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
-                       float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap,
+                       float* mean, float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap,
                        cudaStream_t s) {
   if (!pow2_width(C) || C > 256 || H > 8 || !al16(z)) return false;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
       using M = PbMap<CC>;
       // resident blocks only: each block loads its slice of w once and loops
-      unsigned grid = glue_grid(R * R, M::GROUPS * M::U, 3);
+      unsigned grid = glue_grid(NI * NJ, M::GROUPS * M::U, 3);
       EVO_DISPATCH_T(dt, T, {
         pair_bias_fwd_vec_kernel<CC, T><<<grid, GT, 0, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd,
-                                                            R, (int)H, swap);
+                                                            NI, NJ, (int)H, swap);
       });
     } else {
       return false;
@@ -883,22 +885,22 @@ int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) {
 
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
-                       float* dg, float* db, float* dw, int accumulate, void* ws, int64_t R,
-                       int64_t C, int64_t H, cudaStream_t s) {
+                       float* dg, float* db, float* dw, int accumulate, void* ws, int64_t NI,
+                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s) {
   if (!pow2_width(C) || C > 256 || H > 8 || !al16(z) || !al16(dz)) return false;
   ws = partial_buffer(ws, pair_bias_bwd_vec_ws(C, H));
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {
       using M = PbMap<CC>;
-      grid = glue_grid(R * R, M::GROUPS * M::U, PB_PARTIAL_PER_SM);
+      grid = glue_grid(NI * NJ, M::GROUPS * M::U, PB_PARTIAL_PER_SM);
       const int W = (int)(CC * H + 2 * CC);
       const size_t smem = (size_t)M::GROUPS * W * sizeof(float);
       EVO_DISPATCH_T(dt, T, {
         auto k = pair_bias_bwd_vec_kernel<CC, T>;
         if (smem > 48 * 1024)
           EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k<<<grid, GT, smem, s>>>((const T*)z, mean, rstd, g, bln, w, dnb, swap, dz, (float*)ws, R, (int)H);
+        k<<<grid, GT, smem, s>>>((const T*)z, mean, rstd, g, bln, w, dnb, swap, dz, (float*)ws, NI, NJ, (int)H);
       });
     } else {
       return false;
@@ -914,14 +916,14 @@ bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rs
 }
 
 bool opm_norm_vec(bool fwd, const void* src, int sdt, const float* mask, float* rec, void* dst, int ddt,
-                  int64_t S, int64_t R, int64_t k, cudaStream_t s) {
+                  int64_t S, int64_t R, int64_t k, int64_t i0, int64_t NI, cudaStream_t s) {
   if (k != OPM_K || (R % OPM_JT) != 0 || !al16(src) || !al16(dst)) return false;
   if (fwd) {
-    opm_rec_vec_kernel<<<(unsigned)R, GT, S * sizeof(float), s>>>(mask, rec, S, R);
+    opm_rec_vec_kernel<<<(unsigned)NI, GT, S * sizeof(float), s>>>(mask, rec, S, R, i0);
     EVO_LAUNCH_CHECK();
     count_launch(1);
   }
-  dim3 grid((unsigned)(R / OPM_JT), (unsigned)R);
+  dim3 grid((unsigned)(R / OPM_JT), (unsigned)NI);
   EVO_DISPATCH_T(sdt, TI, EVO_DISPATCH_T(ddt, TO, {
     if (fwd)
       opm_relayout_kernel<TI, TO, true><<<grid, GT, 0, s>>>((const TI*)src, rec, (TO*)dst, R);

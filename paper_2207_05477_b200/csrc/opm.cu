@@ -85,11 +85,11 @@ __global__ void __launch_bounds__(256) opm_proj_bwd_vec_kernel(const T* __restri
 }
 
 __global__ void opm_rec_kernel(const float* __restrict__ mask, float* __restrict__ rec, int64_t S,
-                               int64_t R) {
-  const int64_t n = R * R;
+                               int64_t R, int64_t i0, int64_t NI) {
+  const int64_t n = NI * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / R, j = e % R;
+    const int64_t i = i0 + e / R, j = e % R;
     float acc = 0.f;
     for (int64_t s = 0; s < S; ++s) acc += mask[s * R + i] * mask[s * R + j];
     rec[e] = 1.0f / (acc + 1e-3f);
@@ -158,7 +158,7 @@ __global__ void sq_loss_final_kernel(const float* __restrict__ pm, const float* 
 }
 
 bool opm_norm_vec(bool fwd, const void* src, int sdt, const float* mask, float* rec, void* dst, int ddt,
-                  int64_t S, int64_t R, int64_t k, cudaStream_t s);
+                  int64_t S, int64_t R, int64_t k, int64_t i0, int64_t NI, cudaStream_t s);
 
 }  // namespace evo
 
@@ -206,36 +206,51 @@ int evo_opm_proj_bwd(const void* da, const void* dc, const float* mask, void* d_
   EVO_API_END
 }
 
-int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* rec, void* outn,
-                     int out_dtype, int64_t S, int64_t R, int64_t k, void* stream) {
+int evo_opm_norm_fwd_rows(const void* num, int num_dtype, const float* mask, float* rec, void* outn,
+                          int out_dtype, int64_t S, int64_t R, int64_t k, int64_t i0, int64_t NI,
+                          void* stream) {
   EVO_API_BEGIN
+  EVO_REQUIRE(i0 >= 0 && NI >= 0 && i0 + NI <= R, EVO_ERR_ARG, "opm_norm: row range outside [0, R)");
+  if (NI * R == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (opm_norm_vec(true, num, num_dtype, mask, rec, outn, out_dtype, S, R, k, s)) return EVO_OK;
-  opm_rec_kernel<<<cdiv(R * R, 256), 256, 0, s>>>(mask, rec, S, R);
+  if (opm_norm_vec(true, num, num_dtype, mask, rec, outn, out_dtype, S, R, k, i0, NI, s)) return EVO_OK;
+  opm_rec_kernel<<<cdiv(NI * R, 256), 256, 0, s>>>(mask, rec, S, R, i0, NI);
   EVO_LAUNCH_CHECK();
   int bs = (int)(k * k < 256 ? ((k * k + 31) / 32) * 32 : 256);
   EVO_DISPATCH_T(num_dtype, TI, EVO_DISPATCH_T(out_dtype, TO, {
-    opm_norm_fwd_kernel<TI, TO><<<(unsigned)(R * R), bs, 0, s>>>((const TI*)num, rec, (TO*)outn, R, (int)k);
+    opm_norm_fwd_kernel<TI, TO><<<(unsigned)(NI * R), bs, 0, s>>>((const TI*)num, rec, (TO*)outn, R, (int)k);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(2);
   EVO_API_END
 }
 
-int evo_opm_norm_bwd(const void* doutn, int in_dtype, const float* rec, void* dnum, int out_dtype,
-                     int64_t R, int64_t k, void* stream) {
+int evo_opm_norm_fwd(const void* num, int num_dtype, const float* mask, float* rec, void* outn,
+                     int out_dtype, int64_t S, int64_t R, int64_t k, void* stream) {
+  return evo_opm_norm_fwd_rows(num, num_dtype, mask, rec, outn, out_dtype, S, R, k, 0, R, stream);
+}
+
+int evo_opm_norm_bwd_rows(const void* doutn, int in_dtype, const float* rec, void* dnum, int out_dtype,
+                          int64_t R, int64_t k, int64_t NI, void* stream) {
   EVO_API_BEGIN
-  if (opm_norm_vec(false, doutn, in_dtype, nullptr, const_cast<float*>(rec), dnum, out_dtype, 0, R, k,
-                   (cudaStream_t)stream))
+  EVO_REQUIRE(NI >= 0 && NI <= R, EVO_ERR_ARG, "opm_norm: row count outside [0, R]");
+  if (NI * R == 0) return EVO_OK;
+  if (opm_norm_vec(false, doutn, in_dtype, nullptr, const_cast<float*>(rec), dnum, out_dtype, 0, R, k, 0,
+                   NI, (cudaStream_t)stream))
     return EVO_OK;
   int bs = (int)(k * k < 256 ? ((k * k + 31) / 32) * 32 : 256);
   EVO_DISPATCH_T(in_dtype, TI, EVO_DISPATCH_T(out_dtype, TO, {
-    opm_norm_bwd_kernel<TI, TO><<<(unsigned)(R * R), bs, 0, (cudaStream_t)stream>>>(
+    opm_norm_bwd_kernel<TI, TO><<<(unsigned)(NI * R), bs, 0, (cudaStream_t)stream>>>(
         (const TI*)doutn, rec, (TO*)dnum, R, (int)k);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);
   EVO_API_END
+}
+
+int evo_opm_norm_bwd(const void* doutn, int in_dtype, const float* rec, void* dnum, int out_dtype,
+                     int64_t R, int64_t k, void* stream) {
+  return evo_opm_norm_bwd_rows(doutn, in_dtype, rec, dnum, out_dtype, R, k, R, stream);
 }
 
 int64_t evo_sq_loss_workspace(void) { return 2 * EVO_PARTIAL_BLOCKS * 4; }

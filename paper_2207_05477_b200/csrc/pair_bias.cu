@@ -22,10 +22,10 @@ template <typename T, int NPL>
 __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
     const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
-    float* __restrict__ rstd, int64_t R, int C, int H, int swap_xy) {
+    float* __restrict__ rstd, int64_t NI, int64_t NJ, int C, int H, int swap_xy) {
   const int lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x * (int64_t)PB_WARPS + (threadIdx.x >> 5);
-  if (t >= R * R) return;
+  if (t >= NI * NJ) return;
   float v[NPL];
   float s = 0.f;
 #pragma unroll
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
     int c = lane + 32 * k;
     v[k] = c < C ? (v[k] - mu) * inv * g[c] + b[c] : 0.f;
   }
-  const int64_t x = t / R, y = t % R;
+  const int64_t x = t / NJ, y = t % NJ;
   float mine = 0.f;
 #pragma unroll
   for (int h = 0; h < PB_HMAX; ++h) {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_fwd_kernel(
     }
   }
   if (lane < H) {
-    int64_t o = swap_xy ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+    int64_t o = swap_xy ? ((int64_t)lane * NJ + y) * NI + x : ((int64_t)lane * NI + x) * NJ + y;
     nb[o] = from_f<T>(mine);
   }
   if (lane == 0) {
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
     const T* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
     const float* __restrict__ dnb, int swap_xy, float* __restrict__ dz,
-    float* __restrict__ partials, int64_t R, int C, int H) {
+    float* __restrict__ partials, int64_t NI, int64_t NJ, int C, int H) {
   extern __shared__ float sm[];  // [PB_WARPS][C*H + 2C]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int W = C * H + 2 * C;
@@ -89,12 +89,12 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
 #pragma unroll
     for (int h = 0; h < PB_HMAX; ++h) dw[k][h] = 0.f;
   }
-  for (int64_t t = blockIdx.x * (int64_t)PB_WARPS + warp; t < R * R;
+  for (int64_t t = blockIdx.x * (int64_t)PB_WARPS + warp; t < NI * NJ;
        t += (int64_t)gridDim.x * PB_WARPS) {
-    const int64_t x = t / R, y = t % R;
+    const int64_t x = t / NJ, y = t % NJ;
     float dp = 0.f;
     if (lane < H) {
-      int64_t o = swap_xy ? ((int64_t)lane * R + y) * R + x : ((int64_t)lane * R + x) * R + y;
+      int64_t o = swap_xy ? ((int64_t)lane * NJ + y) * NI + x : ((int64_t)lane * NI + x) * NJ + y;
       dp = dnb[o];
     }
     float dP[PB_HMAX];
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32) pair_bias_bwd_kernel(
   } while (0)
 
 bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
-                       float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap,
+                       float* mean, float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap,
                        cudaStream_t s);
 
 // Thread-per-token forward: each thread owns one token row (no cross-lane
@@ -171,7 +171,7 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
 // projection), and keeps the 8 head accumulators in registers; LN affine and
 // w_bias are broadcast from shared memory.  Threads walk the tokens in output
 // order -- for the transposed triangle-end layout (swap) thread i handles token
-// (i % R, i / R) -- so the 8 head planes of nb are written coalesced.
+// (i % NI, i / NI) -- so the 8 head planes of nb are written coalesced.
 __device__ __forceinline__ uint32_t tc_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -190,19 +190,19 @@ template <int C, typename T>
 __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
     const T* __restrict__ z, const float* __restrict__ g, const float* __restrict__ b,
     const float* __restrict__ w, T* __restrict__ nb, float* __restrict__ mean,
-    float* __restrict__ rstd, int64_t R, int H, int swap) {
+    float* __restrict__ rstd, int64_t NI, int64_t NJ, int H, int swap) {
   using TL = PbTile<C, T>;
   extern __shared__ __align__(16) uint8_t tile[];
   __shared__ float4 sw[C][2];   // w[c, 0..7] (zero beyond H)
   __shared__ float2 sgb[C];     // (gamma, beta)
-  const int64_t RR = R * R;
+  const int64_t RR = NI * NJ;
   const int64_t i0 = blockIdx.x * (int64_t)128;
   // stage: chunk k of row r by thread (r * CPR + k) % 128
   for (int e = threadIdx.x; e < 128 * TL::CPR; e += 128) {
     const int r = e / TL::CPR, k = e % TL::CPR;
     const int64_t i = i0 + r;
     if (i < RR) {
-      const int64_t tok = swap ? (i % R) * R + i / R : i;
+      const int64_t tok = swap ? (i % NI) * NJ + i / NI : i;
       tc::cp_async16(tile + r * TL::ROWB + k * 16, reinterpret_cast<const uint8_t*>(z + tok * C) + k * 16);
     }
   }
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
   __syncthreads();
   const int64_t i = i0 + threadIdx.x;
   if (i >= RR) return;
-  const int64_t tok = swap ? (i % R) * R + i / R : i;
+  const int64_t tok = swap ? (i % NI) * NJ + i / NI : i;
   const uint8_t* row = tile + threadIdx.x * TL::ROWB;
   auto chunk = [&](int c, float (&f)[8]) {
     Vec8<T> v;
@@ -278,9 +278,10 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
 }
 
 bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
-                       float* mean, float* rstd, int64_t R, int64_t C, int64_t H, int swap, cudaStream_t s) {
+                       float* mean, float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap,
+                       cudaStream_t s) {
   if (H > 8 || (C % 8) != 0 || (((uintptr_t)z) & 15) != 0) return false;
-  const int64_t RR = R * R;
+  const int64_t RR = NI * NJ;
   const unsigned grid = (unsigned)((RR + 127) / 128);
   bool done = true;
   auto go = [&](auto cc) {
@@ -293,7 +294,7 @@ bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, co
         EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
         attr = true;
       }
-      k<<<grid, 128, SMEM, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd, R, (int)H, swap);
+      k<<<grid, 128, SMEM, s>>>((const T*)z, g, b, w, (T*)nb, mean, rstd, NI, NJ, (int)H, swap);
     });
   };
   if (C == 32) go(std::integral_constant<int, 32>{});
@@ -310,8 +311,8 @@ bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, co
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
-                       float* dg, float* db, float* dw, int accumulate, void* ws, int64_t R,
-                       int64_t C, int64_t H, cudaStream_t s);
+                       float* dg, float* db, float* dw, int accumulate, void* ws, int64_t NI,
+                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s);
 
 }  // namespace evo
 
@@ -319,25 +320,32 @@ using namespace evo;
 
 extern "C" {
 
-int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
-                      const float* w_bias, void* nb, float* mean, float* rstd, int64_t R,
-                      int64_t C, int64_t H, int swap_xy, void* stream) {
+int evo_pair_bias_fwd_rect(const void* z, int dtype, const float* ln_g, const float* ln_b,
+                           const float* w_bias, void* nb, float* mean, float* rstd, int64_t NI,
+                           int64_t NJ, int64_t C, int64_t H, int swap_xy, void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
-  if (R == 0) return EVO_OK;
+  EVO_REQUIRE(NI >= 0 && NJ >= 0, EVO_ERR_ARG, "pair_bias: negative extent");
+  if (NI * NJ == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (pair_bias_fwd_tpt(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, C, H, swap_xy, s))
+  if (pair_bias_fwd_tpt(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, NI, NJ, C, H, swap_xy, s))
     return EVO_OK;
-  if (pair_bias_fwd_vec(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, C, H, swap_xy, s))
+  if (pair_bias_fwd_vec(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, NI, NJ, C, H, swap_xy, s))
     return EVO_OK;
-  unsigned grid = cdiv(R * R, PB_WARPS);
+  unsigned grid = cdiv(NI * NJ, PB_WARPS);
   PB_NPL_DISPATCH(C, NPL, EVO_DISPATCH_T(dtype, T, {
     pair_bias_fwd_kernel<T, NPL><<<grid, PB_WARPS * 32, 0, s>>>(
-        (const T*)z, ln_g, ln_b, w_bias, (T*)nb, mean, rstd, R, (int)C, (int)H, swap_xy);
+        (const T*)z, ln_g, ln_b, w_bias, (T*)nb, mean, rstd, NI, NJ, (int)C, (int)H, swap_xy);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);
   EVO_API_END
+}
+
+int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
+                      const float* w_bias, void* nb, float* mean, float* rstd, int64_t R,
+                      int64_t C, int64_t H, int swap_xy, void* stream) {
+  return evo_pair_bias_fwd_rect(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, R, R, C, H, swap_xy, stream);
 }
 
 int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H) {
@@ -345,20 +353,21 @@ int64_t evo_pair_bias_bwd_workspace(int64_t C, int64_t H) {
   return a > b ? a : b;
 }
 
-int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
-                      const float* ln_g, const float* ln_b, const float* w_bias,
-                      const float* dnb, int swap_xy, float* dz, float* dln_g,
-                      float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t R,
-                      int64_t C, int64_t H, void* stream) {
+int evo_pair_bias_bwd_rect(const void* z, int dtype, const float* mean, const float* rstd,
+                           const float* ln_g, const float* ln_b, const float* w_bias,
+                           const float* dnb, int swap_xy, float* dz, float* dln_g,
+                           float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t NI,
+                           int64_t NJ, int64_t C, int64_t H, void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(H >= 1 && H <= PB_HMAX, EVO_ERR_UNSUPPORTED, "pair_bias: heads must be in [1,16]");
   EVO_REQUIRE(ws != nullptr, EVO_ERR_ARG, "pair_bias_bwd: workspace required");
-  if (R == 0) return EVO_OK;
+  EVO_REQUIRE(NI >= 0 && NJ >= 0, EVO_ERR_ARG, "pair_bias: negative extent");
+  if (NI * NJ == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (pair_bias_bwd_vec(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b,
-                        dw_bias, accumulate, ws, R, C, H, s))
+                        dw_bias, accumulate, ws, NI, NJ, C, H, s))
     return EVO_OK;
-  const int64_t want = (R * R + PB_WARPS - 1) / PB_WARPS;
+  const int64_t want = (NI * NJ + PB_WARPS - 1) / PB_WARPS;
   unsigned grid = (unsigned)(want < EVO_PARTIAL_BLOCKS ? want : EVO_PARTIAL_BLOCKS);
   const int64_t W = C * H + 2 * C;
   size_t smem = (size_t)PB_WARPS * W * sizeof(float);
@@ -368,7 +377,7 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
     if (smem > 48 * 1024)
       EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<grid, PB_WARPS * 32, smem, s>>>((const T*)z, mean, rstd, ln_g, ln_b, w_bias, dnb,
-                                         swap_xy, dz, part, R, (int)C, (int)H);
+                                         swap_xy, dz, part, NI, NJ, (int)C, (int)H);
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);
@@ -376,6 +385,15 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
   finalize_partials(part + C * H, grid, C, dln_g, accumulate, s, W);
   finalize_partials(part + C * H + C, grid, C, dln_b, accumulate, s, W);
   EVO_API_END
+}
+
+int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* rstd,
+                      const float* ln_g, const float* ln_b, const float* w_bias,
+                      const float* dnb, int swap_xy, float* dz, float* dln_g,
+                      float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t R,
+                      int64_t C, int64_t H, void* stream) {
+  return evo_pair_bias_bwd_rect(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b,
+                                dw_bias, accumulate, ws, R, R, C, H, stream);
 }
 
 }  // extern "C"

@@ -45,6 +45,9 @@ class Variant:
     mask: str          # "msa" or "pair"
     bias: bool         # pair-derived bias present
     swap_xy: bool      # nb[h, i, j] = P[j, i, h] (triangle end) instead of P[i, j, h]
+    moff: int = 0      # mask element offset (a DAP shard's first row / column)
+    ni: int = 0        # bias source extent [ni, nj] (0: the square n_res x n_res pair)
+    nj: int = 0
 
 
 def variants(cfg: ModelConfig) -> dict:
@@ -91,6 +94,9 @@ class BlockEngine:
         self.st = store
         self.dt = act_dtype
         self.var = variants(cfg)
+        # this worker's shard: sequences s0.., residue rows r0..r0+r_loc (whole model here)
+        self.s0, self.r0, self.r_loc = 0, 0, cfg.n_res
+        self.opm_num_dtype = act_dtype
         # MSA branch on a second stream (EVO_BRANCH_STREAMS=0 disables)
         import os
         self.branch_streams = (torch.device(store.device).type == "cuda"
@@ -159,6 +165,24 @@ class BlockEngine:
     def mask(self, feats: DeviceFeatures, which: str):
         return feats.msa_mask if which == "msa" else feats.pair_mask
 
+    # -- sharding hooks: identities here, collectives in the DAP engine (dap.py) ----
+
+    def _gather_bias(self, nb, v: Variant):
+        return nb
+
+    def _scatter_dbias(self, dnb, v: Variant):
+        return dnb
+
+    def _opm_reduce(self, num):
+        return num
+
+    def _opm_gather(self, dnum):
+        return dnum
+
+    def _feat_rows(self, feats: DeviceFeatures):
+        """(msa_feat, pair_feat, msa_mask) rows of this worker's shard."""
+        return feats.msa_feat, feats.pair_feat, feats.msa_mask
+
     def _ln_bwd_chain(self, x, dxl, mu, rs, prefix, d, nxt):
         """LayerNorm backward into the residual gradient d (in place).  With
         ``nxt`` (the output-bias gradient slot of the module that runs next in
@@ -187,10 +211,12 @@ class BlockEngine:
             z = pair if pair is not None else x
             nb, pmu, prs = ops.pair_bias_fwd(z, self.P(f"{prefix}.bias_ln_g"),
                                              self.P(f"{prefix}.bias_ln_b"),
-                                             self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.swap_xy)
+                                             self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.swap_xy,
+                                             ni=v.ni or None, nj=v.nj or None)
+            nb = self._gather_bias(nb, v)
         qkvg = torch.empty((T, 4 * HD), dtype=dt, device=x.device)
         ops.gemm(xl, self.wcat[prefix], qkvg)                         # one merged projection
-        mask = self.mask(feats, v.mask)
+        mask = self.mask(feats, v.mask)[v.moff:]
         ctx, gate, gated, lse = ops.attn_fwd(qkvg, mask, v.msb, v.msl, nb,
                                              self.P(f"{prefix}.attn.bg"), v.B, v.L, H, D, v.sb, v.sl)
         out = torch.empty((T, C), dtype=dt, device=x.device)
@@ -218,11 +244,13 @@ class BlockEngine:
         dgated = torch.empty((T, HD), dtype=dt, device=d.device)
         ops.gemm(d_act, self.W(f"{prefix}.attn.wo", HD), dgated, tb=True)
         del d_act
-        mask = self.mask(feats, v.mask)
+        mask = self.mask(feats, v.mask)[v.moff:]
         dqkvg, dnb = ops.attn_bwd(sv["qkvg"], mask, v.msb, v.msl, sv["nb"], sv["ctx"], sv["gate"],
                                   dgated, sv["lse"], self.G(f"{prefix}.attn.bg"), v.B, v.L, H, D,
                                   v.sb, v.sl, want_dbias=v.bias)
         del dgated
+        if v.bias:
+            dnb = self._scatter_dbias(dnb, v)
         xl = sv["xl"]
         dwcat = torch.empty((C, 4 * HD), dtype=F32, device=d.device)
         ops.gemm(xl, dqkvg, dwcat, ta=True)                           # d[Wq|Wk|Wv|Wg] in one GEMM
@@ -239,7 +267,7 @@ class BlockEngine:
                                   self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
                                   v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
                                   self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
-                                  cfg.n_res, H)
+                                  cfg.n_res, H, ni=v.ni or None, nj=v.nj or None)
             if dpair is not None and late is not None:
                 late.append(pair_bias_bwd)  # into the pair gradient: run by the caller after its join
             else:
@@ -286,19 +314,21 @@ class BlockEngine:
         cfg, dt = self.cfg, self.dt
         S, R, k = cfg.n_seq, cfg.n_res, cfg.opm_dim
         SR, Cm = msa_in.shape
+        s_loc, r_loc = SR // R, self.r_loc
         xl, mu, rs = ops.layernorm(msa_in, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
         ab = torch.empty((SR, 2 * k), dtype=dt, device=msa_in.device)
         ops.gemm(xl, self.W(f"{prefix}.w_left", Cm), ab[:, :k])
         ops.gemm(xl, self.W(f"{prefix}.w_right", Cm), ab[:, k:])
         a, c = ops.opm_proj(ab, self.P(f"{prefix}.b_left"), self.P(f"{prefix}.b_right"),
-                            feats.msa_mask, k)
+                            self._feat_rows(feats)[2], k)
         del ab
-        num = torch.empty((R * k, R * k), dtype=dt, device=msa_in.device)
-        ops.gemm(a.view(S, R * k), c.view(S, R * k), num, ta=True)
-        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt)
+        num = torch.empty((R * k, R * k), dtype=self.opm_num_dtype, device=msa_in.device)
+        ops.gemm(a.view(s_loc, R * k), c.view(s_loc, R * k), num, ta=True)
+        num = self._opm_reduce(num)            # the shard's rows of the sum over all sequences
+        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt, i0=self.r0, ni=r_loc)
         del num
         if out is None:
-            out = torch.empty((R * R, cfg.c_z), dtype=dt, device=msa_in.device)
+            out = torch.empty((r_loc * R, cfg.c_z), dtype=dt, device=msa_in.device)
         ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res,
                       bias16=self.st.weight(f"{prefix}.b_out"))
         return out, dict(x=msa_in, xl=xl, mu=mu, rs=rs, a=a, c=c, rec=rec, outn=outn)
@@ -319,15 +349,17 @@ class BlockEngine:
         doutn = torch.empty((RR, k * k), dtype=dt, device=dev)
         ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
         del d_act
-        dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt)
+        dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt, ni=self.r_loc)
         del doutn
-        a2, c2 = sv["a"].view(S, R * k), sv["c"].view(S, R * k)
-        da = torch.empty((S, R * k), dtype=dt, device=dev)
-        dc = torch.empty((S, R * k), dtype=dt, device=dev)
+        dnum = self._opm_gather(dnum)
+        s_loc = SR // R
+        a2, c2 = sv["a"].view(s_loc, R * k), sv["c"].view(s_loc, R * k)
+        da = torch.empty((s_loc, R * k), dtype=dt, device=dev)
+        dc = torch.empty((s_loc, R * k), dtype=dt, device=dev)
         ops.gemm(c2, dnum, da, tb=True)
         ops.gemm(a2, dnum, dc)
         del dnum
-        d_ab = ops.opm_proj_bwd(da, dc, feats.msa_mask, self.G(f"{prefix}.b_left"),
+        d_ab = ops.opm_proj_bwd(da, dc, self._feat_rows(feats)[2], self.G(f"{prefix}.b_left"),
                                 self.G(f"{prefix}.b_right"), k)
         xl = sv["xl"]
         ops.gemm(xl, d_ab[:, :k], self.Gm(f"{prefix}.w_left", Cm), ta=True)
@@ -518,21 +550,25 @@ class BlockEngine:
 
     def embed_fwd(self, feats: DeviceFeatures, prev=None):
         cfg, dt = self.cfg, self.dt
-        S, R = cfg.n_seq, cfg.n_res
-        dev = feats.msa_feat.device
-        ym = torch.empty((S * R, cfg.c_m), dtype=F32, device=dev)
-        ops.gemm(feats.msa_feat, self.P("msa_embed.w"), ym)
-        msa = torch.empty((S * R, cfg.c_m), dtype=dt, device=dev)
+        R = cfg.n_res
+        mf, pf, _ = self._feat_rows(feats)
+        dev = mf.device
+        ym = torch.empty((mf.shape[0], cfg.c_m), dtype=F32, device=dev)
+        ops.gemm(mf, self.P("msa_embed.w"), ym)
+        msa = torch.empty((mf.shape[0], cfg.c_m), dtype=dt, device=dev)
         ops.bias_residual(None, ym, self.P("msa_embed.b"), msa)
-        yz = torch.empty((R * R, cfg.c_z), dtype=F32, device=dev)
-        ops.gemm(feats.pair_feat, self.P("pair_embed.w"), yz)
-        pair = torch.empty((R * R, cfg.c_z), dtype=dt, device=dev)
+        yz = torch.empty((pf.shape[0], cfg.c_z), dtype=F32, device=dev)
+        ops.gemm(pf, self.P("pair_embed.w"), yz)
+        pair = torch.empty((pf.shape[0], cfg.c_z), dtype=dt, device=dev)
         ops.bias_residual(None, yz, self.P("pair_embed.b"), pair)
         rec = None
         if prev is not None:
-            pm, pz = prev[0][:R].contiguous(), prev[1]
-            fb, m1, r1 = ops.layernorm(pm, self.P("recycle_m.g"), self.P("recycle_m.b"), F32)
-            ops.bias_residual(msa[:R], fb, None, msa[:R])
+            pm = m1 = r1 = None
+            if self.s0 == 0:  # the recycled first MSA row lives on the shard holding sequence 0
+                pm = prev[0][:R].contiguous()
+                fb, m1, r1 = ops.layernorm(pm, self.P("recycle_m.g"), self.P("recycle_m.b"), F32)
+                ops.bias_residual(msa[:R], fb, None, msa[:R])
+            pz = prev[1]
             fz, m2, r2 = ops.layernorm(pz, self.P("recycle_z.g"), self.P("recycle_z.b"), F32)
             ops.bias_residual(pair, fz, None, pair)
             rec = (pm, m1, r1, pz, m2, r2)
@@ -540,16 +576,17 @@ class BlockEngine:
 
     def embed_bwd(self, d_msa, d_pair, feats: DeviceFeatures, rec, which: str = "both"):
         """``which`` = 'msa' / 'pair' closes out one branch only (BP ranks)."""
+        mf, pf, _ = self._feat_rows(feats)
         if which in ("both", "msa"):
-            ops.gemm(feats.msa_feat, d_msa, self.G("msa_embed.w"), ta=True)
+            ops.gemm(mf, d_msa, self.G("msa_embed.w"), ta=True)
             ops.colsum_cast(d_msa, self.G("msa_embed.b"))
         if which in ("both", "pair"):
-            ops.gemm(feats.pair_feat, d_pair, self.G("pair_embed.w"), ta=True)
+            ops.gemm(pf, d_pair, self.G("pair_embed.w"), ta=True)
             ops.colsum_cast(d_pair, self.G("pair_embed.b"))
         if rec is not None:
             R = self.cfg.n_res
             pm, m1, r1, pz, m2, r2 = rec
-            if which in ("both", "msa"):
+            if which in ("both", "msa") and pm is not None:
                 scratch = torch.empty_like(d_msa[:R])
                 ops.layernorm_bwd(pm, d_msa[:R], m1, r1, self.P("recycle_m.g"), None, scratch,
                                   self.G("recycle_m.g"), self.G("recycle_m.b"))

@@ -307,25 +307,31 @@ def attn_bwd(qkvg, mask, msb, msl, nb, ctx, gate, dgated, lse, dbg, B, L, H, D, 
 # pair bias
 
 
-def pair_bias_fwd(z, g, b, w, R, H, swap_xy):
-    """nb [H, R, R] (query, key) in z's dtype; swap_xy for triangle-end."""
+def pair_bias_fwd(z, g, b, w, R, H, swap_xy, ni=None, nj=None):
+    """nb [H, R, R] (query, key) in z's dtype; swap_xy for triangle-end.  With
+    (ni, nj) z holds an ni x nj token block (a DAP shard) and nb is
+    [H, ni, nj] (or [H, nj, ni] with swap_xy)."""
     C = z.shape[1]
     dev = z.device
-    nb = torch.empty((H, R, R), dtype=z.dtype, device=dev)
-    mean = torch.empty(R * R, dtype=torch.float32, device=dev)
-    rstd = torch.empty(R * R, dtype=torch.float32, device=dev)
-    call("evo_pair_bias_fwd", ptr(z), dcode(z), ptr(g), ptr(b), ptr(w), ptr(nb), ptr(mean),
-         ptr(rstd), R, C, H, int(swap_xy), stream())
+    ni = R if ni is None else ni
+    nj = R if nj is None else nj
+    nb = torch.empty((H, nj, ni) if swap_xy else (H, ni, nj), dtype=z.dtype, device=dev)
+    mean = torch.empty(ni * nj, dtype=torch.float32, device=dev)
+    rstd = torch.empty(ni * nj, dtype=torch.float32, device=dev)
+    call("evo_pair_bias_fwd_rect", ptr(z), dcode(z), ptr(g), ptr(b), ptr(w), ptr(nb), ptr(mean),
+         ptr(rstd), ni, nj, C, H, int(swap_xy), stream())
     return nb, mean, rstd
 
 
 def pair_bias_bwd(z, mean, rstd, g, b, w, dnb, swap_xy, dz, dg, db, dw, R, H,
-                  accumulate=False):
+                  accumulate=False, ni=None, nj=None):
     C = z.shape[1]
+    ni = R if ni is None else ni
+    nj = R if nj is None else nj
     ws = _ws(_lib.load().evo_pair_bias_bwd_workspace(C, H), z.device)
-    call("evo_pair_bias_bwd", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
+    call("evo_pair_bias_bwd_rect", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
          ptr(dnb), int(swap_xy), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
-         ptr(ws), R, C, H, stream())
+         ptr(ws), ni, nj, C, H, stream())
 
 
 # ---------------------------------------------------------------------------
@@ -350,20 +356,35 @@ def opm_proj_bwd(da, dc, mask_flat, dbl, dbr, k, accumulate=False):
     return d_ab
 
 
-def opm_norm_fwd(num, mask, S, R, k, out_dtype):
+def opm_norm_fwd(num, mask, S, R, k, out_dtype, i0=0, ni=None):
+    """num holds rows i0..i0+ni-1 (all R rows by default; a DAP shard otherwise)."""
     dev = num.device
-    rec = torch.empty(R * R, dtype=torch.float32, device=dev)
-    outn = torch.empty((R * R, k * k), dtype=out_dtype, device=dev)
-    call("evo_opm_norm_fwd", ptr(num), dcode(num), ptr(mask), ptr(rec), ptr(outn), dcode(outn),
-         S, R, k, stream())
+    ni = R if ni is None else ni
+    rec = torch.empty(ni * R, dtype=torch.float32, device=dev)
+    outn = torch.empty((ni * R, k * k), dtype=out_dtype, device=dev)
+    call("evo_opm_norm_fwd_rows", ptr(num), dcode(num), ptr(mask), ptr(rec), ptr(outn), dcode(outn),
+         S, R, k, i0, ni, stream())
     return rec, outn
 
 
-def opm_norm_bwd(doutn, rec, R, k, out_dtype):
-    dnum = torch.empty((R * k, R * k), dtype=out_dtype, device=doutn.device)
-    call("evo_opm_norm_bwd", ptr(doutn), dcode(doutn), ptr(rec), ptr(dnum), dcode(dnum), R, k,
-         stream())
+def opm_norm_bwd(doutn, rec, R, k, out_dtype, ni=None):
+    ni = R if ni is None else ni
+    dnum = torch.empty((ni * k, R * k), dtype=out_dtype, device=doutn.device)
+    call("evo_opm_norm_bwd_rows", ptr(doutn), dcode(doutn), ptr(rec), ptr(dnum), dcode(dnum), R, k,
+         ni, stream())
     return dnum
+
+
+def swap01(src, A, B, out=None):
+    """out[b, a, ...] = src[a, b, ...] for src viewed as [A, B, rest] (contiguous)."""
+    if not src.is_contiguous():
+        raise ValueError("swap01: src must be contiguous")
+    n = src.numel()
+    if n % (A * B):
+        raise ValueError(f"swap01: {n} elements do not split into {A} x {B} rows")
+    out = torch.empty_like(src) if out is None else out
+    call("evo_swap01", ptr(src), ptr(out), A, B, (n // (A * B)) * src.element_size(), stream())
+    return out
 
 
 # ---------------------------------------------------------------------------

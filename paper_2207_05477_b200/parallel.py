@@ -40,7 +40,8 @@ from .errors import ContractError
 
 @dataclass(frozen=True)
 class GridConfig:
-    """src/harness.py:53-76 (DAP is out of scope: dap must be 1)."""
+    """src/harness.py:53-76.  bp and dap do not compose; dp composes with either
+    (ranks: dp outermost, then bp, then dap)."""
 
     dp: int = 1
     bp: int = 1
@@ -53,8 +54,6 @@ class GridConfig:
             raise ContractError("branch parallelism supports size 1 or 2")
         if self.bp > 1 and self.dap > 1:
             raise ContractError("bp and dap axes do not compose")
-        if self.dap != 1:
-            raise ContractError("DAP is not part of this build (BP x DP only)")
 
     @property
     def world(self) -> int:
@@ -133,6 +132,58 @@ class Comm:
         self._rec("allreduce", t, module)
         return t
 
+    # -- DAP primitives (src/harness.py:262-293): dim-0 chunk i <-> group rank i ----
+    # NCCL runs them on device buffers; a gloo group (the CPU tests, and the
+    # several-ranks-on-one-GPU GPU test) gets host copies, and its missing
+    # reduce-scatter is an all-reduce plus this rank's chunk.
+
+    def _host(self, t):
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
+    def allgather(self, t: torch.Tensor, module: str) -> torch.Tensor:
+        """[n, ...] per rank -> [size * n, ...], rank-major."""
+        t = t.contiguous()
+        out = torch.empty((self.size * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        if self._host(t):
+            parts = [torch.empty_like(t, device="cpu") for _ in range(self.size)]
+            dist.all_gather(parts, t.cpu(), group=self.group)
+            out.copy_(torch.cat(parts))
+        else:
+            dist.all_gather_into_tensor(out, t, group=self.group)
+        self._rec("allgather", t, module)
+        return out
+
+    def reducescatter_sum(self, t: torch.Tensor, module: str) -> torch.Tensor:
+        """[size * n, ...] per rank -> [n, ...]: chunk ``rank`` summed over ranks."""
+        t = t.contiguous()
+        n = t.shape[0] // self.size
+        if n * self.size != t.shape[0]:
+            raise ContractError(f"cannot scatter extent {t.shape[0]} over {self.size} workers")
+        if self._host(t) or (not t.is_cuda and dist.get_backend(self.group) == "gloo"):
+            h = t.cpu() if t.is_cuda else t.clone()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            out = h[self.rank * n:(self.rank + 1) * n].to(t.device).contiguous()
+        else:
+            out = torch.empty((n,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            dist.reduce_scatter_tensor(out, t, op=dist.ReduceOp.SUM, group=self.group)
+        self._rec("reducescatter", t, module)
+        return out
+
+    def alltoall(self, t: torch.Tensor, module: str, out: torch.Tensor = None) -> torch.Tensor:
+        """Chunk j of dim 0 goes to rank j; received chunks land rank-major."""
+        t = t.contiguous()
+        if t.shape[0] % self.size:
+            raise ContractError(f"cannot split extent {t.shape[0]} over {self.size} workers")
+        out = torch.empty_like(t) if out is None else out
+        if self._host(t):
+            h = torch.empty_like(t, device="cpu")
+            dist.all_to_all_single(h, t.cpu(), group=self.group)
+            out.copy_(h)
+        else:
+            dist.all_to_all_single(out, t, group=self.group)
+        self._rec("alltoall", t, module)
+        return out
+
 
 def build_groups(grid: GridConfig):
     """All ranks must create every group in the same order (torch.distributed
@@ -150,6 +201,19 @@ def build_groups(grid: GridConfig):
     return bp_comm, world
 
 
+def build_dap_groups(grid: GridConfig):
+    """Returns (dap Comm of this rank, world Comm); every rank creates every group."""
+    me = dist.get_rank()
+    dpi = grid.coords(me)[0]
+    dap_comm = None
+    for d in range(grid.dp):
+        ranks = [grid.rank(d, 0, j) for j in range(grid.dap)]
+        g = dist.new_group(ranks)
+        if d == dpi:
+            dap_comm = Comm("dap", d, ranks, g)
+    return dap_comm, Comm("dp", 0, list(range(grid.world)), None)
+
+
 @dataclass
 class StepResult:
     loss: float
@@ -157,10 +221,17 @@ class StepResult:
 
 
 def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: int,
-            step: int = 0, n_cycles: int = 1):
+            step: int = 0, n_cycles: int = 1, recompute: bool = False):
     """One branch-parallel forward/backward (src/harness.py:392-553) plus the
     fused gradient all-reduce.  Returns the device loss tensor ([1]); the
-    pooled grad region ends up holding the world-averaged gradients."""
+    pooled grad region ends up holding the world-averaged gradients.
+
+    ``recompute`` (the reference restricts recompute_grads to one
+    worker, src/trainer.py:59-60): each rank keeps only its own branch's
+    block inputs -- (msa, pair) on rank 0, pair_mid on rank 1 -- and re-runs
+    its branch forward right before the block's backward.  Both branches'
+    forwards need only local inputs, so recompute adds no collective and the
+    comm trace is unchanged."""
     me = bp.rank
     for c in (bp, world):
         c.step = step
@@ -182,7 +253,7 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
             bp.broadcast(msa_out, 0, "msa_stack")
             pair_out = engine.empty_like(pair)
             bp.broadcast(pair_out, 1, "pair_stack")
-            saved.append((so, sm))
+            saved.append((msa, pair) if recompute else (so, sm))
         else:
             opm = engine.empty_like(pair)
             bp.broadcast(opm, 0, "opm")
@@ -191,7 +262,8 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
             msa_out = engine.empty_like(msa)
             bp.broadcast(msa_out, 0, "msa_stack")
             bp.broadcast(pair_out, 1, "pair_stack")
-            saved.append(sp)
+            saved.append(pair_mid if recompute else sp)
+        del opm
         msa, pair = msa_out, pair_out
     loss, d_msa, d_pair = engine.loss(msa, pair)
 
@@ -199,6 +271,13 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
         c.phase = "bwd"
     deferred = getattr(engine, "deferred", None)
     for i in reversed(range(n_blocks)):
+        if recompute and me == 0:
+            msa_in, pair_in = saved[i]
+            so = engine.opm_fwd(msa_in, f"block{i}.opm", feats, pair_res=None)[1]
+            sm = engine.msa_branch_fwd(i, msa_in, pair_in, feats)[1]
+            saved[i] = (so, sm)
+        elif recompute:
+            saved[i] = engine.pair_branch_fwd(i, saved[i], feats)[1]
         ctx = deferred() if deferred is not None else _NullCtx()
         with ctx:
             _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair)
@@ -257,12 +336,13 @@ def _bp_close(engine, bp, world, grid, me, d_msa, loss):
     return lt
 
 
-def dp_step(engine, feats, world: Comm, grid: GridConfig, n_cycles: int = 1, step: int = 0):
+def dp_step(engine, feats, world: Comm, grid: GridConfig, n_cycles: int = 1, step: int = 0,
+            recompute: bool = False):
     """Pure data parallelism: serial fwd+bwd per replica, one all-reduce of the
     pooled grad region (src/harness.py:607-616)."""
     world.step = step
     world.phase = "grad-sync"
-    loss, _ = engine.forward_backward(feats, n_cycles)
+    loss, _ = engine.forward_backward(feats, n_cycles, recompute=recompute)
     g = engine.grad_region()
     world.allreduce_sum(g, "grad_sync")
     g.mul_(np.float32(1.0 / grid.dp).item())

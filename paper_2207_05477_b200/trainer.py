@@ -40,8 +40,10 @@ class ExecutionPlan:
     fixed_recycles: int = 0  # >0 pins n_recycles (throughput runs use 1)
 
     def validate(self):
-        if self.dp < 1 or self.bp not in (1, 2) or self.dap != 1:
-            raise ContractError("supported grids: dp>=1, bp in {1,2}, dap=1")
+        if self.dp < 1 or self.bp not in (1, 2) or self.dap < 1:
+            raise ContractError("supported grids: dp>=1, bp in {1,2}, dap>=1")
+        if self.bp > 1 and self.dap > 1:
+            raise ContractError("plan.bp: bp and dap axes do not compose")
         if self.act_dtype not in ("f32", "bf16"):
             raise ContractError(f"act_dtype must be f32 or bf16, got {self.act_dtype!r}")
         if self.chunk < 0:
@@ -49,8 +51,6 @@ class ExecutionPlan:
         unknown = set(self.recompute) - {"evoformer"}
         if unknown:
             raise ContractError(f"unknown recompute stacks {sorted(unknown)}")
-        if self.recompute_on and self.dp * self.bp * self.dap > 1:
-            raise ContractError("recompute is supported on single-worker plans")
 
     @property
     def recompute_on(self) -> bool:

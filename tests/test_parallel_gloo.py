@@ -103,13 +103,13 @@ class OracleEngine:
     def embed_bwd(self, d_msa, d_pair, feats, rec, which="both"):
         O.embed_bwd(d_msa.numpy(), d_pair.numpy(), self.f, rec, self.grads)
 
-    def forward_backward(self, feats, n_cycles=1):
+    def forward_backward(self, feats, n_cycles=1, recompute=False):
         loss, grads, _ = O.serial_grads(self.cfg, self.P, self.f, n_cycles)
         self.grads = grads
         return torch.tensor([loss], dtype=torch.float32), None
 
 
-def _worker(rank, world, port, mode, n_blocks, feat_seeds, out_path, n_cycles):
+def _worker(rank, world, port, mode, n_blocks, feat_seeds, out_path, n_cycles, recompute=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -122,9 +122,10 @@ def _worker(rank, world, port, mode, n_blocks, feat_seeds, out_path, n_cycles):
     eng = OracleEngine(cfg, P, feats)
     bp, world_comm = PL.build_groups(grid)
     if mode == "dp":
-        loss = PL.dp_step(eng, feats, world_comm, grid, n_cycles=n_cycles)
+        loss = PL.dp_step(eng, feats, world_comm, grid, n_cycles=n_cycles, recompute=recompute)
     else:
-        loss = PL.bp_step(eng, feats, bp, world_comm, grid, n_blocks, n_cycles=n_cycles)
+        loss = PL.bp_step(eng, feats, bp, world_comm, grid, n_blocks, n_cycles=n_cycles,
+                          recompute=recompute)
     if rank == 0:
         recs = [(r.group_axis, r.primitive, r.module, r.phase) for r in (bp.records if bp else [])]
         np.savez(out_path, loss=loss.numpy(), grads=eng.flat.numpy(),
@@ -141,10 +142,11 @@ def _free_port():
     return port
 
 
-def _run(world, mode, n_blocks=2, feat_seeds=(3, 3), n_cycles=1):
+def _run(world, mode, n_blocks=2, feat_seeds=(3, 3), n_cycles=1, recompute=False):
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "r.npz")
-        mp.spawn(_worker, args=(world, _free_port(), mode, n_blocks, list(feat_seeds), out, n_cycles),
+        mp.spawn(_worker, args=(world, _free_port(), mode, n_blocks, list(feat_seeds), out, n_cycles,
+                                recompute),
                  nprocs=world, join=True)
         r = np.load(out, allow_pickle=True)
         return float(r["loss"][0]), r["grads"], list(map(tuple, r["recs"]))
@@ -192,6 +194,16 @@ def test_bp_with_recycling_matches_serial():
     assert np.abs(grads - sg).max() <= 1e-5
 
 
+def test_bp_recompute_bitwise_and_same_trace():
+    """BP with per-branch recompute: each rank re-runs its own
+    branch's forward from stored inputs; gradients are bitwise those of the
+    stored-activation BP step and no collective is added."""
+    l0, g0, r0 = _run(2, "bp", n_blocks=2)
+    l1, g1, r1 = _run(2, "bp", n_blocks=2, recompute=True)
+    assert l0 == l1 and np.array_equal(g0, g1)
+    assert r0 == r1
+
+
 def test_grid_config_rules():
     from paper_2207_05477_b200.parallel import GridConfig
     from paper_2207_05477_b200.errors import ContractError
@@ -201,17 +213,54 @@ def test_grid_config_rules():
     for bad in (dict(bp=3), dict(bp=2, dap=2), dict(dp=0)):
         with pytest.raises(ContractError):
             GridConfig(**bad)
+    g = GridConfig(dp=2, dap=2)
+    assert [g.coords(r) for r in range(4)] == [(0, 0, 0), (0, 0, 1), (1, 0, 0), (1, 0, 1)]
 
 
 def test_recompute_plan_rules():
-    """src/trainer.py:44-68: only the 'evoformer' stack recomputes, on
-    single-worker plans only."""
+    """src/trainer.py:44-68: only the 'evoformer' stack recomputes."""
     from paper_2207_05477_b200.errors import ContractError
     from paper_2207_05477_b200.trainer import ExecutionPlan
     ExecutionPlan(recompute=("evoformer",)).validate()
     assert ExecutionPlan(recompute=("evoformer",)).recompute_on
     assert not ExecutionPlan().recompute_on
-    for bad in (dict(recompute=("msa",)), dict(recompute=("evoformer",), dp=2),
-                dict(recompute=("evoformer",), bp=2)):
-        with pytest.raises(ContractError):
-            ExecutionPlan(**bad).validate()
+    with pytest.raises(ContractError):
+        ExecutionPlan(recompute=("msa",)).validate()
+    # extension over the reference (src/trainer.py:59-60): BP/DP plans recompute too
+    ExecutionPlan(recompute=("evoformer",), dp=2, bp=2).validate()
+
+
+def _dap_comm_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2207_05477_b200 import parallel as PL
+    grid = PL.GridConfig(dap=world)
+    dap, _ = PL.build_dap_groups(grid)
+    rng = np.random.default_rng(rank)
+    x = torch.from_numpy(rng.standard_normal((world * 3, 5)).astype(np.float32))
+    ag = dap.allgather(x[:3], "msa_row_attn")
+    rs = dap.reducescatter_sum(x, "opm")
+    a2a = dap.alltoall(x, "tri_end")
+    np.savez(out_path + f".{rank}", x=x.numpy(), ag=ag.numpy(), rs=rs.numpy(), a2a=a2a.numpy(),
+             prims=np.array([r.primitive for r in dap.records]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dap_comm_primitives_match_reference_semantics(world):
+    """Comm.allgather / reducescatter_sum / alltoall on dim-0 chunks have the
+    semantics of the reference's DapPar collectives (src/harness.py:262-293):
+    concat of every rank's chunk, this rank's chunk of the sum, and chunk j to
+    rank j landing rank-major."""
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "c")
+        mp.spawn(_dap_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+        r = [dict(np.load(out + f".{k}.npz")) for k in range(world)]
+    xs = [q["x"] for q in r]
+    for k in range(world):
+        assert np.array_equal(r[k]["ag"], np.concatenate([x[:3] for x in xs]))
+        np.testing.assert_allclose(r[k]["rs"], sum(x[3 * k:3 * k + 3] for x in xs), rtol=1e-6)
+        assert np.array_equal(r[k]["a2a"], np.concatenate([x[3 * k:3 * k + 3] for x in xs]))
+        assert list(r[k]["prims"]) == ["allgather", "reducescatter", "alltoall"]
