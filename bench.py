@@ -284,7 +284,8 @@ def run_ours(args):
     hosts = []
     for s in range(min(4, max(1, args.steps))):
         h = PinnedFeatures(cfg)
-        rep = rank // 2 if (world > 1 and world % 2 == 0) else rank  # both BP ranks: one sample
+        inner = args.dap if args.dap > 1 else 2
+        rep = rank // inner if (world > 1 and world % inner == 0) else rank  # a BP pair / DAP group: one sample
         h.fill(make_features(cfg, step_feature_seed(plan.seed + 7919 * rep, s)))
         hosts.append(h)
     trainer.host = hosts[0]
@@ -292,7 +293,13 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     grid = None
-    if world > 1:
+    if world > 1 and args.dap > 1:
+        from paper_2207_05477_b200.dap import DapEngine, dap_step
+        from paper_2207_05477_b200.parallel import GridConfig, build_dap_groups
+        grid = GridConfig(dp=world // args.dap, dap=args.dap)
+        dap_comm, world_comm = build_dap_groups(grid)
+        trainer.engine = DapEngine(cfg, trainer.store, plan.torch_dtype, dap_comm)
+    elif world > 1:
         from paper_2207_05477_b200.parallel import GridConfig, bp_step, build_groups, dp_step
         grid = GridConfig.for_world(world)
         bp_comm, world_comm = build_groups(grid)
@@ -300,6 +307,8 @@ def run_ours(args):
     def eager_step():
         if grid is None:
             loss, _ = trainer.engine.forward_backward(trainer.feats, 1)
+        elif grid.dap > 1:
+            loss, _ = dap_step(trainer.engine, trainer.feats, world_comm, grid)
         elif grid.bp == 2:
             loss = bp_step(trainer.engine, trainer.feats, bp_comm, world_comm, grid, cfg.n_blocks)
         else:
@@ -363,7 +372,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = float(t[0]), float(t[1])
 
-    samples = args.steps * (grid.dp if grid is not None else 1)  # a BP pair shares one sample
+    samples = args.steps * (grid.dp if grid is not None else 1)  # a BP pair / DAP group shares one sample
     value = samples / dev_s
     e2e_value = samples / e2e_s
     peaks = load_peaks()
@@ -428,7 +437,8 @@ def run_ours(args):
                 "data": "synthetic (reference PRNG features, random-init weights)",
                 "config": {"workload": "48-block Evoformer training step (fwd+bwd+fused Adam), "
                                        "initial shape, 1 recycle", **shape,
-                           "parallelism": (f"dp{grid.dp}xbp{grid.bp}" if grid is not None else "single"),
+                           "parallelism": ((f"dp{grid.dp}xdap{grid.dap}" if grid.dap > 1 else
+                                            f"dp{grid.dp}xbp{grid.bp}") if grid is not None else "single"),
                            "l2": "working set (~tens of GB of activations) >> 126 MB L2",
                            "cuda_graph": use_graph},
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
@@ -453,6 +463,9 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override n_blocks (debug only)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dap", type=int, default=1,
+                    help="N>1: Dynamic Axial Parallelism groups of this size (dp = N / dap) "
+                         "instead of the default BP x DP grid")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -10,7 +10,9 @@ feature buffers keep fixed device addresses and are refreshed in place.
 
 from __future__ import annotations
 
+import json
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -143,15 +145,75 @@ class Trainer:
         return g
 
     def train_step(self, step: int):
-        """src/trainer.py:192-247 (serial): returns (loss, metrics)."""
+        """src/trainer.py:192-247 (serial): returns (loss, metrics).  Metric keys
+        follow the reference: ``launches`` are this step's optimizer-phase
+        launches (src/fusion.py:65-77), ``op_count`` this step's launches of the
+        library's own kernels, ``ledger_peak_bytes`` the device-memory peak of
+        the step above what was live before it (the reference's ledger peak)."""
+        from . import _lib
         n_rec = self.n_recycles(step)
         self.stage_features(step)
+        launches_before = dict(self.store.launches.counts)
+        ops_before = _lib.launch_count()
+        dev = torch.device(self.store.device)
+        live_before = torch.cuda.memory_allocated(dev)
+        torch.cuda.reset_peak_memory_stats(dev)
         loss_t = self.device_step(n_rec)
         loss = float(loss_t.item())
         if not math.isfinite(loss):
             raise TrainingAborted(step, f"non-finite loss {loss!r}")
         grad_norm = float(np.sqrt(self.store.sumsq.item()))
+        launches = {k: self.store.launches.counts[k] - launches_before.get(k, 0)
+                    for k in self.store.launches.PHASES}
         metrics = {"step": step, "loss": loss, "grad_norm": grad_norm, "n_recycles": n_rec,
-                   "launches": dict(self.store.launches.counts)}
+                   "launches": launches, "comm_records": 0,
+                   "ledger_peak_bytes": int(torch.cuda.max_memory_allocated(dev) - live_before),
+                   "op_count": int(_lib.launch_count() - ops_before),
+                   "blocks_executed": self.cfg.n_blocks * n_rec}
         self.history.append(metrics)
         return loss, metrics
+
+    def train_loop(self, steps: int, metrics_path=None):
+        """src/trainer.py:250-262: ``steps`` steps, one compact JSON line of
+        metrics per step into ``metrics_path`` (metrics.jsonl)."""
+        fh = open(metrics_path, "w") if metrics_path else None
+        losses = []
+        try:
+            for s in range(steps):
+                loss, metrics = self.train_step(s)
+                losses.append(loss)
+                if fh:
+                    fh.write(json.dumps(metrics, separators=(",", ":")) + "\n")
+        finally:
+            if fh:
+                fh.close()
+        return losses
+
+    def bench_protocol(self, total: int = 105, discard: int = 5, _spike=None):
+        """src/trainer.py:269-303: run ``total`` steps, drop the first
+        ``discard`` and average the counters and step times of the rest
+        (bench.json).  ``_spike`` = (step, key, amount) perturbs one step's
+        counters so tests can show discarded steps do not leak in."""
+        if total <= discard:
+            raise ContractError("total must exceed the discarded prefix")
+        per_step, times = [], []
+        t0 = time.perf_counter()
+        for s in range(total):
+            s0 = time.perf_counter()
+            _, metrics = self.train_step(s)
+            times.append(time.perf_counter() - s0)
+            metrics = dict(metrics)
+            metrics["launch_total"] = sum(metrics["launches"].values())
+            if _spike is not None and s == _spike[0]:
+                metrics[_spike[1]] = metrics.get(_spike[1], 0) + _spike[2]
+            per_step.append(metrics)
+        wall = time.perf_counter() - t0
+        kept, kept_t = per_step[discard:], times[discard:]
+        counters = {k: float(np.mean([m[k] for m in kept])) for k in COUNTER_KEYS + ("launch_total",)}
+        return {"total_steps": total, "discarded": discard, "averaged_steps": len(kept),
+                "counters": counters, "mean_step_seconds": float(np.mean(kept_t)),
+                "steps_per_second": float(1.0 / np.mean(kept_t)), "wall_seconds": wall,
+                "seed": self.plan.seed}
+
+
+COUNTER_KEYS = ("loss", "grad_norm", "n_recycles", "comm_records", "ledger_peak_bytes", "op_count")

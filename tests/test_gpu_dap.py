@@ -22,13 +22,6 @@ from conftest import rel_err
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-# planner.DAP_BLOCK_COUNTS_MINI, per worker and block (fwd + bwd)
-MINI = {("msa_stack", "alltoall"): 4, ("msa_stack", "allgather"): 1, ("msa_stack", "reducescatter"): 1,
-        ("pair_stack", "alltoall"): 4, ("pair_stack", "allgather"): 2, ("pair_stack", "reducescatter"): 2,
-        ("opm", "allgather"): 1, ("opm", "reducescatter"): 1}
-STACK = {"msa_row_attn": "msa_stack", "msa_col_attn": "msa_stack", "tri_start": "pair_stack",
-         "tri_end": "pair_stack", "opm": "opm"}
-
 CFGS = {
     "mini": dict(n_blocks=2, n_seq=16, n_res=32, c_m=64, c_z=32, heads=2, opm_dim=8),
     "k32": dict(n_blocks=1, n_seq=32, n_res=64, c_m=64, c_z=32, heads=2, opm_dim=32),
@@ -132,12 +125,13 @@ def test_dap_matches_unsharded(world, cfg, dtype, ncyc):
 @pytest.mark.timeout(600)
 def test_dap_trace_matches_planner_mini_table():
     kw = CFGS["mini"]
+    from paper_2207_05477_b200 import planner
     res = _run_dap(2, kw, "f32")
-    measured = Counter()
-    for module, prim, _ in map(tuple, res["recs"]):
-        if module in STACK:
-            measured[(STACK[module], prim)] += 1
-    assert measured == Counter({k: v * kw["n_blocks"] for k, v in MINI.items()})
+    measured = planner.trace_counts([tuple(r) for r in res["recs"]])
+    assert measured == planner.expected_trace("dap", kw["n_blocks"], "mini")
+    # everything after the loss is backward traffic: half of each block's all-to-alls
+    phases = Counter(ph for m, pr, ph in map(tuple, res["recs"]) if pr == "alltoall")
+    assert phases["fwd"] == phases["bwd"] == 4 * kw["n_blocks"]
 
 
 @pytest.mark.timeout(600)

@@ -198,3 +198,30 @@ def test_recompute_grads_bitwise_equal_direct(dtype, streams, nb, s, r):
     diff = [n for n in g0 if not torch.equal(g0[n], g1[n])]
     assert not diff, diff[:5]
     assert any(bool(g.abs().max() > 0) for g in g0.values())
+
+
+def test_train_loop_metrics_jsonl_and_bench_protocol(tmp_path):
+    """src/trainer.py:192-303: per-step metrics (fused optimizer = 1/2/1/1
+    launches per phase, src/planner.py launches_per_step), metrics.jsonl, and
+    the bench protocol's discarded prefix not leaking into the averages."""
+    import json
+    from paper_2207_05477_b200.model import ModelConfig
+    from paper_2207_05477_b200.trainer import COUNTER_KEYS, ExecutionPlan, Trainer
+    cfg = ModelConfig(n_blocks=2, n_seq=16, n_res=32, c_m=64, c_z=32, heads=2, opm_dim=8)
+    tr = Trainer.create(cfg, ExecutionPlan(act_dtype="f32", seed=32))
+    path = tmp_path / "metrics.jsonl"
+    losses = tr.train_loop(3, str(path))
+    lines = [json.loads(x) for x in path.read_text().splitlines()]
+    assert [m["step"] for m in lines] == [0, 1, 2]
+    assert [m["loss"] for m in lines] == losses and all(np.isfinite(losses))
+    for m in lines:
+        assert m["launches"] == {"grad_sync": 1, "grad_clip": 2, "opt_update": 1, "ema": 1}
+        assert set(COUNTER_KEYS) <= set(m)
+        assert m["op_count"] > 0 and m["ledger_peak_bytes"] > 0
+        assert m["blocks_executed"] == cfg.n_blocks * m["n_recycles"]
+    tr2 = Trainer.create(cfg, ExecutionPlan(act_dtype="f32", seed=32))
+    rep = tr2.bench_protocol(total=4, discard=1, _spike=(0, "loss", 1e6))
+    assert rep["averaged_steps"] == 3
+    kept = tr2.history[1:]
+    assert abs(rep["counters"]["loss"] - np.mean([m["loss"] for m in kept])) <= 1e-6 * abs(rep["counters"]["loss"])
+    assert rep["counters"]["launch_total"] == 5.0

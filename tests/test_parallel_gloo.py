@@ -171,7 +171,9 @@ def test_bp_matches_serial(world):
 
 def test_bp_trace_three_broadcasts_one_allreduce_per_block():
     """tests/test_acceptance.py:156-166 of the reference."""
+    from paper_2207_05477_b200 import planner
     _, _, recs = _run(2, "bp", n_blocks=1)
+    assert planner.trace_counts([(r[2], r[1]) for r in recs]) == planner.expected_trace("bp", 1)
     block = [r for r in recs if r[2] in ("opm", "msa_stack", "pair_stack")]
     assert len(block) == 4
     assert sum(1 for r in block if r[1] == "broadcast") == 3
