@@ -28,7 +28,7 @@ inline bool pow2_width(int64_t C) { return C >= 32 && C <= 1024 && (C & (C - 1))
 // capped at PARTIAL_PER_SM blocks per SM (bounded partial rows).
 constexpr int PARTIAL_PER_SM = 2;
 constexpr int EW_UNROLL = 4;          // 16-B vectors per thread in flight in the elementwise kernels
-constexpr int PB_PARTIAL_PER_SM = 2;  // pair-bias backward: 128 registers, 2 blocks per SM
+constexpr int PB_PARTIAL_PER_SM = 3;  // pair-bias backward: partial rows for up to 3 blocks per SM
 inline unsigned glue_grid(int64_t rows, int rows_per_iter, int per_sm = 16) {
   int64_t want = (rows + rows_per_iter - 1) / rows_per_iter;
   int64_t cap = (int64_t)num_sms() * per_sm;
@@ -775,6 +775,11 @@ bool ln_fwd_vec(const void* x, int xdt, const float* g, const float* b, void* y,
   return true;
 }
 
+bool ln_bwd_stream(const void* x, int xdt, const void* dy, int dydt, const float* mean, const float* rstd,
+                   const float* g, const float* dres, float* dx, __nv_bfloat16* dx16, float* dgamma,
+                   float* dbeta, float* dxsum, int accumulate, void* ws, int64_t rows, int64_t C,
+                   int64_t ws_blocks, cudaStream_t s);
+
 int64_t ln_bwd_vec_ws(int64_t C) { return (int64_t)num_sms() * PARTIAL_PER_SM * 3 * C * 4; }
 
 bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* mean, const float* rstd,
@@ -785,6 +790,9 @@ bool ln_bwd_vec(const void* x, int xdt, const void* dy, int dydt, const float* m
       (dx16 && !al16(dx16)))
     return false;
   ws = partial_buffer(ws, ln_bwd_vec_ws(C));
+  if (ln_bwd_stream(x, xdt, dy, dydt, mean, rstd, g, dres, dx, dx16, dgamma, dbeta, dxsum, accumulate, ws,
+                    rows, C, (int64_t)num_sms() * PARTIAL_PER_SM, s))
+    return true;
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     using M = RowMap<CC>;
@@ -879,6 +887,11 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
   return true;
 }
 
+bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float* rstd, const float* g,
+                          const float* bln, const float* w, const float* dnb, int swap, float* dz, float* dg,
+                          float* db, float* dw, int accumulate, void* ws, int64_t NI, int64_t NJ, int64_t C,
+                          int64_t H, int64_t ws_blocks, cudaStream_t s);
+
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) {
   return (int64_t)num_sms() * PB_PARTIAL_PER_SM * (C * H + 2 * C) * 4;
 }
@@ -889,6 +902,9 @@ bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rs
                        int64_t NJ, int64_t C, int64_t H, cudaStream_t s) {
   if (!pow2_width(C) || C > 256 || H > 8 || !al16(z) || !al16(dz)) return false;
   ws = partial_buffer(ws, pair_bias_bwd_vec_ws(C, H));
+  if (pair_bias_bwd_stream(z, dt, mean, rstd, g, bln, w, dnb, swap, dz, dg, db, dw, accumulate, ws, NI, NJ, C, H,
+                           (int64_t)num_sms() * PB_PARTIAL_PER_SM, s))
+    return true;
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {

@@ -386,3 +386,69 @@ def test_attention_long_rows_vs_fp32(name, S, R, H, D, geom):
     if d16 is not None:
         assert torch.isfinite(d16).all()
         assert rel(d16, d32) <= 3e-2
+
+
+@pytest.mark.parametrize("C", [128, 256])
+@pytest.mark.parametrize("rows,dy_dt,with_res", [(8192, "f32", True), (8196, "f32", False),
+                                                 (65536, "bf16", True), (4100, "f32", True)])
+def test_layernorm_bwd_stream_vs_torch(C, rows, dy_dt, with_res):
+    """The bulk-copy-staged LayerNorm backward (csrc/glue_stream.cu; taken for
+    bf16 x, rows % 4 == 0, rows >= 4096) against fp32 torch, including a
+    partial last stage (8196 rows) and the fused bf16 copy / column sums."""
+    from paper_2207_05477_b200 import _lib, ops
+    torch.manual_seed(rows + C)
+    x = (torch.randn(rows, C, device="cuda") * 2 + 0.5).bfloat16()
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    y, mu, rs = ops.layernorm(x, g, b, torch.bfloat16)
+    dy = torch.randn(rows, C, device="cuda").to(torch.float32 if dy_dt == "f32" else torch.bfloat16)
+    dres = torch.randn(rows, C, device="cuda") if with_res else None
+    dx = dres.clone() if with_res else torch.empty(rows, C, device="cuda")
+    dg, db = torch.empty(C, device="cuda"), torch.empty(C, device="cuda")
+    ops.layernorm_bwd(x, dy, mu, rs, g, dx if with_res else None, dx, dg, db)
+    xr = x.float().requires_grad_(True)
+    gr, br_ = g.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    torch.nn.functional.layer_norm(xr, (C,), gr, br_, 1e-5).backward(dy.float())
+    got = dx - dres if with_res else dx
+    assert rel(got, xr.grad) <= 1e-4
+    assert rel(dg, gr.grad) <= 1e-4 and rel(db, br_.grad) <= 1e-4
+    # fused outputs: bf16 copy of dx and its column sums
+    dx2 = dres.clone() if with_res else torch.zeros(rows, C, device="cuda")
+    dx16 = torch.empty(rows, C, device="cuda", dtype=torch.bfloat16)
+    dxs, dg2, db2 = (torch.empty(C, device="cuda") for _ in range(3))
+    ws = torch.empty(_lib.load().evo_layernorm_bwd_workspace(rows, C), dtype=torch.uint8, device="cuda")
+    ops.call("evo_layernorm_bwd_ex", ops.ptr(x), ops.dcode(x), ops.ptr(dy), ops.dcode(dy), ops.ptr(mu),
+             ops.ptr(rs), ops.ptr(g), ops.ptr(dx2), ops.ptr(dx2), ops.ptr(dx16), ops.ptr(dxs), ops.ptr(dg2),
+             ops.ptr(db2), 0, ops.ptr(ws), rows, C, ops.stream())
+    assert torch.equal(dx16, dx2.to(torch.bfloat16))
+    assert rel(dxs, dx2.double().sum(0).float()) <= 1e-5
+    assert rel(dx2 - (dres if with_res else 0), xr.grad) <= 1e-4
+
+
+@pytest.mark.parametrize("NI,NJ,swap", [(256, 256, 0), (256, 256, 1), (128, 256, 0), (256, 128, 1),
+                                        (100, 82, 0)])
+def test_pair_bias_bwd_stream_vs_torch(NI, NJ, swap):
+    """The bulk-copy-staged pair-bias backward (csrc/glue_stream.cu; bf16,
+    C = 128, >= 4096 tokens) against fp32 torch, square and rectangular (DAP
+    shard) extents, both bias layouts, and a partial last stage (100 x 82)."""
+    from paper_2207_05477_b200 import ops
+    C, H = 128, 8
+    torch.manual_seed(NI + NJ + swap)
+    z = torch.randn(NI * NJ, C, device="cuda").bfloat16()
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda") * 0.1
+    w = torch.randn(C, H, device="cuda") * 0.2
+    nb, mu, rs = ops.pair_bias_fwd(z, g, b, w, 0, H, swap, ni=NI, nj=NJ)
+    zr = z.float().requires_grad_(True)
+    gr, br_, wr = (t.clone().requires_grad_(True) for t in (g, b, w))
+    P = torch.nn.functional.layer_norm(zr, (C,), gr, br_, 1e-5) @ wr
+    ref = P.view(NI, NJ, H).permute(2, 0, 1)
+    if swap:
+        ref = ref.transpose(1, 2)
+    assert rel(nb.float(), ref) <= 1e-2
+    dnb = torch.randn(ref.shape, device="cuda").contiguous()
+    dz0 = torch.randn(NI * NJ, C, device="cuda")
+    dz = dz0.clone()
+    dg, db, dw = torch.empty(C, device="cuda"), torch.empty(C, device="cuda"), torch.empty(C, H, device="cuda")
+    ops.pair_bias_bwd(z, mu, rs, g, b, w, dnb, swap, dz, dg, db, dw, 0, H, ni=NI, nj=NJ)
+    ref.backward(dnb)
+    assert rel(dz - dz0, zr.grad) <= 1e-4
+    assert rel(dg, gr.grad) <= 1e-4 and rel(db, br_.grad) <= 1e-4 and rel(dw, wr.grad) <= 1e-4
