@@ -764,9 +764,13 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
 // ============================================================================
 // entry points used by the C ABI wrappers (return false -> scalar fallback)
 
+bool ln_fwd_stream(const void* x, int xdt, const float* g, const float* b, void* y, int ydt, float* mean,
+                   float* rstd, int64_t rows, int64_t C, float eps, cudaStream_t s);
+
 bool ln_fwd_vec(const void* x, int xdt, const float* g, const float* b, void* y, int ydt,
                 float* mean, float* rstd, int64_t rows, int64_t C, float eps, cudaStream_t s) {
   if (!pow2_width(C) || !al16(x) || !al16(y)) return false;
+  if (ln_fwd_stream(x, xdt, g, b, y, ydt, mean, rstd, rows, C, eps, s)) return true;
   POW2_C_DISPATCH(C, CC, EVO_DISPATCH_T(xdt, TX, {
     ln_fwd_dispatch_y<CC, TX>(x, g, b, y, ydt, mean, rstd, rows, eps, s);
   }));

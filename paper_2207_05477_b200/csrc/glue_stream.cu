@@ -351,6 +351,107 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kerne
   }
 }
 
+
+// LayerNorm forward (src/tensor.py:173-188): y = (x - mean) * rstd * g + b in the
+// output dtype, plus the row statistics.  Warp-per-row (C = 256) or two rows per
+// warp (C = 128), TPW row steps per warp and stage; x arrives by bulk copy.
+template <int C, typename TY, int NST>
+struct LnfStream {
+  static constexpr int LANES = C / 8 < 32 ? C / 8 : 32;
+  static constexpr int RPW = 32 / LANES;
+  static constexpr int TPW = 4;
+  static constexpr int RS = (ST / 32) * RPW * TPW;
+  static constexpr int STAGE = (RS * C * 2 + 127) / 128 * 128;
+  static constexpr int BYTES = NST * STAGE + 2 * NST * 8;
+};
+
+template <int C, typename TY, int NST>
+__global__ void __launch_bounds__(ST + 32) ln_fwd_stream_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                const float* __restrict__ g,
+                                                                const float* __restrict__ b, TY* __restrict__ y,
+                                                                float* __restrict__ mean, float* __restrict__ rstd,
+                                                                int64_t rows, float eps) {
+  using M = LnfStream<C, TY, NST>;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NST * M::STAGE);
+  uint64_t* emp = bar + NST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int l = lane % M::LANES, gi = lane / M::LANES;
+  const int64_t nstage = (rows + M::RS - 1) / M::RS;
+  const int64_t s0 = nstage * blockIdx.x / gridDim.x, s1 = nstage * (blockIdx.x + 1) / gridDim.x;
+  const int n = (int)(s1 - s0);
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_init(&bar[s], 1);
+      tc::mbar_init(&emp[s], ST / 32);
+    }
+  }
+  __syncthreads();
+  if (warp == ST / 32) {
+    if (lane == 0) {
+      for (int it = 0; it < n; ++it) {
+        const int s = it % NST;
+        if (it >= NST) tc::mbar_wait(&emp[s], (uint32_t)(((it / NST) - 1) & 1));
+        const int64_t r0 = (s0 + it) * M::RS;
+        const int nr = (int)(rows - r0 < M::RS ? rows - r0 : M::RS);
+        mbar_expect_tx(&bar[s], nr * C * 2);
+        bulk_g2s(sm + s * M::STAGE, x + r0 * C, nr * C * 2, &bar[s]);
+      }
+    }
+    return;
+  }
+  float gg[8], bb[8];
+  ld8(g + l * 8, gg);
+  ld8(b + l * 8, bb);
+  for (int it = 0; it < n; ++it) {
+    const int s = it % NST;
+    const int64_t r0 = (s0 + it) * M::RS;
+    const int nr = (int)(rows - r0 < M::RS ? rows - r0 : M::RS);
+    tc::mbar_wait(&bar[s], (uint32_t)((it / NST) & 1));
+    const __nv_bfloat16* st = reinterpret_cast<const __nv_bfloat16*>(sm + s * M::STAGE);
+    float v[M::TPW][8];
+#pragma unroll
+    for (int u = 0; u < M::TPW; ++u) {
+      const int rr = (warp * M::TPW + u) * M::RPW + gi;
+      ld8(st + (rr < nr ? rr : 0) * C + l * 8, v[u]);
+    }
+    tc::mbar_arrive_warp(&emp[s]);  // the stage is in registers
+    float mu[M::TPW], inv[M::TPW];
+#pragma unroll
+    for (int u = 0; u < M::TPW; ++u) {
+      float sum = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sum += v[u][e];
+      mu[u] = group_sum<M::LANES>(sum) / (float)C;
+    }
+#pragma unroll
+    for (int u = 0; u < M::TPW; ++u) {
+      float q = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = v[u][e] - mu[u];
+        q += d * d;
+      }
+      inv[u] = rsqrtf(group_sum<M::LANES>(q) / (float)C + eps);
+    }
+#pragma unroll
+    for (int u = 0; u < M::TPW; ++u) {
+      const int rr = (warp * M::TPW + u) * M::RPW + gi;
+      if (rr < nr) {
+        const int64_t r = r0 + rr;
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = (v[u][e] - mu[u]) * inv[u] * gg[e] + bb[e];
+        st8(y + r * C + l * 8, o);
+        if (l == 0) {
+          if (mean) mean[r] = mu[u];
+          if (rstd) rstd[r] = inv[u];
+        }
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // Returns false (caller falls back) for shapes this path does not cover.
@@ -432,6 +533,46 @@ bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float*
   finalize_partials((const float*)ws, grid, C * H, dw, accumulate, s, W);
   finalize_partials((const float*)ws + C * H, grid, C, dg, accumulate, s, W);
   finalize_partials((const float*)ws + C * H + C, grid, C, db, accumulate, s, W);
+  return true;
+}
+
+}  // namespace evo
+
+namespace evo {
+
+bool ln_fwd_stream(const void* x, int xdt, const float* g, const float* b, void* y, int ydt, float* mean,
+                   float* rstd, int64_t rows, int64_t C, float eps, cudaStream_t s) {
+  static const bool off = [] {
+    const char* e = getenv("EVO_GLUE_STREAM");
+    return e && e[0] == '0';
+  }();
+  if (off || (C != 128 && C != 256) || xdt != EVO_BF16 || rows < 4096) return false;
+  if (((uintptr_t)x | (uintptr_t)y) & 15) return false;
+  constexpr int NST = 4;
+  const unsigned grid = (unsigned)(2 * num_sms());
+  bool done = false;
+  auto go = [&](auto cc, auto ty) {
+    constexpr int CC = decltype(cc)::value;
+    using TY = typename decltype(ty)::type;
+    using M = LnfStream<CC, TY, NST>;
+    auto k = ln_fwd_stream_kernel<CC, TY, NST>;
+    static bool attr = false;
+    if (!attr) {
+      EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, M::BYTES));
+      attr = true;
+    }
+    k<<<grid, ST + 32, M::BYTES, s>>>((const __nv_bfloat16*)x, g, b, (TY*)y, mean, rstd, rows, eps);
+    done = true;
+  };
+  struct F32 { using type = float; };
+  struct B16 { using type = __nv_bfloat16; };
+  if (C == 256 && ydt == EVO_BF16) go(std::integral_constant<int, 256>{}, B16{});
+  else if (C == 128 && ydt == EVO_BF16) go(std::integral_constant<int, 128>{}, B16{});
+  else if (C == 256 && ydt == EVO_F32) go(std::integral_constant<int, 256>{}, F32{});
+  else if (C == 128 && ydt == EVO_F32) go(std::integral_constant<int, 128>{}, F32{});
+  if (!done) return false;
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
   return true;
 }
 

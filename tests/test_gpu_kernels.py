@@ -452,3 +452,21 @@ def test_pair_bias_bwd_stream_vs_torch(NI, NJ, swap):
     ref.backward(dnb)
     assert rel(dz - dz0, zr.grad) <= 1e-4
     assert rel(dg, gr.grad) <= 1e-4 and rel(db, br_.grad) <= 1e-4 and rel(dw, wr.grad) <= 1e-4
+
+
+@pytest.mark.parametrize("C", [128, 256])
+@pytest.mark.parametrize("rows,ydt", [(8192, "bf16"), (8200, "bf16"), (65536, "f32")])
+def test_layernorm_fwd_stream_vs_torch(C, rows, ydt):
+    """Bulk-copy-staged LayerNorm forward (bf16 x, >= 4096 rows) against fp32
+    torch, including a partial last stage."""
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(rows + C)
+    x = (torch.randn(rows, C, device="cuda") * 2 + 0.5).bfloat16()
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    dt = torch.bfloat16 if ydt == "bf16" else torch.float32
+    y, mu, rs = ops.layernorm(x, g, b, dt)
+    ref = torch.nn.functional.layer_norm(x.float(), (C,), g, b, 1e-5)
+    assert rel(y.float(), ref) <= (1e-2 if ydt == "bf16" else 1e-5)
+    xf = x.float()
+    assert rel(mu, xf.mean(1)) <= 1e-5
+    assert rel(rs, torch.rsqrt(xf.var(1, unbiased=False) + 1e-5)) <= 1e-4
