@@ -151,6 +151,10 @@ int evo_cast(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, void* 
  * memory; one launch per 64 groups. */
 int evo_pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N,
                   int n, int src_dtype, int dst_dtype, int unpack, void* stream);
+/* The same with ns (2 or 4) matrices per group: dst[i] = [C, ns*N] (the OPM's
+ * merged [w_left | w_right] projection, src/model.py:360-361). */
+int evo_pack_cols_ns(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N,
+                     int n, int ns, int src_dtype, int dst_dtype, int unpack, void* stream);
 /* in-place y *= s (fp32) */
 int evo_scale_inplace(float* y, float s, int64_t n, void* stream);
 

@@ -51,6 +51,8 @@ SIGNATURES = {
     "evo_cast": (_i, [_p, _i, _p, _i, _i64, _p]),
     "evo_pack_cols": (_i, [ctypes.POINTER(_p), ctypes.POINTER(_p), ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64), _i, _i, _i, _i, _p]),
+    "evo_pack_cols_ns": (_i, [ctypes.POINTER(_p), ctypes.POINTER(_p), ctypes.POINTER(_i64),
+                           ctypes.POINTER(_i64), _i, _i, _i, _i, _i, _p]),
     "evo_scale_inplace": (_i, [_p, _f, _i64, _p]),
     "evo_attn_fwd": (_i, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p,
                           _i64, _i64, _i64, _i64, _i64, _i64, _i, _p]),

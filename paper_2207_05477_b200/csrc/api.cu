@@ -87,7 +87,7 @@ bool bias_residual_vec(const void* res, int rdt, const void* y, int ydt, const f
                        int odt, int64_t rows, int64_t C, cudaStream_t s);
 bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, cudaStream_t s);
 void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N, int n,
-               int sdt, int ddt, int unpack, cudaStream_t s);
+               int sdt, int ddt, int unpack, cudaStream_t s, int ns);
 
 // tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
 bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
@@ -231,7 +231,17 @@ int evo_pack_cols(const void* const* src, void* const* dst, const int64_t* C, co
   EVO_API_BEGIN
   EVO_REQUIRE(n >= 0 && src && dst && C && N, EVO_ERR_ARG, "pack_cols: bad arguments");
   if (n == 0) return EVO_OK;
-  pack_cols(src, dst, C, N, n, src_dtype, dst_dtype, unpack, (cudaStream_t)stream);
+  pack_cols(src, dst, C, N, n, src_dtype, dst_dtype, unpack, (cudaStream_t)stream, 4);
+  EVO_API_END
+}
+
+int evo_pack_cols_ns(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N,
+                     int n, int ns, int src_dtype, int dst_dtype, int unpack, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(n >= 0 && src && dst && C && N && (ns == 2 || ns == 4), EVO_ERR_ARG,
+              "pack_cols: bad arguments (ns must be 2 or 4)");
+  if (n == 0) return EVO_OK;
+  pack_cols(src, dst, C, N, n, src_dtype, dst_dtype, unpack, (cudaStream_t)stream, ns);
   EVO_API_END
 }
 

@@ -671,6 +671,7 @@ struct PackDesc {
   const void* src[4];
   void* dst[4];
   int64_t C, N;
+  int ns;  // matrices per group (2 or 4)
 };
 struct PackBatch {
   int n, dtype_src, dtype_dst, unpack;
@@ -680,9 +681,9 @@ struct PackBatch {
 template <typename TS, typename TD>
 __global__ void __launch_bounds__(GT) pack_cols_kernel(const __grid_constant__ PackBatch pb) {
   const PackDesc& d = pb.d[blockIdx.y];
-  const int64_t n = d.C * 4 * d.N;
+  const int64_t n = d.C * d.ns * d.N;
   for (int64_t e = blockIdx.x * (int64_t)GT + threadIdx.x; e < n; e += (int64_t)gridDim.x * GT) {
-    const int64_t c = e / (4 * d.N), r = e % (4 * d.N);
+    const int64_t c = e / (d.ns * d.N), r = e % (d.ns * d.N);
     const int s = (int)(r / d.N);
     const int64_t j = r % d.N;
     if (!pb.unpack)
@@ -736,7 +737,7 @@ inline bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 }  // namespace
 
 void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N, int n,
-               int sdt, int ddt, int unpack, cudaStream_t s) {
+               int sdt, int ddt, int unpack, cudaStream_t s, int ns) {
   for (int i0 = 0; i0 < n; i0 += PACK_MAX) {
     PackBatch pb{};
     pb.n = n - i0 < PACK_MAX ? n - i0 : PACK_MAX;
@@ -746,13 +747,14 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
     int64_t maxe = 0;
     for (int k = 0; k < pb.n; ++k) {
       const int i = i0 + k;
-      for (int q = 0; q < 4; ++q) {
-        pb.d[k].src[q] = unpack ? src[i] : src[4 * i + q];
-        pb.d[k].dst[q] = unpack ? dst[4 * i + q] : dst[i];
+      for (int q = 0; q < ns; ++q) {
+        pb.d[k].src[q] = unpack ? src[i] : src[ns * i + q];
+        pb.d[k].dst[q] = unpack ? dst[ns * i + q] : dst[i];
       }
       pb.d[k].C = C[i];
       pb.d[k].N = N[i];
-      maxe = std::max<int64_t>(maxe, C[i] * 4 * N[i]);
+      pb.d[k].ns = ns;
+      maxe = std::max<int64_t>(maxe, C[i] * ns * N[i]);
     }
     dim3 grid((unsigned)std::min<int64_t>((maxe + GT - 1) / GT, 1024), (unsigned)pb.n);
     EVO_DISPATCH_T(sdt, TS, EVO_DISPATCH_T(ddt, TD, { pack_cols_kernel<TS, TD><<<grid, GT, 0, s>>>(pb); }));

@@ -133,13 +133,25 @@ class BlockEngine:
                     Cs.append(cfg.c_z)
                     Ns.append(ch)
         wdt = ops.dcode(store.weight(f"block0.row_attn.attn.wq")) if cfg.n_blocks else 0
-        self._pack = ops.PackPlan(srcs, dsts, Cs, Ns, False, wdt, ops.dcode(torch.empty(0, dtype=act_dtype)))
+        adt = ops.dcode(torch.empty(0, dtype=act_dtype))
+        self._pack = ops.PackPlan(srcs, dsts, Cs, Ns, False, wdt, adt)
+        # merged [w_left | w_right] OPM projection [c_m, 2k]: one GEMM each way
+        srcs, dsts = [], []
+        for i in range(cfg.n_blocks):
+            p = f"block{i}.opm"
+            self.wcat[p] = torch.empty((cfg.c_m, 2 * cfg.opm_dim), dtype=act_dtype, device=store.device)
+            srcs += [store.weight(f"{p}.w_left"), store.weight(f"{p}.w_right")]
+            dsts.append(self.wcat[p])
+        self._pack_opm = ops.PackPlan(srcs, dsts, [cfg.c_m] * cfg.n_blocks, [cfg.opm_dim] * cfg.n_blocks,
+                                      False, wdt, adt, ns=2)
         self.refresh_weights()
 
     def refresh_weights(self):
         """Re-pack the merged projection weights after an optimizer step."""
         if self._pack.n:
             self._pack.run()
+        if self._pack_opm.n:
+            self._pack_opm.run()
 
     def deferred(self):
         """Batch the ~40 small parameter-gradient reductions of a block backward
@@ -317,8 +329,7 @@ class BlockEngine:
         s_loc, r_loc = SR // R, self.r_loc
         xl, mu, rs = ops.layernorm(msa_in, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
         ab = torch.empty((SR, 2 * k), dtype=dt, device=msa_in.device)
-        ops.gemm(xl, self.W(f"{prefix}.w_left", Cm), ab[:, :k])
-        ops.gemm(xl, self.W(f"{prefix}.w_right", Cm), ab[:, k:])
+        ops.gemm(xl, self.wcat[prefix], ab)                           # [a | c] projections in one GEMM
         a, c = ops.opm_proj(ab, self.P(f"{prefix}.b_left"), self.P(f"{prefix}.b_right"),
                             self._feat_rows(feats)[2], k)
         del ab
@@ -362,11 +373,12 @@ class BlockEngine:
         d_ab = ops.opm_proj_bwd(da, dc, self._feat_rows(feats)[2], self.G(f"{prefix}.b_left"),
                                 self.G(f"{prefix}.b_right"), k)
         xl = sv["xl"]
-        ops.gemm(xl, d_ab[:, :k], self.Gm(f"{prefix}.w_left", Cm), ta=True)
-        ops.gemm(xl, d_ab[:, k:], self.Gm(f"{prefix}.w_right", Cm), ta=True)
+        dwlr = torch.empty((Cm, 2 * k), dtype=F32, device=dev)
+        ops.gemm(xl, d_ab, dwlr, ta=True)                             # d[w_left | w_right] in one GEMM
+        ops.PackPlan([dwlr], [self.Gm(f"{prefix}.w_left", Cm), self.Gm(f"{prefix}.w_right", Cm)],
+                     [Cm], [k], True, ops.F32, ops.F32, ns=2).run()
         dxl = torch.empty((SR, Cm), dtype=F32, device=dev)
-        ops.gemm(d_ab[:, :k], self.W(f"{prefix}.w_left", Cm), dxl, tb=True)
-        ops.gemm(d_ab[:, k:], self.W(f"{prefix}.w_right", Cm), dxl, tb=True, beta=1.0)
+        ops.gemm(d_ab, self.wcat[prefix], dxl, tb=True)
         return dxl
 
     def opm_ln_bwd(self, dxl, sv, prefix, d_msa):

@@ -249,7 +249,7 @@ class PackPlan:
     """Host-side pointer tables for evo_pack_cols (built once: the pooled
     parameter storage and the packed buffers never move)."""
 
-    def __init__(self, srcs, dsts, Cs, Ns, unpack, sdt, ddt):
+    def __init__(self, srcs, dsts, Cs, Ns, unpack, sdt, ddt, ns=4):
         import ctypes
         P = ctypes.c_void_p
         self.src = (P * len(srcs))(*[t.data_ptr() for t in srcs])
@@ -257,11 +257,11 @@ class PackPlan:
         self.C = (ctypes.c_int64 * len(Cs))(*Cs)
         self.N = (ctypes.c_int64 * len(Ns))(*Ns)
         self.n = len(Cs)
-        self.unpack, self.sdt, self.ddt = int(unpack), sdt, ddt
+        self.unpack, self.sdt, self.ddt, self.ns = int(unpack), sdt, ddt, int(ns)
         self.keep = (srcs, dsts)
 
     def run(self):
-        call("evo_pack_cols", self.src, self.dst, self.C, self.N, self.n, self.sdt, self.ddt,
+        call("evo_pack_cols_ns", self.src, self.dst, self.C, self.N, self.n, self.ns, self.sdt, self.ddt,
              self.unpack, stream())
 
 
