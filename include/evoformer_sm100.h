@@ -236,6 +236,11 @@ int evo_opm_norm_fwd_rows(const void* num, int num_dtype, const float* mask, flo
                           int64_t i0, int64_t NI, void* stream);
 int evo_opm_norm_bwd_rows(const void* doutn, int in_dtype, const float* rec, void* dnum,
                           int out_dtype, int64_t R, int64_t k, int64_t NI, void* stream);
+/* rec rows i0..i0+NI-1 alone (they depend only on the mask: computed once per
+ * forward pass and shared by every block), and the normalisation with a given rec. */
+int evo_opm_rec(const float* mask, float* rec, int64_t S, int64_t R, int64_t i0, int64_t NI, void* stream);
+int evo_opm_norm_apply_rows(const void* num, int num_dtype, const float* rec, void* outn, int out_dtype,
+                            int64_t R, int64_t k, int64_t NI, void* stream);
 
 /* ---- DAP re-layout (src/harness.py:262-293) ------------------------------
  * dst[b, a, :] = src[a, b, :] for src [A, B, elem_bytes]: the outer-axis swap

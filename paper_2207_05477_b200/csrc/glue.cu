@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(GT) pack_cols_kernel(const __grid_constant__ P
 
 // rec[i, j] = 1 / (sum_s m[s, i0 + i] m[s, j] + 1e-3)   (block per local row i; exact
 // integer sums).  i0 > 0: the rows of one DAP shard (src/model.py:351-378 sharded)
-__global__ void __launch_bounds__(GT) opm_rec_vec_kernel(const float* __restrict__ mask,
+__global__ void __launch_bounds__(GT) opm_rec_vec_kernel_(const float* __restrict__ mask,
                                                          float* __restrict__ rec, int64_t S, int64_t R,
                                                          int64_t i0) {
   extern __shared__ float mi[];  // [S]
@@ -937,15 +937,23 @@ bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rs
   return true;
 }
 
+void opm_rec_rows(const float* mask, float* rec, int64_t S, int64_t R, int64_t i0, int64_t NI, cudaStream_t s) {
+  if (NI * R == 0) return;
+  opm_rec_vec_kernel_<<<(unsigned)NI, GT, S * sizeof(float), s>>>(mask, rec, S, R, i0);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+}
+
 bool opm_norm_vec(bool fwd, const void* src, int sdt, const float* mask, float* rec, void* dst, int ddt,
                   int64_t S, int64_t R, int64_t k, int64_t i0, int64_t NI, cudaStream_t s) {
   if (k != OPM_K || (R % OPM_JT) != 0 || !al16(src) || !al16(dst)) return false;
-  if (fwd) {
-    opm_rec_vec_kernel<<<(unsigned)NI, GT, S * sizeof(float), s>>>(mask, rec, S, R, i0);
+  if (fwd && mask) {  // mask == nullptr: rec is given
+    opm_rec_vec_kernel_<<<(unsigned)NI, GT, S * sizeof(float), s>>>(mask, rec, S, R, i0);
     EVO_LAUNCH_CHECK();
     count_launch(1);
   }
   dim3 grid((unsigned)(R / OPM_JT), (unsigned)NI);
+  if (NI == 0) return true;
   EVO_DISPATCH_T(sdt, TI, EVO_DISPATCH_T(ddt, TO, {
     if (fwd)
       opm_relayout_kernel<TI, TO, true><<<grid, GT, 0, s>>>((const TI*)src, rec, (TO*)dst, R);

@@ -159,6 +159,7 @@ __global__ void sq_loss_final_kernel(const float* __restrict__ pm, const float* 
 
 bool opm_norm_vec(bool fwd, const void* src, int sdt, const float* mask, float* rec, void* dst, int ddt,
                   int64_t S, int64_t R, int64_t k, int64_t i0, int64_t NI, cudaStream_t s);
+void opm_rec_rows(const float* mask, float* rec, int64_t S, int64_t R, int64_t i0, int64_t NI, cudaStream_t s);
 
 }  // namespace evo
 
@@ -222,6 +223,31 @@ int evo_opm_norm_fwd_rows(const void* num, int num_dtype, const float* mask, flo
   }));
   EVO_LAUNCH_CHECK();
   count_launch(2);
+  EVO_API_END
+}
+
+int evo_opm_rec(const float* mask, float* rec, int64_t S, int64_t R, int64_t i0, int64_t NI, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(i0 >= 0 && NI >= 0 && i0 + NI <= R && S * 4 <= 48 * 1024, EVO_ERR_ARG,
+              "opm_rec: row range outside [0, R) or S too large");
+  opm_rec_rows(mask, rec, S, R, i0, NI, (cudaStream_t)stream);
+  EVO_API_END
+}
+
+int evo_opm_norm_apply_rows(const void* num, int num_dtype, const float* rec, void* outn, int out_dtype,
+                            int64_t R, int64_t k, int64_t NI, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(NI >= 0 && NI <= R, EVO_ERR_ARG, "opm_norm: row count outside [0, R]");
+  if (NI * R == 0) return EVO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (opm_norm_vec(true, num, num_dtype, nullptr, const_cast<float*>(rec), outn, out_dtype, 0, R, k, 0, NI, s))
+    return EVO_OK;
+  int bs = (int)(k * k < 256 ? ((k * k + 31) / 32) * 32 : 256);
+  EVO_DISPATCH_T(num_dtype, TI, EVO_DISPATCH_T(out_dtype, TO, {
+    opm_norm_fwd_kernel<TI, TO><<<(unsigned)(NI * R), bs, 0, s>>>((const TI*)num, rec, (TO*)outn, R, (int)k);
+  }));
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
   EVO_API_END
 }
 

@@ -97,6 +97,7 @@ class BlockEngine:
         # this worker's shard: sequences s0.., residue rows r0..r0+r_loc (whole model here)
         self.s0, self.r0, self.r_loc = 0, 0, cfg.n_res
         self.opm_num_dtype = act_dtype
+        self._rec = None
         # MSA branch on a second stream (EVO_BRANCH_STREAMS=0 disables)
         import os
         self.branch_streams = (torch.device(store.device).type == "cuda"
@@ -176,6 +177,14 @@ class BlockEngine:
 
     def mask(self, feats: DeviceFeatures, which: str):
         return feats.msa_mask if which == "msa" else feats.pair_mask
+
+    def _rec_for(self, feats: DeviceFeatures):
+        """The OPM normaliser rec = 1/(mask^T mask + 1e-3) of this worker's rows:
+        a function of the MSA mask only, so it is computed once per forward pass
+        (``embed_fwd`` drops the previous one) and shared by every block."""
+        if self._rec is None:
+            self._rec = ops.opm_rec(feats.msa_mask, self.cfg.n_seq, self.cfg.n_res, self.r0, self.r_loc)
+        return self._rec
 
     # -- sharding hooks: identities here, collectives in the DAP engine (dap.py) ----
 
@@ -336,7 +345,8 @@ class BlockEngine:
         num = torch.empty((R * k, R * k), dtype=self.opm_num_dtype, device=msa_in.device)
         ops.gemm(a.view(s_loc, R * k), c.view(s_loc, R * k), num, ta=True)
         num = self._opm_reduce(num)            # the shard's rows of the sum over all sequences
-        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt, i0=self.r0, ni=r_loc)
+        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt, i0=self.r0, ni=r_loc,
+                                     rec=self._rec_for(feats))
         del num
         if out is None:
             out = torch.empty((r_loc * R, cfg.c_z), dtype=dt, device=msa_in.device)
@@ -565,6 +575,7 @@ class BlockEngine:
         R = cfg.n_res
         mf, pf, _ = self._feat_rows(feats)
         dev = mf.device
+        self._rec = None  # the step's mask may have changed: recompute the OPM normaliser
         ym = torch.empty((mf.shape[0], cfg.c_m), dtype=F32, device=dev)
         ops.gemm(mf, self.P("msa_embed.w"), ym)
         msa = torch.empty((mf.shape[0], cfg.c_m), dtype=dt, device=dev)

@@ -356,10 +356,24 @@ def opm_proj_bwd(da, dc, mask_flat, dbl, dbr, k, accumulate=False):
     return d_ab
 
 
-def opm_norm_fwd(num, mask, S, R, k, out_dtype, i0=0, ni=None):
-    """num holds rows i0..i0+ni-1 (all R rows by default; a DAP shard otherwise)."""
+def opm_rec(mask, S, R, i0=0, ni=None):
+    """rec rows i0..i0+ni-1 = 1 / (mask^T mask + 1e-3): a function of the mask only."""
+    ni = R if ni is None else ni
+    rec = torch.empty(ni * R, dtype=torch.float32, device=mask.device)
+    call("evo_opm_rec", ptr(mask), ptr(rec), S, R, i0, ni, stream())
+    return rec
+
+
+def opm_norm_fwd(num, mask, S, R, k, out_dtype, i0=0, ni=None, rec=None):
+    """num holds rows i0..i0+ni-1 (all R rows by default; a DAP shard otherwise).
+    With ``rec`` (from opm_rec) only the normalisation runs."""
     dev = num.device
     ni = R if ni is None else ni
+    if rec is not None:
+        outn = torch.empty((ni * R, k * k), dtype=out_dtype, device=dev)
+        call("evo_opm_norm_apply_rows", ptr(num), dcode(num), ptr(rec), ptr(outn), dcode(outn), R, k, ni,
+             stream())
+        return rec, outn
     rec = torch.empty(ni * R, dtype=torch.float32, device=dev)
     outn = torch.empty((ni * R, k * k), dtype=out_dtype, device=dev)
     call("evo_opm_norm_fwd_rows", ptr(num), dcode(num), ptr(mask), ptr(rec), ptr(outn), dcode(outn),
