@@ -262,18 +262,23 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kerne
   }
   // this lane's 4 channels: LN affine, w_bias rows, accumulators
   const int c0 = lane * 4;
-  float gg[4], bb[4], wr[4][M::HM], dw[4][M::HM], dgs[4], dbs[4];
+  // this lane's 4 channels as two pairs on the paired fp32 pipes (FFMA2):
+  // w2[j][hh] = w[c0+2j .. c0+2j+1, hh], dw2[e][q] = dw[c0+e, 2q .. 2q+1]
+  float2 gg2[2], bb2[2], dgs2[2], dbs2[2], w2[2][M::HM], dw2[4][M::HM / 2];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    gg[e] = g[c0 + e];
-    bb[e] = bln[c0 + e];
-    dgs[e] = dbs[e] = 0.f;
+  for (int j = 0; j < 2; ++j) {
+    gg2[j] = make_float2(g[c0 + 2 * j], g[c0 + 2 * j + 1]);
+    bb2[j] = make_float2(bln[c0 + 2 * j], bln[c0 + 2 * j + 1]);
+    dgs2[j] = dbs2[j] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int hh = 0; hh < M::HM; ++hh) {
-      wr[e][hh] = hh < H ? w[(c0 + e) * H + hh] : 0.f;
-      dw[e][hh] = 0.f;
-    }
+    for (int hh = 0; hh < M::HM; ++hh)
+      w2[j][hh] = hh < H ? make_float2(w[(c0 + 2 * j) * H + hh], w[(c0 + 2 * j + 1) * H + hh])
+                         : make_float2(0.f, 0.f);
   }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+#pragma unroll
+    for (int q = 0; q < M::HM / 2; ++q) dw2[e][q] = make_float2(0.f, 0.f);
   for (int it = 0; it < n; ++it) {
     const int s = it % NST;
     const int64_t t0 = (s0 + it) * M::RS;
@@ -294,7 +299,7 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kerne
 #pragma unroll
     for (int u = 0; u < M::TPW; ++u) {
       const int tt = warp * M::TPW + u;
-      if (tt >= nt) break;  // warp-uniform
+      if (tt < nt) {  // warp-uniform
       float dpm = dpg[u];
       if (!swap_xy && lane < H)
         dpm = reinterpret_cast<const float*>(st + M::ZB + M::DZB + 2 * M::SB + lane * M::SB)[tt];
@@ -305,29 +310,41 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kerne
       const float inv = reinterpret_cast<const float*>(st + M::ZB + M::DZB + M::SB)[tt];
       const uint2 zr = *reinterpret_cast<const uint2*>(st + (tt * C + c0) * 2);
       const float4 dzr = *reinterpret_cast<const float4*>(st + M::ZB + (tt * C + c0) * 4);
-      const float zv[4] = {__uint_as_float(zr.x << 16), __uint_as_float(zr.x & 0xFFFF0000u),
-                           __uint_as_float(zr.y << 16), __uint_as_float(zr.y & 0xFFFF0000u)};
-      float xh[4], dxh[4], s1 = 0.f, s2 = 0.f;
+      const float2 mu2 = make_float2(-mu * inv, -mu * inv), inv2 = make_float2(inv, inv);
+      // xh = (z - mu) * inv = z * inv - mu * inv ; zl = xh * g + b
+      const float2 xh2[2] = {__ffma2_rn(tc::bf16x2_f2(zr.x), inv2, mu2), __ffma2_rn(tc::bf16x2_f2(zr.y), inv2, mu2)};
+      float2 dzl2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        xh[e] = (zv[e] - mu) * inv;
-        const float zl = xh[e] * gg[e] + bb[e];
-        float dzl = 0.f;
-#pragma unroll
-        for (int hh = 0; hh < M::HM; ++hh) {
-          dzl = fmaf(dP[hh], wr[e][hh], dzl);
-          dw[e][hh] = fmaf(zl, dP[hh], dw[e][hh]);
-        }
-        dgs[e] += dzl * xh[e];
-        dbs[e] += dzl;
-        dxh[e] = dzl * gg[e];
-        s1 += dxh[e];
-        s2 += dxh[e] * xh[e];
+      for (int hh = 0; hh < M::HM; ++hh) {
+        const float2 p2 = make_float2(dP[hh], dP[hh]);
+        dzl2[0] = __ffma2_rn(p2, w2[0][hh], dzl2[0]);
+        dzl2[1] = __ffma2_rn(p2, w2[1][hh], dzl2[1]);
       }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float2 zl2 = __ffma2_rn(xh2[j], gg2[j], bb2[j]);
+        const float zl[2] = {zl2.x, zl2.y};
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const float2 z2 = make_float2(zl[e2], zl[e2]);
+#pragma unroll
+          for (int q = 0; q < M::HM / 2; ++q)
+            dw2[2 * j + e2][q] = __ffma2_rn(z2, make_float2(dP[2 * q], dP[2 * q + 1]), dw2[2 * j + e2][q]);
+        }
+        dgs2[j] = __ffma2_rn(dzl2[j], xh2[j], dgs2[j]);
+        dbs2[j] = __fadd2_rn(dbs2[j], dzl2[j]);
+      }
+      const float2 dxh2[2] = {__fmul2_rn(dzl2[0], gg2[0]), __fmul2_rn(dzl2[1], gg2[1])};
+      const float s1 = (dxh2[0].x + dxh2[0].y) + (dxh2[1].x + dxh2[1].y);
+      const float2 t2 = __ffma2_rn(dxh2[0], xh2[0], __fmul2_rn(dxh2[1], xh2[1]));
+      const float s2 = t2.x + t2.y;
       const float m1 = group_sum<32>(s1) / (float)C, m2 = group_sum<32>(s2) / (float)C;
-      const float4 o = make_float4(dzr.x + inv * (dxh[0] - m1 - xh[0] * m2), dzr.y + inv * (dxh[1] - m1 - xh[1] * m2),
-                                   dzr.z + inv * (dxh[2] - m1 - xh[2] * m2), dzr.w + inv * (dxh[3] - m1 - xh[3] * m2));
-      *reinterpret_cast<float4*>(dz + (t0 + tt) * C + c0) = o;
+      // dz += inv * (dxh - m1 - xh * m2)
+      const float2 nm1 = make_float2(-m1, -m1), nm2 = make_float2(-m2, -m2);
+      const float2 o0 = __ffma2_rn(inv2, __ffma2_rn(xh2[0], nm2, __fadd2_rn(dxh2[0], nm1)), make_float2(dzr.x, dzr.y));
+      const float2 o1 = __ffma2_rn(inv2, __ffma2_rn(xh2[1], nm2, __fadd2_rn(dxh2[1], nm1)), make_float2(dzr.z, dzr.w));
+      *reinterpret_cast<float4*>(dz + (t0 + tt) * C + c0) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      }
     }
     tc::mbar_arrive_warp(&emp[s]);
   }
@@ -338,9 +355,9 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kerne
   for (int e = 0; e < 4; ++e) {
 #pragma unroll
     for (int hh = 0; hh < M::HM; ++hh)
-      if (hh < H) mine[(c0 + e) * H + hh] = dw[e][hh];
-    mine[C * H + c0 + e] = dgs[e];
-    mine[C * H + C + c0 + e] = dbs[e];
+      if (hh < H) mine[(c0 + e) * H + hh] = (hh & 1) ? dw2[e][hh / 2].y : dw2[e][hh / 2].x;
+    mine[C * H + c0 + e] = (e & 1) ? dgs2[e / 2].y : dgs2[e / 2].x;
+    mine[C * H + C + c0 + e] = (e & 1) ? dbs2[e / 2].y : dbs2[e / 2].x;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(PB_CW * 32) : "memory");
   const int Wd = C * H + 2 * C;
