@@ -242,6 +242,14 @@ int evo_opm_rec(const float* mask, float* rec, int64_t S, int64_t R, int64_t i0,
 int evo_opm_norm_apply_rows(const void* num, int num_dtype, const float* rec, void* outn, int out_dtype,
                             int64_t R, int64_t k, int64_t NI, void* stream);
 
+/* OPM backward d(pair) -> d(num) as one tcgen05 GEMM with the normalisation
+ * and the [i*k+p, j*k+q] re-layout in its epilogue:
+ *   dnum[i*k+p, j*k+q] = rec[i*R+j] * sum_c d_act[i*R+j, c] * w_out[p*k+q, c]
+ * d_act [NI*R, C], w_out [k*k, C] bf16; dnum [NI*k, R*k] bf16.  Needs C = 128,
+ * k = 32, R % 128 == 0 (EVO_ERR_UNSUPPORTED otherwise). */
+int evo_opm_dnum(const void* d_act, const void* w_out, const float* rec, void* dnum, int64_t R, int64_t k,
+                 int64_t NI, int64_t C, int dtype, void* stream);
+
 /* ---- DAP re-layout (src/harness.py:262-293) ------------------------------
  * dst[b, a, :] = src[a, b, :] for src [A, B, elem_bytes]: the outer-axis swap
  * that brackets every DAP all-to-all / all-gather / reduce-scatter. */

@@ -367,11 +367,13 @@ class BlockEngine:
             d_act = torch.empty((RR, Cz), dtype=dt, device=dev)
             ops.colsum_cast(d, self.G(f"{prefix}.b_out"), y=d_act)
         ops.gemm(sv["outn"], d_act, self.Gm(f"{prefix}.w_out", k * k), ta=True)
-        doutn = torch.empty((RR, k * k), dtype=dt, device=dev)
-        ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
+        dnum = ops.opm_dnum(d_act, self.W(f"{prefix}.w_out", k * k), sv["rec"], R, k, ni=self.r_loc)
+        if dnum is None:  # shapes the fused tcgen05 kernel does not cover
+            doutn = torch.empty((RR, k * k), dtype=dt, device=dev)
+            ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
+            dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt, ni=self.r_loc)
+            del doutn
         del d_act
-        dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt, ni=self.r_loc)
-        del doutn
         dnum = self._opm_gather(dnum)
         s_loc = SR // R
         a2, c2 = sv["a"].view(s_loc, R * k), sv["c"].view(s_loc, R * k)

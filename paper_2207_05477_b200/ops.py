@@ -381,6 +381,20 @@ def opm_norm_fwd(num, mask, S, R, k, out_dtype, i0=0, ni=None, rec=None):
     return rec, outn
 
 
+def opm_dnum(d_act, w_out, rec, R, k, ni=None):
+    """d(num) straight from d(pair): the w_out data-gradient GEMM with the OPM
+    normalisation and re-layout in its tcgen05 epilogue.  None when the shape
+    is not covered (the caller runs GEMM + opm_norm_bwd)."""
+    ni = R if ni is None else ni
+    C = d_act.shape[1]
+    if (d_act.dtype != torch.bfloat16 or w_out.dtype != torch.bfloat16 or C != 128 or k != 32
+            or R % 128 or not d_act.is_contiguous() or not w_out.is_contiguous()):
+        return None
+    dnum = torch.empty((ni * k, R * k), dtype=torch.bfloat16, device=d_act.device)
+    call("evo_opm_dnum", ptr(d_act), ptr(w_out), ptr(rec), ptr(dnum), R, k, ni, C, dcode(d_act), stream())
+    return dnum
+
+
 def opm_norm_bwd(doutn, rec, R, k, out_dtype, ni=None):
     ni = R if ni is None else ni
     dnum = torch.empty((ni * k, R * k), dtype=out_dtype, device=doutn.device)

@@ -470,3 +470,21 @@ def test_layernorm_fwd_stream_vs_torch(C, rows, ydt):
     xf = x.float()
     assert rel(mu, xf.mean(1)) <= 1e-5
     assert rel(rs, torch.rsqrt(xf.var(1, unbiased=False) + 1e-5)) <= 1e-4
+
+
+@pytest.mark.parametrize("R,ni", [(256, 256), (256, 128), (384, 384)])
+def test_opm_dnum_tc_vs_torch(R, ni):
+    """OPM backward d(pair) -> d(num) as one tcgen05 GEMM with the normalisation
+    and [i*k+p, j*k+q] re-layout in the epilogue (csrc/opm_tc.cu), against
+    fp32 torch; ni < R is a DAP row shard."""
+    from paper_2207_05477_b200 import ops
+    k, C = 32, 128
+    torch.manual_seed(R + ni)
+    d_act = (torch.randn(ni * R, C, device="cuda") * 0.5).bfloat16()
+    w_out = (torch.randn(k * k, C, device="cuda") * 0.1).bfloat16()
+    rec = torch.rand(ni * R, device="cuda") + 0.01
+    dnum = ops.opm_dnum(d_act, w_out, rec, R, k, ni=ni)
+    assert dnum is not None and dnum.shape == (ni * k, R * k)
+    doutn = (d_act.float() @ w_out.float().t()) * rec[:, None]          # [(i, j), (p, q)]
+    ref = doutn.view(ni, R, k, k).permute(0, 2, 1, 3).reshape(ni * k, R * k)
+    assert rel(dnum.float(), ref) <= 1e-2
