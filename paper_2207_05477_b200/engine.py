@@ -103,6 +103,7 @@ class BlockEngine:
         self.branch_streams = (torch.device(store.device).type == "cuda"
                                and os.environ.get("EVO_BRANCH_STREAMS", "1") != "0")
         self._s2 = None
+        self.opm_dnum_fused = os.environ.get("EVO_OPM_DNUM_TC", "0") == "1"
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
         # two arenas for the block-pipelined backward (blocks_bwd), alternating by block
@@ -367,8 +368,10 @@ class BlockEngine:
             d_act = torch.empty((RR, Cz), dtype=dt, device=dev)
             ops.colsum_cast(d, self.G(f"{prefix}.b_out"), y=d_act)
         ops.gemm(sv["outn"], d_act, self.Gm(f"{prefix}.w_out", k * k), ta=True)
-        dnum = ops.opm_dnum(d_act, self.W(f"{prefix}.w_out", k * k), sv["rec"], R, k, ni=self.r_loc)
-        if dnum is None:  # shapes the fused tcgen05 kernel does not cover
+        dnum = None
+        if self.opm_dnum_fused:  # one tcgen05 GEMM with the re-layout in its epilogue (opt-in)
+            dnum = ops.opm_dnum(d_act, self.W(f"{prefix}.w_out", k * k), sv["rec"], R, k, ni=self.r_loc)
+        if dnum is None:
             doutn = torch.empty((RR, k * k), dtype=dt, device=dev)
             ops.gemm(d_act, self.W(f"{prefix}.w_out", k * k), doutn, tb=True)
             dnum = ops.opm_norm_bwd(doutn, sv["rec"], R, k, dt, ni=self.r_loc)
