@@ -26,71 +26,116 @@ constexpr int OT_K = 128;             // c_z (the contraction)
 constexpr int OT_M = 128, OT_N = 256;  // tile
 constexpr int OT_DC = OT_K / 8;        // 16-byte k chunks per row
 constexpr int OT_A = OT_M * OT_K * 2, OT_B = OT_N * OT_K * 2;
-constexpr int OT_SMEM = OT_A + OT_B + 64;
 
-__global__ void __launch_bounds__(256) opm_dnum_tc_kernel(const bf16* __restrict__ dact,
-                                                          const bf16* __restrict__ wout,
-                                                          const float* __restrict__ rec,
-                                                          bf16* __restrict__ dnum, int64_t R, int k) {
+// Persistent form: CTA (n, g) keeps the w_out rows of N-tile n resident and
+// walks M-tiles g, g + G, ...; A tiles are double-buffered (cp.async two tiles
+// ahead) and the accumulator is double-buffered in TMEM, so the MMAs of tile
+// t+1 and the loads of t+2 run under the (store-bound) epilogue of tile t.
+constexpr int OT_T = 512;  // 16 warps: 4 TMEM lane quarters x 4 column quarters in the epilogue
+constexpr int OT_X = (OT_T / 32) * 32 * 64;  // per-warp 2 KB transpose buffers of the epilogue
+constexpr int OT_SMEM_P = OT_B + 2 * OT_A + OT_X + 64;
+
+__global__ void __launch_bounds__(OT_T, 1) opm_dnum_tc_kernel(const bf16* __restrict__ dact,
+                                                             const bf16* __restrict__ wout,
+                                                             const float* __restrict__ rec,
+                                                             bf16* __restrict__ dnum, int64_t R, int k,
+                                                             int64_t n_mt, int G) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OT_A + OT_B);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + OT_B;  // two buffers of OT_A
+  uint8_t* sX = smem + OT_B + 2 * OT_A;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OT_B + 2 * OT_A + OT_X);  // [2]
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * OT_M;  // d_act rows (i, j0 ..)
-  const int n0 = blockIdx.y * OT_N;               // dnum columns (p, q) ..
-  // stage A = d_act[m0 .. m0+127, 0 .. 127] and B = w_out[n0 .. n0+255, 0 .. 127]
-  for (int e = tid; e < OT_M * OT_DC; e += 256) {
+  const int n0 = blockIdx.y * OT_N;
+  const int g = blockIdx.x;
+  const int nt = (int)((n_mt - g + G - 1) / G);  // M-tiles of this CTA
+  auto load_a = [&](int t, int buf) {
+    const int64_t m0 = (int64_t)(g + (int64_t)t * G) * OT_M;
+    uint8_t* d = sA + buf * OT_A;
+    for (int e = tid; e < OT_M * OT_DC; e += OT_T) {
+      const int r = e / OT_DC, c = e % OT_DC;
+      tc::cp_async16(d + ((r >> 3) * OT_DC + c) * 128 + (r & 7) * 16, dact + (m0 + r) * OT_K + c * 8);
+    }
+  };
+  for (int e = tid; e < OT_N * OT_DC; e += OT_T) {
     const int r = e / OT_DC, c = e % OT_DC;
-    tc::cp_async16(smem + ((r >> 3) * OT_DC + c) * 128 + (r & 7) * 16, dact + (m0 + r) * OT_K + c * 8);
+    tc::cp_async16(sB + ((r >> 3) * OT_DC + c) * 128 + (r & 7) * 16, wout + (int64_t)(n0 + r) * OT_K + c * 8);
   }
-  for (int e = tid; e < OT_N * OT_DC; e += 256) {
-    const int r = e / OT_DC, c = e % OT_DC;
-    tc::cp_async16(smem + OT_A + ((r >> 3) * OT_DC + c) * 128 + (r & 7) * 16, wout + (int64_t)(n0 + r) * OT_K + c * 8);
-  }
+  if (nt > 0) load_a(0, 0);
+  if (nt > 1) load_a(1, 1);
   tc::cp_async_commit();
-  if (warp == 0) tc::tmem_alloc<256>(slot);
-  if (tid == 0) tc::mbar_init(bar, 1);
+  if (warp == 0) tc::tmem_alloc<512>(slot);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+  }
   tc::cp_async_wait0();
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tbase = *slot;
-  if (warp == 0) {
-    const uint32_t idesc = tc::idesc_bf16(OT_M, OT_N, false, false);
-    const uint32_t sa = tc::smem_u32(smem), sb = tc::smem_u32(smem + OT_A);
+  const uint32_t idesc = tc::idesc_bf16(OT_M, OT_N, false, false);
+  const uint32_t sb = tc::smem_u32(sB);
+  auto issue = [&](int t) {  // warp 0: MMAs of tile t into accumulator t & 1
+    const uint32_t sa = tc::smem_u32(sA + (t & 1) * OT_A);
+    const uint32_t acc = tbase + (uint32_t)((t & 1) * OT_N);
 #pragma unroll
     for (int ks = 0; ks < OT_K / 16; ++ks)
-      tc::mma_bf16_ss_w(tbase, tc::sdesc(sa + ks * 256, 128, OT_DC * 128), tc::sdesc(sb + ks * 256, 128, OT_DC * 128),
+      tc::mma_bf16_ss_w(acc, tc::sdesc(sa + ks * 256, 128, OT_DC * 128), tc::sdesc(sb + ks * 256, 128, OT_DC * 128),
                         idesc, ks > 0 ? 1u : 0u);
-    tc::mma_commit_w(bar);
-  }
-  tc::mbar_wait(bar, 0);
-  tc::fence_after();
-  // epilogue: warp w reads TMEM lanes 32*(w&3) .. +31 (rows), columns half (w>>2)
-  const int quarter = warp & 3, half = warp >> 2;
+    tc::mma_commit_w(&bar[t & 1]);
+  };
+  if (warp == 0 && nt > 0) issue(0);
+  const int quarter = warp & 3, cq = warp >> 2;  // TMEM lane quarter, column quarter
   const int row = quarter * 32 + lane;
-  const int64_t t = m0 + row;                // d_act row = (i, j)
-  const int64_t i = t / R, j = t % R;
-  const float sc = rec[t];
   const int64_t Rk = R * k;
+  for (int t = 0; t < nt; ++t) {
+    if (warp == 0 && t + 1 < nt) issue(t + 1);  // A(t+1) resident, accumulator (t+1)&1 drained
+    tc::mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+    tc::fence_after();
+    if (t + 2 < nt) {  // MMA(t) is done with A buffer t & 1
+      load_a(t + 2, t & 1);
+      tc::cp_async_commit();
+    }
+    const int64_t tr = (int64_t)(g + (int64_t)t * G) * OT_M + row;  // d_act row = (i, j)
+    const int64_t i = tr / R, j = tr % R;
+    const float sc = rec[tr];
 #pragma unroll 1
-  for (int pc = 0; pc < OT_N / 2 / 32; ++pc) {  // 4 groups of 32 columns per thread
-    const int col = half * (OT_N / 2) + pc * 32;
-    float v[32];
-    tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + col, v);
-    tc::wait_ld();
-    const int p = (n0 + col) / k;  // k == 32: one p per 32 columns
-    uint32_t pk[16];
+    for (int pc = 0; pc < OT_N / 4 / 32; ++pc) {
+      const int col = cq * (OT_N / 4) + pc * 32;
+      float v[32];
+      tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((t & 1) * OT_N + col), v);
+      tc::wait_ld();
+      const int p = (n0 + col) / k;
+      uint32_t pk[16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e] * sc, v[2 * e + 1] * sc);
-    uint4* dst = reinterpret_cast<uint4*>(dnum + (i * k + p) * Rk + j * k);
+      for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e] * sc, v[2 * e + 1] * sc);
+      // the warp's 32 rows are 32 x 64 B = 2 KB contiguous in dnum row (i, p): go
+      // through a per-warp shared buffer so each store instruction writes 512
+      // contiguous bytes (chunk c = e*32 + lane <- row c/4, part c%4)
+      uint4* xb = reinterpret_cast<uint4*>(sX + warp * 2048);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      for (int e = 0; e < 4; ++e)
+        xb[lane * 4 + (e ^ (lane & 3))] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(dnum + (i * k + p) * Rk + (j - lane) * k);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int c = e * 32 + lane, r = c >> 2, q = c & 3;
+        dst[c] = xb[r * 4 + (q ^ (r & 3))];
+      }
+      __syncwarp();
+    }
+    if (t + 2 < nt) asm volatile("cp.async.wait_group 1;" ::: "memory");  // A(t+1) landed, A(t+2) in flight
+    else tc::cp_async_wait0();
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();  // A(t+1) visible to the tensor core; accumulator t & 1 drained
+    tc::fence_after();
   }
-  tc::fence_before();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<256>(tbase);
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
 }  // namespace
@@ -103,11 +148,17 @@ bool opm_dnum_tc(const void* dact, const void* wout, const float* rec, void* dnu
   if (((uintptr_t)dact | (uintptr_t)wout | (uintptr_t)dnum) & 15) return false;
   static bool attr = false;
   if (!attr) {
-    EVO_CUDA(cudaFuncSetAttribute(opm_dnum_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OT_SMEM));
+    EVO_CUDA(cudaFuncSetAttribute(opm_dnum_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OT_SMEM_P));
     attr = true;
   }
-  dim3 grid((unsigned)(NI * R / OT_M), (unsigned)(k * k / OT_N));
-  opm_dnum_tc_kernel<<<grid, 256, OT_SMEM, s>>>((const bf16*)dact, (const bf16*)wout, rec, (bf16*)dnum, R, (int)k);
+  const int64_t n_mt = NI * R / OT_M;
+  const int n_nt = (int)(k * k / OT_N);
+  int G = num_sms() / n_nt;
+  if (G < 1) G = 1;
+  if (G > n_mt) G = (int)n_mt;
+  dim3 grid((unsigned)G, (unsigned)n_nt);
+  opm_dnum_tc_kernel<<<grid, OT_T, OT_SMEM_P, s>>>((const bf16*)dact, (const bf16*)wout, rec, (bf16*)dnum, R,
+                                                  (int)k, n_mt, G);
   EVO_LAUNCH_CHECK();
   count_launch(1);
   return true;

@@ -103,7 +103,7 @@ class BlockEngine:
         self.branch_streams = (torch.device(store.device).type == "cuda"
                                and os.environ.get("EVO_BRANCH_STREAMS", "1") != "0")
         self._s2 = None
-        self.opm_dnum_fused = os.environ.get("EVO_OPM_DNUM_TC", "0") == "1"
+        self.opm_dnum_fused = os.environ.get("EVO_OPM_DNUM_TC", "1") != "0"
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
         # two arenas for the block-pipelined backward (blocks_bwd), alternating by block
