@@ -249,6 +249,13 @@ int evo_opm_norm_apply_rows(const void* num, int num_dtype, const float* rec, vo
  * k = 32, R % 128 == 0 (EVO_ERR_UNSUPPORTED otherwise). */
 int evo_opm_dnum(const void* d_act, const void* w_out, const float* rec, void* dnum, int64_t R, int64_t k,
                  int64_t NI, int64_t C, int dtype, void* stream);
+/* OPM forward a, c -> outn: the sum over sequences as one tcgen05 GEMM with the
+ * normalisation and the [(i, j), p*k+q] re-layout in its epilogue:
+ *   outn[i*R+j, p*k+q] = rec[i*R+j] * sum_s a[s, i*k+p] * c[s, j*k+q]
+ * a [S, NI*k], c [S, R*k], outn [NI*R, k*k] bf16.  Needs S = 128, k = 32,
+ * R*k % 256 == 0 (EVO_ERR_UNSUPPORTED otherwise). */
+int evo_opm_outn(const void* a, const void* c, const float* rec, void* outn, int64_t S, int64_t R, int64_t k,
+                 int64_t NI, int dtype, void* stream);
 
 /* ---- DAP re-layout (src/harness.py:262-293) ------------------------------
  * dst[b, a, :] = src[a, b, :] for src [A, B, elem_bytes]: the outer-axis swap

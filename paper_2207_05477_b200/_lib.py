@@ -67,6 +67,7 @@ SIGNATURES = {
     "evo_opm_norm_bwd_rows": (_i, [_p, _i, _p, _p, _i, _i64, _i64, _i64, _p]),
     "evo_swap01": (_i, [_p, _p, _i64, _i64, _i64, _p]),
     "evo_opm_dnum": (_i, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _p]),
+    "evo_opm_outn": (_i, [_p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _p]),
     "evo_opm_rec": (_i, [_p, _p, _i64, _i64, _i64, _i64, _p]),
     "evo_opm_norm_apply_rows": (_i, [_p, _i, _p, _p, _i, _i64, _i64, _i64, _p]),
     "evo_pair_bias_bwd_workspace": (_i64, [_i64, _i64]),

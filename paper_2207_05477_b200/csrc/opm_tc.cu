@@ -174,3 +174,165 @@ extern "C" int evo_opm_dnum(const void* d_act, const void* w_out, const float* r
               "opm_dnum: needs c_z = 128, k = 32, n_res a multiple of 128, 16-B aligned operands");
   EVO_API_END
 }
+
+// ---------------------------------------------------------------------------
+// Forward: num = a^T c over this worker's sequences, written straight in the
+// normalised [(i, j), p*k + q] layout the w_out projection reads
+// (src/model.py:366-377):
+//
+//   outn[i*R + j, p*k + q] = rec[i*R + j] * sum_s a[s, i*k + p] * c[s, j*k + q]
+//
+// A = a^T and B = c are both MN-major in memory ([S, R*k] rows); K = S = 128 is
+// staged whole.  Tile 128 rows (4 values of i x 32 p) x 256 columns (8 j x
+// 32 q): TMEM lane quarter = one i, lane = p, and a 32-column slice = one j,
+// so a warp's 32 lanes hold the 2 KB outn row (i, j); it goes out through the
+// same per-warp shared-memory transpose as above (512 B per store).
+namespace evo {
+namespace {
+
+constexpr int OF_K = 128;                        // sequences (contraction)
+constexpr int OF_M = 128, OF_N = 256;
+constexpr int OF_A = OF_M * OF_K * 2, OF_B = OF_N * OF_K * 2;
+constexpr int OF_T = 512;
+constexpr int OF_X = (OF_T / 32) * 2048;
+constexpr int OF_SMEM = OF_B + 2 * OF_A + OF_X + 64;
+
+// MN-major staging: element (kk, m) of a [K x E] tile (E contiguous in memory)
+// -> core (kk/8, m/8) at ((kk/8)*(E/8) + m/8)*128 + (kk%8)*16 + (m%8)*2
+template <int E>
+__device__ __forceinline__ void stage_mn(uint8_t* dst, const bf16* src, int64_t ld, int tid) {
+  constexpr int EC = E / 8;
+  for (int e = tid; e < OF_K * EC; e += OF_T) {
+    const int kk = e / EC, c = e % EC;
+    tc::cp_async16(dst + ((kk >> 3) * EC + c) * 128 + (kk & 7) * 16, src + (int64_t)kk * ld + c * 8);
+  }
+}
+
+__global__ void __launch_bounds__(OF_T, 1) opm_outn_tc_kernel(const bf16* __restrict__ a, const bf16* __restrict__ c,
+                                                              const float* __restrict__ rec,
+                                                              bf16* __restrict__ outn, int64_t R, int k,
+                                                              int64_t n_mt, int G) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + OF_B;
+  uint8_t* sX = smem + OF_B + 2 * OF_A;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OF_B + 2 * OF_A + OF_X);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t Rk = R * k;
+  const int64_t n0 = (int64_t)blockIdx.y * OF_N;  // c columns (j, q)
+  const int g = blockIdx.x;
+  const int nt = (int)((n_mt - g + G - 1) / G);
+  auto load_a = [&](int t, int buf) {
+    stage_mn<OF_M>(sA + buf * OF_A, a + (int64_t)(g + (int64_t)t * G) * OF_M, Rk, tid);
+  };
+  stage_mn<OF_N>(sB, c + n0, Rk, tid);
+  if (nt > 0) load_a(0, 0);
+  if (nt > 1) load_a(1, 1);
+  tc::cp_async_commit();
+  if (warp == 0) tc::tmem_alloc<512>(slot);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+  }
+  tc::cp_async_wait0();
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tbase = *slot;
+  const uint32_t idesc = tc::idesc_bf16(OF_M, OF_N, true, true);
+  const uint32_t sb = tc::smem_u32(sB);
+  auto issue = [&](int t) {
+    const uint32_t sa = tc::smem_u32(sA + (t & 1) * OF_A);
+    const uint32_t acc = tbase + (uint32_t)((t & 1) * OF_N);
+#pragma unroll
+    for (int ks = 0; ks < OF_K / 16; ++ks)
+      tc::mma_bf16_ss_w(acc, tc::sdesc(sa + ks * 2 * (OF_M / 8) * 128, (OF_M / 8) * 128, 128),
+                        tc::sdesc(sb + ks * 2 * (OF_N / 8) * 128, (OF_N / 8) * 128, 128), idesc, ks > 0 ? 1u : 0u);
+    tc::mma_commit_w(&bar[t & 1]);
+  };
+  if (warp == 0 && nt > 0) issue(0);
+  const int quarter = warp & 3, cq = warp >> 2;  // TMEM lane quarter (= one i), column quarter (2 j)
+  for (int t = 0; t < nt; ++t) {
+    if (warp == 0 && t + 1 < nt) issue(t + 1);
+    tc::mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
+    tc::fence_after();
+    if (t + 2 < nt) {
+      load_a(t + 2, t & 1);
+      tc::cp_async_commit();
+    }
+    const int64_t m0 = (int64_t)(g + (int64_t)t * G) * OF_M;  // rows (i, p) of num
+    const int64_t i = m0 / k + quarter;
+    const int p = lane;
+#pragma unroll 1
+    for (int jc = 0; jc < OF_N / 4 / 32; ++jc) {
+      const int col = cq * (OF_N / 4) + jc * 32;
+      const int64_t j = (n0 + col) / k;
+      float v[32];
+      tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((t & 1) * OF_N + col), v);
+      tc::wait_ld();
+      const float sc = rec[i * R + j];
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e] * sc, v[2 * e + 1] * sc);
+      // lane p's 64 B are at p*64 in the 2 KB outn row (i, j)
+      uint4* xb = reinterpret_cast<uint4*>(sX + warp * 2048);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        xb[p * 4 + (e ^ (p & 3))] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+      __syncwarp();
+      uint4* dst = reinterpret_cast<uint4*>(outn + (i * R + j) * (int64_t)(k * k));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int cc = e * 32 + lane, r = cc >> 2, q = cc & 3;
+        dst[cc] = xb[r * 4 + (q ^ (r & 3))];
+      }
+      __syncwarp();
+    }
+    if (t + 2 < nt) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else tc::cp_async_wait0();
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace
+
+// a, c [S = 128, NI*k] / [S, R*k] bf16 (this shard's rows of a; all of c),
+// rec [NI*R] -> outn [NI*R, k*k] bf16.  false: shape not covered.
+bool opm_outn_tc(const void* a, const void* c, const float* rec, void* outn, int64_t S, int64_t R, int64_t k,
+                 int64_t NI, cudaStream_t s) {
+  if (S != OF_K || k != 32 || ((R * k) % OF_N) != 0 || NI <= 0 || ((NI * k) % OF_M) != 0) return false;
+  if (((uintptr_t)a | (uintptr_t)c | (uintptr_t)outn) & 15) return false;
+  static bool attr = false;
+  if (!attr) {
+    EVO_CUDA(cudaFuncSetAttribute(opm_outn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OF_SMEM));
+    attr = true;
+  }
+  const int64_t n_mt = NI * k / OF_M;
+  const int n_nt = (int)(R * k / OF_N);
+  int G = num_sms() / n_nt;
+  if (G < 1) G = 1;
+  if (G > n_mt) G = (int)n_mt;
+  dim3 grid((unsigned)G, (unsigned)n_nt);
+  opm_outn_tc_kernel<<<grid, OF_T, OF_SMEM, s>>>((const bf16*)a, (const bf16*)c, rec, (bf16*)outn, R, (int)k,
+                                                 n_mt, G);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  return true;
+}
+
+}  // namespace evo
+
+extern "C" int evo_opm_outn(const void* a, const void* c, const float* rec, void* outn, int64_t S, int64_t R,
+                            int64_t k, int64_t NI, int dtype, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(dtype == EVO_BF16, EVO_ERR_UNSUPPORTED, "opm_outn: bf16 only");
+  EVO_REQUIRE(evo::opm_outn_tc(a, c, rec, outn, S, R, k, NI, (cudaStream_t)stream), EVO_ERR_UNSUPPORTED,
+              "opm_outn: needs S = 128 sequences per worker, k = 32, n_res*k a multiple of 256");
+  EVO_API_END
+}

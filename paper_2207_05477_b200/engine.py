@@ -343,12 +343,16 @@ class BlockEngine:
         a, c = ops.opm_proj(ab, self.P(f"{prefix}.b_left"), self.P(f"{prefix}.b_right"),
                             self._feat_rows(feats)[2], k)
         del ab
-        num = torch.empty((R * k, R * k), dtype=self.opm_num_dtype, device=msa_in.device)
-        ops.gemm(a.view(s_loc, R * k), c.view(s_loc, R * k), num, ta=True)
-        num = self._opm_reduce(num)            # the shard's rows of the sum over all sequences
-        rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt, i0=self.r0, ni=r_loc,
-                                     rec=self._rec_for(feats))
-        del num
+        rec = self._rec_for(feats)
+        outn = None
+        if self.opm_dnum_fused and self.r_loc == R:  # unsharded: sum + normalise + re-layout in one kernel
+            outn = ops.opm_outn(a.view(s_loc, R * k), c.view(s_loc, R * k), rec, s_loc, R, k)
+        if outn is None:
+            num = torch.empty((R * k, R * k), dtype=self.opm_num_dtype, device=msa_in.device)
+            ops.gemm(a.view(s_loc, R * k), c.view(s_loc, R * k), num, ta=True)
+            num = self._opm_reduce(num)            # the shard's rows of the sum over all sequences
+            rec, outn = ops.opm_norm_fwd(num, feats.msa_mask, S, R, k, dt, i0=self.r0, ni=r_loc, rec=rec)
+            del num
         if out is None:
             out = torch.empty((r_loc * R, cfg.c_z), dtype=dt, device=msa_in.device)
         ops.gemm_bias(outn, self.W(f"{prefix}.w_out", k * k), out, self.P(f"{prefix}.b_out"), res=pair_res,

@@ -395,6 +395,20 @@ def opm_dnum(d_act, w_out, rec, R, k, ni=None):
     return dnum
 
 
+def opm_outn(a, c, rec, S, R, k, ni=None):
+    """The OPM's normalised outer-product block outn [(i, j), p*k+q] straight
+    from the projections a, c [S, R*k]: the sum over sequences as one tcgen05
+    GEMM with the normalisation and re-layout in its epilogue.  None when the
+    shape is not covered (the caller runs GEMM + opm_norm_fwd)."""
+    ni = R if ni is None else ni
+    if (a.dtype != torch.bfloat16 or c.dtype != torch.bfloat16 or S != 128 or k != 32 or (R * k) % 256
+            or (ni * k) % 128 or not a.is_contiguous() or not c.is_contiguous()):
+        return None
+    outn = torch.empty((ni * R, k * k), dtype=torch.bfloat16, device=a.device)
+    call("evo_opm_outn", ptr(a), ptr(c), ptr(rec), ptr(outn), S, R, k, ni, dcode(a), stream())
+    return outn
+
+
 def opm_norm_bwd(doutn, rec, R, k, out_dtype, ni=None):
     ni = R if ni is None else ni
     dnum = torch.empty((ni * k, R * k), dtype=out_dtype, device=doutn.device)

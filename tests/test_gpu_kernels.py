@@ -488,3 +488,20 @@ def test_opm_dnum_tc_vs_torch(R, ni):
     doutn = (d_act.float() @ w_out.float().t()) * rec[:, None]          # [(i, j), (p, q)]
     ref = doutn.view(ni, R, k, k).permute(0, 2, 1, 3).reshape(ni * k, R * k)
     assert rel(dnum.float(), ref) <= 1e-2
+
+
+@pytest.mark.parametrize("R", [256, 384])
+def test_opm_outn_tc_vs_torch(R):
+    """OPM forward: sum over sequences + normalisation + [(i, j), p*k+q]
+    re-layout as one tcgen05 GEMM (csrc/opm_tc.cu) against fp32 torch."""
+    from paper_2207_05477_b200 import ops
+    S, k = 128, 32
+    torch.manual_seed(R)
+    a = (torch.randn(S, R * k, device="cuda") * 0.3).bfloat16()
+    c = (torch.randn(S, R * k, device="cuda") * 0.3).bfloat16()
+    rec = torch.rand(R * R, device="cuda") + 0.01
+    outn = ops.opm_outn(a, c, rec, S, R, k)
+    assert outn is not None and outn.shape == (R * R, k * k)
+    num = a.float().t() @ c.float()                                      # [(i, p), (j, q)]
+    ref = num.view(R, k, R, k).permute(0, 2, 1, 3).reshape(R * R, k * k) * rec[:, None]
+    assert rel(outn.float(), ref) <= 1e-2

@@ -1,4 +1,6 @@
 import os, sys, subprocess, numpy as np
+"""A/B the gradients of one bench-shape fwd+bwd (2 blocks) with an engine switch on/off:
+    CMP_VAR=EVO_OPM_DNUM_TC python tools/cmp_stream.py"""
 sys.path.insert(0, "/root/repo")
 if len(sys.argv) > 1:
     import torch
@@ -12,7 +14,7 @@ if len(sys.argv) > 1:
     print("loss", float(loss))
 else:
     for e in ("1", "0"):
-        subprocess.run([sys.executable, __file__, f"/tmp/g{e}.npy"], env=dict(os.environ, EVO_GLUE_STREAM=e), check=True)
+        subprocess.run([sys.executable, __file__, f"/tmp/g{e}.npy"], env=dict(os.environ, **{os.environ.get("CMP_VAR", "EVO_GLUE_STREAM"): e}), check=True)
     a, b = np.load("/tmp/g1.npy"), np.load("/tmp/g0.npy")
     from paper_2207_05477_b200.model import ModelConfig, flatten_params
     from paper_2207_05477_b200.fusion import build_layout
@@ -25,4 +27,12 @@ else:
         d = np.abs(x - y).max() / max(np.abs(y).max(), 1e-30)
         worst.append((d, s.name))
     worst.sort(reverse=True)
+    gmax = np.abs(b).max()
+    print(f"global: max|diff| / max|g| = {np.abs(a - b).max() / gmax:.3e}  (gmax {gmax:.3e})")
+    w2 = []
+    for s_ in slots:
+        lo = s_.offset // 4; n = int(np.prod(s_.shape)) if s_.shape else 1
+        w2.append((np.abs(a[lo:lo+n] - b[lo:lo+n]).max() / max(np.abs(b[lo:lo+n]).max(), 1e-3 * gmax), s_.name))
+    w2.sort(reverse=True)
+    print("floored at 1e-3 gmax:", [(f"{d:.2e}", n) for d, n in w2[:6]])
     for d, n in worst[:12]: print(f"{d:.3e} {n}")
