@@ -1,7 +1,7 @@
-import os, sys, subprocess, numpy as np
 """A/B the gradients of one bench-shape fwd+bwd (2 blocks) with an engine switch on/off:
-    CMP_VAR=EVO_OPM_DNUM_TC python tools/cmp_stream.py"""
-sys.path.insert(0, "/root/repo")
+    CMP_VAR=EVO_OPM_DNUM_TC python tools/cmp_stream.py     (default switch: EVO_GLUE_STREAM)"""
+import os, sys, subprocess, numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1:
     import torch
     from paper_2207_05477_b200.model import ModelConfig
