@@ -244,13 +244,18 @@ bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
         EVO_CUDA(cudaEventSynchronize(e1));
         EVO_CUDA(cudaEventElapsedTime(&tms[r], e0, e1));
       }
-      // the first candidate (heuristic order) within 3% of the fastest: near-ties
-      // resolve the same way from run to run, so the chosen algorithm -- and the
-      // rounding it implies -- rarely depends on timing noise
+      // the first candidate (heuristic order) within EVO_GEMM_TUNE_MARGIN (default
+      // 0: the fastest) of the fastest; a margin of a few percent makes near-ties
+      // resolve the same way from run to run (the chosen algorithm, and the
+      // rounding it implies, then rarely depends on timing noise) at ~1% step time
       float best = 1e30f;
       for (int r = 0; r < nres; ++r) best = fminf(best, tms[r]);
+      static const float margin = [] {
+        const char* e = getenv("EVO_GEMM_TUNE_MARGIN");
+        return e ? (float)atof(e) : 0.0f;
+      }();
       for (int r = 0; r < nres; ++r)
-        if (tms[r] <= best * 1.03f) {
+        if (tms[r] <= best * (1.0f + margin)) {
           ch.algo = res[r].algo;
           break;
         }
