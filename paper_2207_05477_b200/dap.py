@@ -34,7 +34,6 @@ The reference transposes around its collectives as well (src/model.py:335-340).
 from __future__ import annotations
 
 import numpy as np
-import torch
 
 from . import ops
 from .engine import F32, BlockEngine, DeviceFeatures, Variant
