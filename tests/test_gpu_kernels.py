@@ -505,3 +505,30 @@ def test_opm_outn_tc_vs_torch(R):
     num = a.float().t() @ c.float()                                      # [(i, p), (j, q)]
     ref = num.view(R, k, R, k).permute(0, 2, 1, 3).reshape(R * R, k * k) * rec[:, None]
     assert rel(outn.float(), ref) <= 1e-2
+
+
+@pytest.mark.parametrize("A,B,E,dt", [(8, 4, 256, torch.bfloat16), (3, 5, 7, torch.bfloat16), (16, 2, 33, torch.float32)])
+def test_swap01_vs_torch(A, B, E, dt):
+    """DAP outer-axis swap (csrc/dap.cu): dst[b, a, :] = src[a, b, :] for 16-B,
+    4-B and byte-granular row sizes."""
+    from paper_2207_05477_b200 import ops
+    x = torch.randn(A, B, E, device="cuda").to(dt)
+    y = ops.swap01(x, A, B)
+    assert torch.equal(y.view(B, A, E), x.permute(1, 0, 2))
+
+
+def test_opm_rec_once_per_pass_matches_inline():
+    """The normaliser computed once (evo_opm_rec) and applied per block
+    (evo_opm_norm_apply_rows) equals the inline evo_opm_norm_fwd_rows, full and
+    for a row shard."""
+    from paper_2207_05477_b200 import ops
+    S, R, k = 24, 64, 32
+    torch.manual_seed(5)
+    mask = (torch.rand(S * R, device="cuda") > 0.2).float()
+    num = torch.randn(R * k, R * k, device="cuda").bfloat16()
+    rec0, out0 = ops.opm_norm_fwd(num, mask, S, R, k, torch.bfloat16)
+    rec = ops.opm_rec(mask, S, R)
+    _, out1 = ops.opm_norm_fwd(num, mask, S, R, k, torch.bfloat16, rec=rec)
+    assert torch.equal(rec0, rec) and torch.equal(out0, out1)
+    rec_s = ops.opm_rec(mask, S, R, i0=16, ni=32)
+    assert torch.equal(rec_s, rec.view(R, R)[16:48].reshape(-1))
