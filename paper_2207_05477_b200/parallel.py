@@ -123,12 +123,22 @@ class Comm:
 
     def broadcast(self, t: torch.Tensor, root: int, module: str) -> torch.Tensor:
         """In place: ``t`` is the payload on the root, the receive buffer elsewhere."""
-        dist.broadcast(t, src=self.ranks[root], group=self.group)
+        if self._host(t):
+            h = t.cpu()
+            dist.broadcast(h, src=self.ranks[root], group=self.group)
+            t.copy_(h)
+        else:
+            dist.broadcast(t, src=self.ranks[root], group=self.group)
         self._rec("broadcast", t, module)
         return t
 
     def allreduce_sum(self, t: torch.Tensor, module: str) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        if self._host(t):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         self._rec("allreduce", t, module)
         return t
 

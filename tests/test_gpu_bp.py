@@ -1,0 +1,87 @@
+"""Branch Parallelism and DP (src/harness.py:392-616) on the sm_100a engine.
+
+As in test_gpu_dap.py, the ranks are processes sharing the test box's one
+GPU over a gloo group (device buffers staged through host memory; NCCL takes
+them in place).  The synced gradients and the loss of a bp2 and a dp2 x bp2
+step must match the unsharded engine (tests/test_acceptance.py:184-198 of the
+reference), and each block must record the reference's 3 broadcasts + 1
+all-reduce (tests/test_acceptance.py:156-166)."""
+
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+CFG = dict(n_blocks=2, n_seq=16, n_res=32, c_m=64, c_z=32, heads=2, opm_dim=8)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2207_05477_b200 import _lib
+    _lib.lib()
+
+
+def _engine(dtype_name):
+    from paper_2207_05477_b200.engine import BlockEngine, DeviceFeatures
+    from paper_2207_05477_b200.fusion import FusionEngine
+    from paper_2207_05477_b200.model import ModelConfig, flatten_params, init_params, make_features
+    cfg = ModelConfig(**CFG)
+    P = init_params(cfg, 7)
+    dt = torch.bfloat16 if dtype_name == "bf16" else torch.float32
+    st = FusionEngine([(n, P[n]) for n, _ in flatten_params(cfg)], shadow_dtype=dt)
+    eng = BlockEngine(cfg, st, dt)
+    return cfg, st, eng, DeviceFeatures(make_features(cfg, 3), "cuda", cfg)
+
+
+def _worker(rank, world, port, dtype_name, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2207_05477_b200.parallel import GridConfig, bp_step, build_groups
+    cfg, st, eng, feats = _engine(dtype_name)
+    grid = GridConfig.for_world(world)
+    bp, world_comm = build_groups(grid)
+    loss = bp_step(eng, feats, bp, world_comm, grid, cfg.n_blocks)
+    torch.cuda.synchronize()
+    if rank == 0:
+        recs = [(r.module, r.primitive) for r in bp.records]
+        np.savez(out_path, loss=loss.cpu().numpy(), grads=st.regions["grads"].cpu().numpy(),
+                 recs=np.array(recs, dtype=object), allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, dtype_name):
+    import torch.multiprocessing as mp
+    from test_gpu_dap import _free_port
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r.npz")
+        mp.spawn(_worker, args=(world, _free_port(), dtype_name, out), nprocs=world, join=True)
+        r = np.load(out, allow_pickle=True)
+        return {k: r[k] for k in r.files}
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world,dtype", [(2, "f32"), (4, "f32"), (2, "bf16")])
+def test_bp_matches_unsharded(world, dtype):
+    _, st, eng, feats = _engine(dtype)
+    loss, _ = eng.forward_backward(feats, 1)
+    torch.cuda.synchronize()
+    base_loss, base_g = float(loss.item()), st.regions["grads"].cpu().numpy()
+    res = _run(world, dtype)
+    tol = 1e-4 if dtype == "f32" else 3e-2
+    assert abs(float(res["loss"][0]) - base_loss) <= tol * abs(base_loss)
+    assert rel_err(res["grads"], base_g, np.abs(base_g).max()) <= (tol if dtype == "f32" else 5e-2)
+    block = [r for r in map(tuple, res["recs"]) if r[0] in ("opm", "msa_stack", "pair_stack")]
+    assert len(block) == 4 * CFG["n_blocks"]
+    assert sum(1 for r in block if r[1] == "broadcast") == 3 * CFG["n_blocks"]
