@@ -270,9 +270,12 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one process per GPU; EVO_DIST_BACKEND=gloo lets several ranks share a GPU
+    # (functional checks of the multi-rank path on a one-GPU box, not a bench)
+    backend = os.environ.get("EVO_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count() if backend == "gloo" else local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     _lib.lib()
     shape = dict(SHAPE)
     if args.blocks:
