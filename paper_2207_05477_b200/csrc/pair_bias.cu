@@ -194,7 +194,6 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
   using TL = PbTile<C, T>;
   extern __shared__ __align__(16) uint8_t tile[];
   __shared__ float4 sw[C][2];   // w[c, 0..7] (zero beyond H)
-  __shared__ float2 sgb[C];     // (gamma, beta)
   const int64_t RR = NI * NJ;
   const int64_t i0 = blockIdx.x * (int64_t)128;
   // stage: chunk k of row r by thread (r * CPR + k) % 128
@@ -207,13 +206,49 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
     }
   }
   tc::cp_async_commit();
-  for (int e = threadIdx.x; e < C; e += blockDim.x) {
-    float t[8];
+  // LayerNorm folded into the projection: with gw = g (x) w and the per-head
+  // constants G = sum_c gw[c, :], BW = sum_c b[c] w[c, :],
+  //   nb[h] = rstd * (sum_c z_c gw[c, h] - mean * G[h]) + BW[h],
+  // so one pass over the row gives the statistics and the head sums together
+  __shared__ float sG[8], sBW[8], spart[4][16];
+  static_assert(C <= 128 * 4, "one block of 128 threads covers the channels");
+  {
+    float gsum[8], bsum[8];
 #pragma unroll
-    for (int hh = 0; hh < 8; ++hh) t[hh] = hh < H ? w[e * H + hh] : 0.f;
-    sw[e][0] = make_float4(t[0], t[1], t[2], t[3]);
-    sw[e][1] = make_float4(t[4], t[5], t[6], t[7]);
-    sgb[e] = make_float2(g[e], b[e]);
+    for (int hh = 0; hh < 8; ++hh) gsum[hh] = bsum[hh] = 0.f;
+    for (int e = threadIdx.x; e < C; e += blockDim.x) {
+      float t[8];
+      const float ge = g[e], be = b[e];
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) {
+        const float we = hh < H ? w[e * H + hh] : 0.f;
+        t[hh] = ge * we;
+        gsum[hh] += t[hh];
+        bsum[hh] += be * we;
+      }
+      sw[e][0] = make_float4(t[0], t[1], t[2], t[3]);
+      sw[e][1] = make_float4(t[4], t[5], t[6], t[7]);
+    }
+#pragma unroll
+    for (int hh = 0; hh < 8; ++hh) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        gsum[hh] += __shfl_xor_sync(0xffffffffu, gsum[hh], o);
+        bsum[hh] += __shfl_xor_sync(0xffffffffu, bsum[hh], o);
+      }
+    }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int hh = 0; hh < 8; ++hh) {
+        spart[threadIdx.x >> 5][hh] = gsum[hh];
+        spart[threadIdx.x >> 5][8 + hh] = bsum[hh];
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) {
+    const float acc = spart[0][threadIdx.x] + spart[1][threadIdx.x] + spart[2][threadIdx.x] + spart[3][threadIdx.x];
+    if (threadIdx.x < 8) sG[threadIdx.x] = acc;
+    else sBW[threadIdx.x - 8] = acc;
   }
   tc::cp_async_wait0();
   __syncthreads();
@@ -221,7 +256,10 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
   if (i >= RR) return;
   const int64_t tok = swap ? (i % NI) * NJ + i / NI : i;
   const uint8_t* row = tile + threadIdx.x * TL::ROWB;
-  auto chunk = [&](int c, float (&f)[8]) {
+  float s = 0.f, q = 0.f;
+  float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll 2
+  for (int c = 0; c < C; c += 8) {
     Vec8<T> v;
     if constexpr (sizeof(T) == 2) {
       v.u = *reinterpret_cast<const uint4*>(row + c * 2);
@@ -229,50 +267,26 @@ __global__ void __launch_bounds__(128) pair_bias_fwd_tpt_kernel(
       v.a = *reinterpret_cast<const float4*>(row + c * 4);
       v.b = *reinterpret_cast<const float4*>(row + c * 4 + 16);
     }
+    float f[8];
     cvt8(v, f);
-  };
-  float s = 0.f;
-#pragma unroll 4
-  for (int c = 0; c < C; c += 8) {
-    float f[8];
-    chunk(c, f);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) s += f[e];
-  }
-  const float mu = s / (float)C;
-  float q = 0.f;
-#pragma unroll 4
-  for (int c = 0; c < C; c += 8) {
-    float f[8];
-    chunk(c, f);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float d = f[e] - mu;
-      q += d * d;
-    }
-  }
-  const float inv = rsqrtf(q / (float)C + 1e-5f);
-  float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll 1
-  for (int c = 0; c < C; c += 8) {
-    float f[8];
-    chunk(c, f);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float2 gb = sgb[c + e];
       const float4 w0 = sw[c + e][0], w1 = sw[c + e][1];
-      const float zl = (f[e] - mu) * inv * gb.x + gb.y;
-      const float2 z2 = make_float2(zl, zl);
+      const float2 z2 = make_float2(f[e], f[e]);
+      s += f[e];
+      q = fmaf(f[e], f[e], q);
       p[0] = __ffma2_rn(z2, make_float2(w0.x, w0.y), p[0]);
       p[1] = __ffma2_rn(z2, make_float2(w0.z, w0.w), p[1]);
       p[2] = __ffma2_rn(z2, make_float2(w1.x, w1.y), p[2]);
       p[3] = __ffma2_rn(z2, make_float2(w1.z, w1.w), p[3]);
     }
   }
+  const float mu = s / (float)C;
+  const float inv = rsqrtf(fmaxf(q / (float)C - mu * mu, 0.f) + 1e-5f);
   const float ph[8] = {p[0].x, p[0].y, p[1].x, p[1].y, p[2].x, p[2].y, p[3].x, p[3].y};
 #pragma unroll
   for (int hh = 0; hh < 8; ++hh)
-    if (hh < H) nb[hh * RR + i] = from_f<T>(ph[hh]);
+    if (hh < H) nb[hh * RR + i] = from_f<T>(fmaf(inv, ph[hh] - mu * sG[hh], sBW[hh]));
   mean[tok] = mu;
   rstd[tok] = inv;
 }
