@@ -93,15 +93,15 @@ __global__ void __launch_bounds__(OT_T, 1) opm_dnum_tc_kernel(const bf16* __rest
   const int64_t Rk = R * k;
   for (int t = 0; t < nt; ++t) {
     if (warp == 0 && t + 1 < nt) issue(t + 1);  // A(t+1) resident, accumulator (t+1)&1 drained
+    const int64_t tr = (int64_t)(g + (int64_t)t * G) * OT_M + row;  // d_act row = (i, j)
+    const int64_t i = tr / R, j = tr % R;
+    const float sc = __ldg(rec + tr);  // fetched while the MMAs run
     tc::mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     tc::fence_after();
     if (t + 2 < nt) {  // MMA(t) is done with A buffer t & 1
       load_a(t + 2, t & 1);
       tc::cp_async_commit();
     }
-    const int64_t tr = (int64_t)(g + (int64_t)t * G) * OT_M + row;  // d_act row = (i, j)
-    const int64_t i = tr / R, j = tr % R;
-    const float sc = rec[tr];
 #pragma unroll 1
     for (int pc = 0; pc < OT_N / 4 / 32; ++pc) {
       const int col = cq * (OT_N / 4) + pc * 32;
@@ -128,11 +128,10 @@ __global__ void __launch_bounds__(OT_T, 1) opm_dnum_tc_kernel(const bf16* __rest
       }
       __syncwarp();
     }
-    if (t + 2 < nt) asm volatile("cp.async.wait_group 1;" ::: "memory");  // A(t+1) landed, A(t+2) in flight
-    else tc::cp_async_wait0();
+    tc::cp_async_wait0();  // A(t+2) landed: MMA(t+2) is issued at the top of the next iteration
     tc::fence_proxy_async();
     tc::fence_before();
-    __syncthreads();  // A(t+1) visible to the tensor core; accumulator t & 1 drained
+    __syncthreads();  // A(t+2) visible to the tensor core; accumulator t & 1 drained
     tc::fence_after();
   }
   if (warp == 0) tc::tmem_dealloc<512>(tbase);
@@ -256,23 +255,26 @@ __global__ void __launch_bounds__(OF_T, 1) opm_outn_tc_kernel(const bf16* __rest
   const int quarter = warp & 3, cq = warp >> 2;  // TMEM lane quarter (= one i), column quarter (2 j)
   for (int t = 0; t < nt; ++t) {
     if (warp == 0 && t + 1 < nt) issue(t + 1);
+    const int64_t m0 = (int64_t)(g + (int64_t)t * G) * OF_M;  // rows (i, p) of num
+    const int64_t i = m0 / k + quarter;
+    const int p = lane;
+    float scv[OF_N / 4 / 32];  // rec of this warp's (i, j) rows, fetched while the MMAs run
+#pragma unroll
+    for (int jc = 0; jc < OF_N / 4 / 32; ++jc) scv[jc] = __ldg(rec + i * R + (n0 + cq * (OF_N / 4) + jc * 32) / k);
     tc::mbar_wait(&bar[t & 1], (uint32_t)((t >> 1) & 1));
     tc::fence_after();
     if (t + 2 < nt) {
       load_a(t + 2, t & 1);
       tc::cp_async_commit();
     }
-    const int64_t m0 = (int64_t)(g + (int64_t)t * G) * OF_M;  // rows (i, p) of num
-    const int64_t i = m0 / k + quarter;
-    const int p = lane;
-#pragma unroll 1
+#pragma unroll
     for (int jc = 0; jc < OF_N / 4 / 32; ++jc) {
       const int col = cq * (OF_N / 4) + jc * 32;
       const int64_t j = (n0 + col) / k;
       float v[32];
       tc::tmem_ld32(tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)((t & 1) * OF_N + col), v);
       tc::wait_ld();
-      const float sc = rec[i * R + j];
+      const float sc = scv[jc];
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) pk[e] = tc::pack_bf16(v[2 * e] * sc, v[2 * e + 1] * sc);
@@ -290,8 +292,7 @@ __global__ void __launch_bounds__(OF_T, 1) opm_outn_tc_kernel(const bf16* __rest
       }
       __syncwarp();
     }
-    if (t + 2 < nt) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else tc::cp_async_wait0();
+    tc::cp_async_wait0();  // A(t+2) landed: MMA(t+2) is issued at the top of the next iteration
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
