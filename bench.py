@@ -127,6 +127,28 @@ class ClockSampler:
 # CPU baseline (oracle port; test infrastructure, timed only here)
 
 
+def host_info():
+    """CPU model, BLAS threads and numpy version of the CPU baseline's host."""
+    import numpy as np
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((d.get("num_threads") or 0) for d in threadpool_info()) or None
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas_threads": threads, "numpy": np.__version__,
+            "os_cpu_count": os.cpu_count()}
+
+
 def cpu_block_sample(shape, threads=None, reps=1):
     """Seconds for one block fwd+bwd of the oracle at ``shape`` (fp32 numpy)."""
     if threads:
@@ -168,7 +190,8 @@ def run_reference(args):
             "config": {"workload": "48-block Evoformer fwd+bwd, initial shape; CPU sample = 1 block "
                                    "fwd+bwd per step x 48", **SHAPE},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
-                             "sample": "1 Evoformer block fwd+bwd (oracle numpy, fp32) per step, x48"},
+                             "sample": "1 Evoformer block fwd+bwd (oracle numpy, fp32) per step, x48",
+                             **host_info()},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -323,13 +346,16 @@ def run_ours(args):
     if use_graph:
         trainer.capture(n_cycles=1, warmup=max(1, args.warmup))
 
-        def step():
-            trainer.graph.replay()
-            return trainer.graph_loss
+        def step(host=None):
+            return trainer.replay(host)
     else:
         for _ in range(args.warmup):
             eager_step()
-        step = eager_step
+
+        def step(host=None):
+            if host is not None:
+                trainer.feats.copy_from_host(host)
+            return eager_step()
     torch.cuda.synchronize()
     # launches per step: count one eager step
     c0 = _lib.launch_count()
@@ -364,8 +390,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2.record(stream)
     for s in range(args.steps):
-        trainer.feats.copy_from_host(hosts[s % len(hosts)])
-        loss = step()
+        loss = step(hosts[s % len(hosts)])          # one H2D of this step's features, then the step
         losses.append(float(loss.item()))
     e3.record(stream)
     torch.cuda.synchronize()
@@ -432,7 +457,8 @@ def run_ours(args):
             tb = cpu_block_sample(shape, cores)
             cpu_baseline = {"value": 1.0 / (tb * shape["n_blocks"]), "unit": "samples/s",
                             "cores": cores, "kind": "port",
-                            "sample": f"1 Evoformer block fwd+bwd (numpy oracle, fp32) = {tb:.2f} s, x{shape['n_blocks']}"}
+                            "sample": f"1 Evoformer block fwd+bwd (numpy oracle, fp32) = {tb:.2f} s, x{shape['n_blocks']}",
+                            **host_info()}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
@@ -457,6 +483,32 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> int:
+    """``bench.py --gpus N`` without a torchrun environment: launch N ranks of
+    this script (one per GPU, RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* set the way
+    torchrun sets them), forward rank 0's JSON line, return the worst exit
+    code.  NCCL_DEBUG=INFO stays on (rank stderr) so the communicator size
+    can be checked in the logs."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=subprocess.PIPE if r == 0 else subprocess.DEVNULL, text=True))
+    out, _ = procs[0].communicate()
+    rcs = [procs[0].returncode] + [p.wait() for p in procs[1:]]
+    for line in (out or "").splitlines():
+        if line.startswith("{"):
+            print(line, flush=True)
+    return max(rcs, key=abs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -470,6 +522,8 @@ def main():
                     help="N>1: Dynamic Axial Parallelism groups of this size (dp = N / dap) "
                          "instead of the default BP x DP grid")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -281,6 +281,19 @@ int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema,
                       void* p_bf16, int64_t n, const double* sumsq, double clip,
                       float lr, float b1, float omb1, float b2, float omb2, float eps,
                       float bc1, float bc2, float decay, float omdecay, void* stream);
+/* CUDA-graph-safe form of the same step: the step counter t lives on the
+ * device.  evo_sumsq_f64_step also increments *step and writes this step's
+ * bias corrections bc_out = (bc_table[t-1], bc_table[table_len + t-1]) (t
+ * clamped to table_len: the host tabulates np.float32(1 - beta**t) for
+ * t = 1..table_len, src/fusion.py:189-192, until both have rounded to 1.0f);
+ * evo_adam_clip_ema_dev reads them from `bc`.  Replaying a captured step then
+ * advances t exactly as an eager step does. */
+int evo_sumsq_f64_step(const float* g, int64_t n, double* out, void* ws, int64_t* step,
+                       const float* bc_table, int64_t table_len, float* bc_out, void* stream);
+int evo_adam_clip_ema_dev(float* p, const float* g, float* m, float* v, float* ema,
+                          void* p_bf16, int64_t n, const double* sumsq, double clip,
+                          float lr, float b1, float omb1, float b2, float omb2, float eps,
+                          const float* bc, float decay, float omdecay, void* stream);
 
 /* ---- triangle multiplication (extension; AF2 Supplementary Alg. 11/12) -----
  * Absent from the reference (planner inventory only, src/planner.py:37-45).

@@ -86,6 +86,9 @@ SIGNATURES = {
     "evo_gated_residual_bwd": (_i, [_p, _p, _p, _p, _p, _p, _i64, _i64, _i, _p]),
     "evo_sumsq_workspace": (_i64, []),
     "evo_sumsq_f64": (_i, [_p, _i64, _p, _p, _p]),
+    "evo_sumsq_f64_step": (_i, [_p, _i64, _p, _p, _p, _p, _i64, _p, _p]),
+    "evo_adam_clip_ema_dev": (_i, [_p, _p, _p, _p, _p, _p, _i64, _p, _d, _f, _f, _f, _f, _f, _f, _p,
+                                   _f, _f, _p]),
     "evo_adam_clip_ema": (_i, [_p, _p, _p, _p, _p, _p, _i64, _p, _d, _f, _f, _f, _f, _f, _f,
                                _f, _f, _f, _f, _p]),
 }

@@ -359,10 +359,21 @@ void launch_fwd_kb(const void* qkvg, const float* mask, const void* nb, const fl
 
 }  // namespace
 
-// L > 256 (and a tcgen05-capable problem otherwise): the key-blocked kernel
+static bool kb_tc_disabled() {  // EVO_DISABLE_TC=1, as in attention_tc_bwd.cu
+  static const bool v = [] {
+    const char* e = getenv("EVO_DISABLE_TC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+// 256 < L <= 1024 (and a tcgen05-capable problem otherwise): the key-blocked
+// kernel.  The bounds and the EVO_DISABLE_TC switch are the backward's
+// (bwd_supported), so every problem's forward and backward take the same
+// path and form the logits in the same operation order.
 bool attn_fwd_tc_kb_try(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
                         void* gate, void* gated, float* lse, const AttnGeom& g, int dtype, cudaStream_t s) {
-  if (dtype != EVO_BF16 || g.L <= 256) return false;
+  if (kb_tc_disabled() || dtype != EVO_BF16 || g.L <= 256 || g.L > 1024) return false;
   if (!(g.D == 16 || g.D == 32)) return false;
   if ((g.ld % 8) != 0 || (((uintptr_t)qkvg) & 15) != 0) return false;
   if (((uintptr_t)ctx | (uintptr_t)gate | (uintptr_t)gated) & 15) return false;

@@ -41,11 +41,24 @@ __global__ void __launch_bounds__(OPT_THREADS) sumsq_kernel(const float* __restr
   }
 }
 
-__global__ void sumsq_final_kernel(const double* __restrict__ partials, int G, double* out) {
+// Also advances the device step counter and looks up this step's Adam bias
+// corrections bc = (1 - b1^t, 1 - b2^t) in fp32, tabulated on the host with the
+// reference's own expression (src/fusion.py:189-192); past the end of the
+// table both corrections have rounded to exactly 1.0f, so clamping is exact.
+// Keeping t on the device is what lets a captured CUDA graph replay the step.
+__global__ void sumsq_final_kernel(const double* __restrict__ partials, int G, double* out,
+                                   int64_t* __restrict__ step, const float* __restrict__ bc_table,
+                                   int64_t table_len, float* __restrict__ bc_out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < G; ++i) s += partials[i];
     *out = s;
+    if (step) {
+      const int64_t t = ++*step;
+      const int64_t i = (t < table_len ? t : table_len) - 1;
+      bc_out[0] = bc_table[i];
+      bc_out[1] = bc_table[table_len + i];
+    }
   }
 }
 
@@ -69,7 +82,11 @@ __device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, 
 __global__ void __launch_bounds__(OPT_THREADS) adam_clip_ema_kernel(
     float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
     float* __restrict__ v, float* __restrict__ ema, __nv_bfloat16* __restrict__ pb, int64_t n,
-    const double* __restrict__ sumsq, AdamArgs a) {
+    const double* __restrict__ sumsq, AdamArgs a, const float* __restrict__ bc_dev) {
+  if (bc_dev) {  // this step's bias corrections, written by sumsq_final_kernel
+    a.bc1 = bc_dev[0];
+    a.bc2 = bc_dev[1];
+  }
   const double norm = sqrt(*sumsq);
   const bool do_scale = norm > a.clip;
   const float scale = do_scale ? (float)(a.clip / norm) : 1.0f;            // :176-178
@@ -126,16 +143,33 @@ int evo_sumsq_f64(const float* g, int64_t n, double* out, void* ws, void* stream
   if (G > 1024) G = 1024;
   sumsq_kernel<<<G, OPT_THREADS, 0, s>>>(g, n, (double*)ws);
   EVO_LAUNCH_CHECK();
-  sumsq_final_kernel<<<1, 32, 0, s>>>((const double*)ws, G, out);
+  sumsq_final_kernel<<<1, 32, 0, s>>>((const double*)ws, G, out, nullptr, nullptr, 0, nullptr);
   EVO_LAUNCH_CHECK();
   count_launch(2);
   EVO_API_END
 }
 
-int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema, void* p_bf16,
-                      int64_t n, const double* sumsq, double clip, float lr, float b1, float omb1,
-                      float b2, float omb2, float eps, float bc1, float bc2, float decay,
-                      float omdecay, void* stream) {
+int evo_sumsq_f64_step(const float* g, int64_t n, double* out, void* ws, int64_t* step,
+                       const float* bc_table, int64_t table_len, float* bc_out, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(((uintptr_t)g & 15) == 0, EVO_ERR_ARG, "sumsq: grad region must be 16-B aligned");
+  EVO_REQUIRE(step && bc_table && bc_out && table_len >= 1, EVO_ERR_ARG, "sumsq_step: bad step arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int G = num_sms() * 4;
+  if (G > 1024) G = 1024;
+  sumsq_kernel<<<G, OPT_THREADS, 0, s>>>(g, n, (double*)ws);
+  EVO_LAUNCH_CHECK();
+  sumsq_final_kernel<<<1, 32, 0, s>>>((const double*)ws, G, out, step, bc_table, table_len, bc_out);
+  EVO_LAUNCH_CHECK();
+  count_launch(2);
+  EVO_API_END
+}
+
+namespace {
+int adam_launch(float* p, const float* g, float* m, float* v, float* ema, void* p_bf16, int64_t n,
+                const double* sumsq, double clip, float lr, float b1, float omb1, float b2, float omb2,
+                float eps, float bc1, float bc2, const float* bc_dev, float decay, float omdecay,
+                void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE((((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v | (uintptr_t)ema) & 15) == 0,
               EVO_ERR_ARG, "adam: regions must be 16-B aligned");
@@ -145,10 +179,31 @@ int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema, 
   int64_t cap = (int64_t)num_sms() * 8;
   unsigned G = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
   adam_clip_ema_kernel<<<G, OPT_THREADS, 0, (cudaStream_t)stream>>>(
-      p, g, m, v, ema, (__nv_bfloat16*)p_bf16, n, sumsq, a);
+      p, g, m, v, ema, (__nv_bfloat16*)p_bf16, n, sumsq, a, bc_dev);
   EVO_LAUNCH_CHECK();
   count_launch(1);
   EVO_API_END
+}
+}  // namespace
+
+int evo_adam_clip_ema(float* p, const float* g, float* m, float* v, float* ema, void* p_bf16,
+                      int64_t n, const double* sumsq, double clip, float lr, float b1, float omb1,
+                      float b2, float omb2, float eps, float bc1, float bc2, float decay,
+                      float omdecay, void* stream) {
+  return adam_launch(p, g, m, v, ema, p_bf16, n, sumsq, clip, lr, b1, omb1, b2, omb2, eps, bc1, bc2, nullptr,
+                     decay, omdecay, stream);
+}
+
+int evo_adam_clip_ema_dev(float* p, const float* g, float* m, float* v, float* ema, void* p_bf16,
+                          int64_t n, const double* sumsq, double clip, float lr, float b1, float omb1,
+                          float b2, float omb2, float eps, const float* bc, float decay, float omdecay,
+                          void* stream) {
+  if (!bc) {
+    set_error("adam_dev: null bias-correction pointer");
+    return EVO_ERR_ARG;
+  }
+  return adam_launch(p, g, m, v, ema, p_bf16, n, sumsq, clip, lr, b1, omb1, b2, omb2, eps, 1.0f, 1.0f, bc,
+                     decay, omdecay, stream);
 }
 
 }  // extern "C"

@@ -56,6 +56,23 @@ def build_layout(named_shapes, align: int = ALIGN) -> list:
     return slots
 
 
+def bias_correction_table(o: OptimConfig, max_len: int = 1 << 22) -> np.ndarray:
+    """[2, T] fp32: np.float32(1 - beta**t) for t = 1..T (src/fusion.py:189-192),
+    T the first step at which both corrections have rounded to exactly 1.0f
+    (so the device's clamp at T is exact for every later step)."""
+    rows = ([], [])
+    t = 1
+    while t <= max_len:
+        b1 = np.float32(1.0 - o.beta1 ** t)
+        b2 = np.float32(1.0 - o.beta2 ** t)
+        rows[0].append(b1)
+        rows[1].append(b2)
+        if b1 == np.float32(1.0) and b2 == np.float32(1.0):
+            break
+        t += 1
+    return np.array(rows, np.float32)
+
+
 def layout_total_bytes(slots) -> int:
     return slots[-1].offset + slots[-1].padded_bytes if slots else 0
 
@@ -106,6 +123,12 @@ class FusionEngine:
             self.shadow = torch.empty(self.n_total, dtype=shadow_dtype, device=self.device)
             ops.cast(self.regions["params"], self.shadow)
         self.sumsq = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # Adam's step counter t on the device (advanced by the sumsq kernel), so
+        # a CUDA graph that captured step() replays with the right t; the
+        # bias corrections are tabulated once with the reference's expression
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.bc_table = torch.from_numpy(bias_correction_table(self.optim)).to(self.device)
+        self.bc = torch.ones(2, dtype=torch.float32, device=self.device)
         self._views = {}
 
     # -- storage access --------------------------------------------------------
@@ -165,23 +188,34 @@ class FusionEngine:
 
     def step(self):
         """clip + Adam + EMA over the pooled regions; returns the fp64
-        sum-of-squares of the pre-clip gradient as a device tensor."""
+        sum-of-squares of the pre-clip gradient as a device tensor.  The step
+        counter advances on the device (``step_dev``), so this sequence can be
+        captured in a CUDA graph; ``note_replayed_step`` keeps the host count."""
         o = self.optim
         self.step_count += 1
-        t = self.step_count
         f32 = np.float32
-        ops.sumsq_f64(self.regions["grads"], self.sumsq)
+        ops.sumsq_f64_step(self.regions["grads"], self.sumsq, self.step_dev, self.bc_table, self.bc)
         self.launches.hit("grad_clip", 2)
         r = self.regions
-        ops.adam_clip_ema(r["params"], r["grads"], r["adam_m"], r["adam_v"], r["ema"], self.shadow,
-                          self.sumsq, float(o.clip_norm), float(f32(o.lr)), float(f32(o.beta1)),
-                          float(f32(1 - o.beta1)), float(f32(o.beta2)), float(f32(1 - o.beta2)),
-                          float(f32(o.eps)), float(f32(1.0 - o.beta1 ** t)),
-                          float(f32(1.0 - o.beta2 ** t)), float(f32(o.ema_decay)),
-                          float(f32(1.0) - f32(o.ema_decay)))
+        ops.adam_clip_ema_dev(r["params"], r["grads"], r["adam_m"], r["adam_v"], r["ema"], self.shadow,
+                              self.sumsq, float(o.clip_norm), float(f32(o.lr)), float(f32(o.beta1)),
+                              float(f32(1 - o.beta1)), float(f32(o.beta2)), float(f32(1 - o.beta2)),
+                              float(f32(o.eps)), self.bc, float(f32(o.ema_decay)),
+                              float(f32(1.0) - f32(o.ema_decay)))
         self.launches.hit("opt_update", 1)
         self.launches.hit("ema", 1)
         return self.sumsq
+
+    def note_replayed_step(self):
+        """A captured step() was replayed: advance the host-side counters the
+        way step() itself would have."""
+        self.step_count += 1
+        self.launches.hit("grad_clip", 2)
+        self.launches.hit("opt_update", 1)
+        self.launches.hit("ema", 1)
+
+    def device_step_count(self) -> int:
+        return int(self.step_dev.item())
 
     def apply(self, grads: dict = None, reducer=None, sync: bool = True):
         """Full optimizer tail (src/fusion.py:226-233); returns the pre-clip

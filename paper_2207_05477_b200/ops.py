@@ -453,3 +453,14 @@ def adam_clip_ema(p, g, m, v, ema, p_bf16, sumsq, clip, lr, b1, omb1, b2, omb2, 
                   decay, omdecay):
     call("evo_adam_clip_ema", ptr(p), ptr(g), ptr(m), ptr(v), ptr(ema), ptr(p_bf16), p.numel(),
          ptr(sumsq), clip, lr, b1, omb1, b2, omb2, eps, bc1, bc2, decay, omdecay, stream())
+
+
+def sumsq_f64_step(g, out, step, bc_table, bc_out):
+    ws = _ws(_lib.load().evo_sumsq_workspace(), g.device)
+    call("evo_sumsq_f64_step", ptr(g), g.numel(), ptr(out), ptr(ws), ptr(step), ptr(bc_table),
+         bc_table.shape[1], ptr(bc_out), stream())
+
+
+def adam_clip_ema_dev(p, g, m, v, ema, p_bf16, sumsq, clip, lr, b1, omb1, b2, omb2, eps, bc, decay, omdecay):
+    call("evo_adam_clip_ema_dev", ptr(p), ptr(g), ptr(m), ptr(v), ptr(ema), ptr(p_bf16), p.numel(),
+         ptr(sumsq), clip, lr, b1, omb1, b2, omb2, eps, ptr(bc), decay, omdecay, stream())

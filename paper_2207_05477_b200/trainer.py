@@ -120,10 +120,12 @@ class Trainer:
         feats = feats or make_features(self.cfg, step_feature_seed(self.plan.seed, step))
         self.host.fill(feats)
 
-    def device_step(self, n_cycles: int):
-        """H2D of the staged features, fwd+bwd, optimizer; returns the
-        device loss tensor (no host sync)."""
-        self.feats.copy_from_host(self.host)
+    def device_step(self, n_cycles: int, h2d: bool = True):
+        """H2D of the staged features (unless ``h2d`` is False: the features
+        already in HBM are used), fwd+bwd, optimizer; returns the device loss
+        tensor (no host sync)."""
+        if h2d:
+            self.feats.copy_from_host(self.host)
         loss, _ = self.engine.forward_backward(self.feats, n_cycles,
                                                recompute=self.plan.recompute_on)
         self.store.grad_sync(None)
@@ -131,18 +133,33 @@ class Trainer:
         return loss
 
     def capture(self, n_cycles: int = 1, warmup: int = 2):
-        """Capture ``device_step`` into a CUDA graph (after eager warm-up)."""
+        """Capture the device part of ``device_step`` (fwd+bwd+optimizer on the
+        features resident in ``self.feats``) into a CUDA graph, after eager
+        warm-up.  ``replay(host)`` copies a step's features in first."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(warmup):
-                self.device_step(n_cycles)
+                self.device_step(n_cycles, h2d=False)
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
+        count = self.store.step_count
         with torch.cuda.graph(g):
-            self.graph_loss = self.device_step(n_cycles)
+            self.graph_loss = self.device_step(n_cycles, h2d=False)
+        self.store.step_count = count     # capture records the step, it does not run it
         self.graph = g
         return g
+
+    def replay(self, host: "PinnedFeatures" = None):
+        """One captured device step; with ``host`` (pinned features) their H2D
+        copy is enqueued first, else the features already in HBM are used.
+        Returns the device loss tensor.  Adam's step counter advances on the
+        device, so replayed steps equal eager ones."""
+        if host is not None:
+            self.feats.copy_from_host(host)
+        self.graph.replay()
+        self.store.note_replayed_step()
+        return self.graph_loss
 
     def train_step(self, step: int):
         """src/trainer.py:192-247 (serial): returns (loss, metrics).  Metric keys

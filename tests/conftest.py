@@ -10,6 +10,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# deterministic algorithm choice for any library GEMM path in every (spawned)
+# test process: no timing-dependent selection (inherited by mp.spawn workers)
+os.environ.setdefault("EVO_GEMM_TUNE", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
@@ -32,3 +36,24 @@ def rel_err(a, b, floor=0.0):
 @pytest.fixture
 def golden():
     return load_golden
+
+
+def slot_errs(store, flat, ref, floor_frac):
+    """Per-parameter floored errors of a flat pooled grad region against
+    ``ref`` (another flat region with the same layout, or a name -> array dict
+    such as the oracle's grads): err(t) = max|a-b| / max(max|a|, max|b|,
+    floor_frac * G), G = max|ref| over all parameters.
+    A wrong, missing or double-counted small-magnitude slot cannot hide behind
+    the largest gradient of the region."""
+    flat = np.asarray(flat)
+    views = {}
+    for s in store.slots:
+        n = int(np.prod(s.shape, dtype=np.int64)) if s.shape else 1
+        lo = s.offset // 4
+        views[s.name] = (lo, n, s.shape)
+    if isinstance(ref, dict):
+        refs = {k: np.asarray(ref[k]).ravel() for k in views}
+    else:
+        refs = {k: np.asarray(ref)[lo:lo + n] for k, (lo, n, _) in views.items()}
+    G = max(float(np.abs(r).max(initial=0.0)) for r in refs.values())
+    return {k: rel_err(flat[lo:lo + n], refs[k], floor_frac * G) for k, (lo, n, _) in views.items()}

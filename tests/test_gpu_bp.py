@@ -13,7 +13,7 @@ import tempfile
 import numpy as np
 import pytest
 
-from conftest import rel_err
+from conftest import slot_errs
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -81,7 +81,19 @@ def test_bp_matches_unsharded(world, dtype):
     res = _run(world, dtype)
     tol = 1e-4 if dtype == "f32" else 3e-2
     assert abs(float(res["loss"][0]) - base_loss) <= tol * abs(base_loss)
-    assert rel_err(res["grads"], base_g, np.abs(base_g).max()) <= (tol if dtype == "f32" else 5e-2)
+    # per parameter, floored: a BP-pair gradient summed on both ranks or a
+    # branch slot never synced would show here
+    errs = slot_errs(st, res["grads"], base_g, 1e-6 if dtype == "f32" else 1e-3)
+    worst = max(errs, key=errs.get)
+    assert errs[worst] <= (tol if dtype == "f32" else 5e-2), (worst, errs[worst])
+    if dtype == "f32":  # and against the CPU oracle itself, not only the unsharded engine
+        from oracle import evoformer_np as O
+        ocfg = O.ModelConfig(**CFG)
+        oloss, ograds, _ = O.serial_grads(ocfg, O.init_params(ocfg, 7), O.make_features(ocfg, 3))
+        assert abs(float(res["loss"][0]) - oloss) <= 1e-4 * abs(oloss)
+        errs = slot_errs(st, res["grads"], ograds, 1e-6)
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= 1e-4, (worst, errs[worst])
     block = [r for r in map(tuple, res["recs"]) if r[0] in ("opm", "msa_stack", "pair_stack")]
     assert len(block) == 4 * CFG["n_blocks"]
     assert sum(1 for r in block if r[1] == "broadcast") == 3 * CFG["n_blocks"]
