@@ -66,41 +66,34 @@ size_t evo_defer_used(void);
  * src/model.py:314,346-347,363-364,378.  Row-major, batched-strided:
  *   C_b[M,N] = alpha * op(A_b)[M,K] . op(B_b)[K,N] + beta * C_b
  * ab_dtype: EVO_F32 (true fp32, no TF32) or EVO_BF16; c_dtype: F32 or BF16.
- * Routed to the hand-written tcgen05 GEMM when the shape is supported,
- * else cuBLAS (plain library GEMM). */
+ * bf16 operands run on the library's tcgen05 + TMA GEMM (gemm_tc.cu:
+ * persistent, warp-specialised, split-K with a deterministic reduction for
+ * long K); fp32 operands (the parity mode: true fp32, no TF32) and operands
+ * TMA cannot address (16-B alignment of base and row pitch) run on the
+ * library's CUDA-core GEMM (gemm_simt.cu).  No CUDA math library is used. */
 int evo_gemm(int64_t M, int64_t N, int64_t K,
              const void* A, int64_t lda, int trans_a, int64_t stride_a,
              const void* B, int64_t ldb, int trans_b, int64_t stride_b,
              void* C, int64_t ldc, int64_t stride_c, int batch,
              float alpha, float beta, int ab_dtype, int c_dtype, void* stream);
 
+/* Number of evo_gemm / evo_gemm_bias calls that ran on the tensor cores
+ * (process-wide; instrumentation for tests and the bench). */
+int64_t evo_gemm_tc_launches(void);
+
 /* Projection with its module epilogue fused (replaces the np.matmul + bias +
  * residual of src/attention.py:173 / src/model.py:346-348, 378 and the
  * matmul + bias + relu of src/model.py:346):
  *   out[M,N] = op(A) . op(B) + bias[N] (+ res[M,N])      relu == 0
  *   out[M,N] = relu(op(A) . op(B) + bias[N])              relu == 1, res == NULL
- * res may alias nothing else; res_dtype is its storage dtype.  bias_bf16 (nullable):
- * a bf16 copy of bias (the parameter store's shadow) used by bf16 fused epilogues. */
+ * res: contiguous [M, N] (ld = N), alias of nothing else; res_dtype its storage
+ * dtype.  The epilogue runs in fp32 on the accumulator (fp32 bias) before the
+ * single rounding to c_dtype.  bias_bf16 is accepted for ABI compatibility and
+ * ignored. */
 int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
                   const void* B, int64_t ldb, int trans_b, const void* res, int res_dtype,
                   const float* bias, const void* bias_bf16, int relu, void* out, int64_t ldo,
                   int ab_dtype, int c_dtype, void* stream);
-
-/* Projection with a training epilogue, for the transition's ReLU and the
- * bias gradients (replaces the np.maximum / np.sum steps of src/model.py:346
- * and their tape backward):
- *   epi 3  D = relu(op(A).op(B) + vec[N]); aux <- ReLU bit mask (aux_ld bits/row, %128)
- *   epi 4  D = op(A).op(B) * relu'(aux)                    (dReLU with that mask)
- *   epi 5  D = op(A).op(B) + beta*D; vec[N] (+)= ... column sums of op(B)  (fp32 D)
- *   epi 6  as 5 with the row sums of op(A) (length M)
- * Returns EVO_ERR_UNSUPPORTED when no fused kernel exists for the problem; the
- * caller then runs the unfused sequence.  (Measured on B200, tools/epi_time.py:
- * the library's dReLU / bias-gradient epilogues are 2-4x slower than the
- * unfused GEMM + relu_bwd_colsum, so the engine does not route through them.) */
-int evo_gemm_epilogue(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a,
-                      const void* B, int64_t ldb, int trans_b, void* D, int64_t ldd, float beta,
-                      int epi, float* vec, void* aux, int64_t aux_ld, int ab_dtype, int c_dtype,
-                      void* stream);
 
 /* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
  * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */

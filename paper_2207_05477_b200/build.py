@@ -5,7 +5,8 @@
 Each ``csrc/*.cu`` is compiled to an object under ``build/`` (in parallel,
 skipped when up to date), then linked into
 ``paper_2207_05477_b200/libevoformer_sm100.so`` against the static CUDA
-runtime and cuBLAS.  The shared object travels to the GPU box with the repo
+runtime only (no CUDA libraries: every kernel is the library's own; TMA
+descriptors are encoded through the driver entry point).  The shared object travels to the GPU box with the repo
 snapshot (it is git-ignored, not gpurun-ignored).
 """
 
@@ -58,9 +59,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     objs = [o for o, _ in results]
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static",
-               "-L/usr/local/cuda/lib64", "-lcublas", "-lcublasLt",
-               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n$ {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

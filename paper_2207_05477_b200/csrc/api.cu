@@ -1,6 +1,5 @@
-// Library plumbing, dense projections (GEMM routing) and elementwise glue.
-#include <cublas_v2.h>
-
+// Library plumbing, dense projections (GEMM routing: gemm_tc.cu / gemm_simt.cu) and
+// elementwise glue.
 #include <mutex>
 #include <string>
 
@@ -28,15 +27,12 @@ static __global__ void __launch_bounds__(256) finalize_batch_kernel(const __grid
 }
 
 // ---------------------------------------------------------------------------
-// cuBLAS handle per (thread, device); a fixed workspace so the handle is
-// usable inside CUDA-graph capture.
-
-// Streams map to one of EVO_STREAM_SLOTS slots; every per-stream scratch
-// (cuBLAS handle + workspace, cuBLASLt workspace, epilogue bias copy) is
-// indexed by slot, so kernels on concurrently running streams (the two branch
-// streams of the engine) never share a workspace.  Slots are assigned on first
-// sight and their buffers allocated when a slot's owner first needs them --
-// before CUDA-graph capture, since the eager warm-up step touches every stream.
+// Streams map to one of EVO_STREAM_SLOTS slots; per-stream scratch (the
+// tensor-core GEMM's split-K workspace) is indexed by slot, so kernels on
+// concurrently running streams (the two branch streams of the engine) never
+// share a workspace.  Slots are assigned on first sight; the workspaces are
+// allocated on the first GEMM, before CUDA-graph capture (the eager warm-up
+// step touches every stream).
 int stream_slot(cudaStream_t s) {
   static thread_local cudaStream_t seen[EVO_STREAM_SLOTS] = {};
   static thread_local int n = 0;
@@ -49,36 +45,6 @@ int stream_slot(cudaStream_t s) {
   return (int)(((uintptr_t)s >> 4) % EVO_STREAM_SLOTS);
 }
 
-struct BlasState {
-  cublasHandle_t h = nullptr;
-  void* ws = nullptr;
-};
-
-static cublasHandle_t blas_handle(cudaStream_t s) {
-  static thread_local BlasState st[16][EVO_STREAM_SLOTS];
-  int dev = 0;
-  EVO_CUDA(cudaGetDevice(&dev));
-  if (!st[dev & 15][0].h) {  // every slot at once (no allocation inside graph capture)
-    for (int k = 0; k < EVO_STREAM_SLOTS; ++k) {
-      BlasState& b = st[dev & 15][k];
-      if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) throw Error(EVO_ERR_CUDA, "cublasCreate failed");
-      const size_t ws = size_t(32) << 20;
-      EVO_CUDA(cudaMalloc(&b.ws, ws));
-      cublasSetWorkspace(b.h, b.ws, ws);
-      cublasSetMathMode(b.h, CUBLAS_DEFAULT_MATH);  // never TF32
-    }
-  }
-  BlasState& b = st[dev & 15][stream_slot(s)];
-  cublasSetStream(b.h, s);
-  return b.h;
-}
-
-static cudaDataType_t cuda_dt(int d) {
-  if (d == EVO_F32) return CUDA_R_32F;
-  if (d == EVO_BF16) return CUDA_R_16BF;
-  throw Error(EVO_ERR_ARG, "bad dtype code");
-}
-
 // vectorised glue (glue.cu); return false -> scalar kernels below
 int64_t colsum_vec_ws(int64_t C);
 bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, float* out,
@@ -89,11 +55,30 @@ bool bias_relu_vec(void* y, int dt, const float* bias, int64_t rows, int64_t C, 
 void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const int64_t* N, int n,
                int sdt, int ddt, int unpack, cudaStream_t s, int ns);
 
-// tcgen05 GEMM (gemm_tc.cu); returns false if the shape is not covered.
-bool gemm_lt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
-             int64_t ldb, int tb, int64_t sb, const void* Cin, void* D, int64_t ldc, int64_t sc, int batch,
-             float alpha, float beta, int ab_dtype, int c_dtype, int epi, const float* bias, cudaStream_t s,
-             void* aux = nullptr, int64_t aux_ld = 0, const void* bias16 = nullptr);
+// tcgen05 + TMA GEMM (gemm_tc.cu): false when TMA cannot address an operand.
+bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
+             int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha,
+             float beta, const void* Cin, int64_t ldc, const float* bias, int relu, int d_dtype, cudaStream_t s);
+// CUDA-core GEMM (gemm_simt.cu): the fp32 parity path and odd layouts.
+void gemm_simt(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
+               int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha, float beta,
+               const void* Cin, int c_dtype, int64_t ldc, int64_t sc, const float* bias, int relu, int ab_dtype,
+               int d_dtype, cudaStream_t s);
+
+// One GEMM with an optional fused epilogue, routed to the tensor cores when the
+// operands are bf16 and TMA-addressable, else to the CUDA-core kernel.
+static void gemm_route(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
+                       const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
+                       float alpha, float beta, const void* Cin, int c_dtype, int64_t ldc, int64_t sc,
+                       const float* bias, int relu, int ab_dtype, int d_dtype, cudaStream_t s) {
+  const bool res_ok = Cin == nullptr || beta == 0.f || (c_dtype == d_dtype && (batch == 1 || sc == sd));
+  if (ab_dtype == EVO_BF16 && res_ok &&
+      gemm_tc(M, N, K, A, lda, ta, sa, B, ldb, tb, sb, D, ldd, sd, batch, alpha, beta, Cin, ldc, bias, relu, d_dtype,
+              s))
+    return;
+  gemm_simt(M, N, K, A, lda, ta, sa, B, ldb, tb, sb, D, ldd, sd, batch, alpha, beta, Cin, c_dtype, ldc, sc, bias,
+            relu, ab_dtype, d_dtype, s);
+}
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
                  int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
@@ -267,42 +252,11 @@ int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int tr
              int ab_dtype, int c_dtype, void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0 && batch >= 1, EVO_ERR_ARG, "gemm: bad extents");
+  EVO_REQUIRE((ab_dtype == EVO_F32 || ab_dtype == EVO_BF16) && (c_dtype == EVO_F32 || c_dtype == EVO_BF16),
+              EVO_ERR_ARG, "gemm: bad dtype code");
   if (M == 0 || N == 0) return EVO_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (gemm_tc_try(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, ldc, stride_c,
-                  batch, alpha, beta, ab_dtype, c_dtype, s))
-    return EVO_OK;
-  if (gemm_lt(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, C, ldc, stride_c, batch,
-              alpha, beta, ab_dtype, c_dtype, 0, nullptr, s))
-    return EVO_OK;
-  cublasHandle_t h = blas_handle(s);
-  // row-major C = op(A) op(B)  <=>  column-major C^T = op(B)^T op(A)^T
-  cublasOperation_t ob = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
-  cublasOperation_t oa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
-  cublasStatus_t st;
-  if (batch == 1)
-    st = cublasGemmEx(h, ob, oa, (int)N, (int)M, (int)K, &alpha, B, cuda_dt(ab_dtype), (int)ldb, A,
-                      cuda_dt(ab_dtype), (int)lda, &beta, C, cuda_dt(c_dtype), (int)ldc,
-                      CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-  else
-    st = cublasGemmStridedBatchedEx(h, ob, oa, (int)N, (int)M, (int)K, &alpha, B, cuda_dt(ab_dtype),
-                                    (int)ldb, stride_b, A, cuda_dt(ab_dtype), (int)lda, stride_a,
-                                    &beta, C, cuda_dt(c_dtype), (int)ldc, stride_c, batch,
-                                    CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-  EVO_REQUIRE(st == CUBLAS_STATUS_SUCCESS, EVO_ERR_CUDA,
-              "cublasGemmEx failed with status " + std::to_string((int)st));
-  EVO_API_END
-}
-
-int evo_gemm_epilogue(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
-                      int64_t ldb, int trans_b, void* D, int64_t ldd, float beta, int epi, float* vec, void* aux,
-                      int64_t aux_ld, int ab_dtype, int c_dtype, void* stream) {
-  EVO_API_BEGIN
-  EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0 && epi >= 3 && epi <= 6, EVO_ERR_ARG, "gemm_epilogue: bad arguments");
-  if (M == 0 || N == 0) return EVO_OK;
-  if (!gemm_lt(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, D, D, ldd, 0, 1, 1.0f, beta, ab_dtype, c_dtype,
-               epi, vec, (cudaStream_t)stream, aux, aux_ld))
-    return EVO_ERR_UNSUPPORTED;
+  gemm_route(M, N, K, A, lda, trans_a, stride_a, B, ldb, trans_b, stride_b, C, ldc, stride_c, batch, alpha, beta,
+             beta != 0.f ? C : nullptr, c_dtype, ldc, stride_c, nullptr, 0, ab_dtype, c_dtype, (cudaStream_t)stream);
   EVO_API_END
 }
 
@@ -311,34 +265,14 @@ int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
                   const void* bias_bf16, int relu, void* out, int64_t ldo, int ab_dtype, int c_dtype,
                   void* stream) {
   EVO_API_BEGIN
+  (void)bias_bf16;  // the fused epilogues add the fp32 bias
   EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0, EVO_ERR_ARG, "gemm_bias: bad extents");
   EVO_REQUIRE(!(relu && res), EVO_ERR_ARG, "gemm_bias: relu with a residual is not a module of the path");
+  EVO_REQUIRE(bias != nullptr, EVO_ERR_ARG, "gemm_bias: null bias");
   if (M == 0 || N == 0) return EVO_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool fuse_res = res != nullptr && res_dtype == c_dtype;
-  if (gemm_lt(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, fuse_res ? res : out, out, ldo, 0, 1, 1.0f,
-              fuse_res ? 1.0f : 0.0f, ab_dtype, c_dtype, relu ? 2 : 1, bias, s, nullptr, 0, bias_bf16)) {
-    if (res && !fuse_res) {  // residual of another dtype: add it after the fused bias
-      EVO_REQUIRE(ldo == N, EVO_ERR_ARG, "gemm_bias: strided output with a mixed-dtype residual");
-      static float* zero = nullptr;
-      static int64_t zn = 0;
-      if (zn < N) {
-        if (zero) EVO_CUDA(cudaFree(zero));
-        EVO_CUDA(cudaMalloc(&zero, N * sizeof(float)));
-        EVO_CUDA(cudaMemset(zero, 0, N * sizeof(float)));
-        zn = N;
-      }
-      return evo_bias_residual(res, res_dtype, out, c_dtype, zero, out, c_dtype, M, N, stream);
-    }
-    return EVO_OK;
-  }
-  // library fallback: plain GEMM, then the glue kernel
-  const int rc = evo_gemm(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, out, ldo, 0, 1, 1.0f, 0.0f, ab_dtype,
-                          c_dtype, stream);
-  if (rc != EVO_OK) return rc;
-  EVO_REQUIRE(ldo == N, EVO_ERR_ARG, "gemm_bias: strided output needs the fused path");
-  if (relu) return evo_bias_relu(out, c_dtype, bias, M, N, stream);
-  return evo_bias_residual(res, res ? res_dtype : EVO_F32, out, c_dtype, bias, out, c_dtype, M, N, stream);
+  // residual rows are contiguous [M, N] (ld = N), the output may be strided
+  gemm_route(M, N, K, A, lda, trans_a, 0, B, ldb, trans_b, 0, out, ldo, 0, 1, 1.0f, res ? 1.0f : 0.0f, res,
+             res_dtype, N, 0, bias, relu, ab_dtype, c_dtype, (cudaStream_t)stream);
   EVO_API_END
 }
 

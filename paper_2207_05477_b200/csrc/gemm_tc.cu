@@ -1,0 +1,552 @@
+// Dense projections on the 5th-generation tensor cores: a persistent,
+// warp-specialised tcgen05 GEMM fed by TMA, with the module epilogues fused.
+//
+//   D[b] = act(alpha * op(A[b]) op(B[b]) + bias) + beta * C[b]      (row-major)
+//
+// These are the Evoformer's projections (src/attention.py:133-173 merged
+// Q|K|V|gate and output projections; src/model.py:344-348 transition W1/W2;
+// src/model.py:361-378 OPM projections and w_out) and their data / weight
+// gradients, plus TriangleMultiplication's channel-batched contractions.
+//
+// Structure (one CTA per SM, 6 warps):
+//   warp 0      TMA producer: A and B k-blocks (BK = 64 bf16 = one 128-byte
+//               swizzle row) into a STAGES-deep shared-memory ring
+//               (mbarrier full/empty pairs, transaction-count completion);
+//   warp 1      allocates TMEM and issues tcgen05.mma (M = 128, N = BN,
+//               K = 16) from one elected lane into one of two TMEM
+//               accumulators, committing each stage back to the producer;
+//   warps 2..5  epilogue: tcgen05.ld of the accumulator (lane quarter =
+//               warp % 4), alpha / bias / ReLU / residual (beta * C, the
+//               residual tile itself fetched by TMA), conversion, and a TMA
+//               store through a swizzled, double-buffered staging tile.
+// Operands may be K-major or MN-major in HBM (the weight-gradient GEMMs read
+// activations transposed): both are staged with 128-byte swizzling and
+// described to the tensor core accordingly, so no transpose pass exists.
+// Tiles are walked persistently (tile = blockIdx.x + i * gridDim.x); the
+// double-buffered accumulator lets tile i+1's MMAs run under tile i's
+// epilogue.  Problems with few output tiles and a long K (weight gradients:
+// K = tokens) are split along K; the partial tiles go to a per-stream fp32
+// workspace and one reduction kernel sums them in a fixed order (results are
+// deterministic) and applies the epilogue.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "reduce.cuh"
+#include "tc_common.cuh"
+
+namespace evo {
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int BM = 128, BK = 64;
+constexpr int GT_THREADS = 192;
+constexpr int EPI_WARPS = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int STG_BYTES = 32 * 128;   // one staging tile: 32 rows x 128 B
+
+template <int BN>
+struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int OFF_STG = STAGES * STAGE;
+  static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * 2 * STG_BYTES;
+  static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // +1 KB: runtime 1024-B alignment
+  static constexpr int TMEM_COLS = 2 * BN;                      // two accumulators (128/256/512)
+};
+
+struct Params {
+  int M, N, K;
+  int batch, n_mt, n_nt, kblocks, kb_per_split;
+  int tiles;
+  int a_mn, b_mn;
+  int has_res, relu, partial;
+  float alpha, beta;
+  const float* bias;
+};
+
+// --- TMA / bulk-async helpers -------------------------------------------------
+
+__device__ __forceinline__ void tma_load3(const CUtensorMap* m, void* dst, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Operand tile of `rows` MN-rows x 64 K in shared memory, as TMA wrote it:
+//  K-major : row r (128 B = 64 k) at r*128, 8-row swizzle atoms of 1 KB
+//            (SBO = 1 KB); a K = 16 step advances 32 B inside the row.
+//  MN-major: atom a (64 MN elements = 128 B) x 64 k-rows at a*8 KB (LBO),
+//            8-k-row groups of 1 KB (SBO); a K = 16 step advances 2 KB.
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int mn_major, int ks) {
+  return mn_major ? sdesc_sw128(base + ks * 2048, 8192, 1024) : sdesc_sw128(base + ks * 32, 16, 1024);
+}
+
+struct TileCoord {
+  int b, m0, n0, kb0, kb1, split;
+};
+
+__device__ __forceinline__ TileCoord decode(const Params& p, int t) {
+  const int per_split = p.batch * p.n_mt * p.n_nt;
+  TileCoord c;
+  c.split = t / per_split;
+  int r = t - c.split * per_split;
+  c.b = r / (p.n_mt * p.n_nt);
+  r -= c.b * p.n_mt * p.n_nt;
+  c.m0 = (r / p.n_nt) * BM;
+  c.n0 = (r % p.n_nt);
+  c.kb0 = c.split * p.kb_per_split;
+  c.kb1 = min(p.kblocks, c.kb0 + p.kb_per_split);
+  return c;
+}
+
+template <int BN, bool OUT_F32>
+__global__ void __launch_bounds__(GT_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmC, Params p) {
+  using F = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + F::OFF_BAR);
+  uint64_t* empty = full + F::STAGES;
+  uint64_t* tfull = empty + F::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rbar = tempty + 2;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(rbar + EPI_WARPS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmD);
+    if (p.has_res) prefetch_tmap(&tmC);
+    for (int s = 0; s < F::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], EPI_WARPS);
+    }
+    for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
+  }
+  if (warp == 1) tc::tmem_alloc<F::TMEM_COLS>(slot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        const TileCoord c = decode(p, t);
+        const int n0 = c.n0 * BN;
+        for (int kb = c.kb0; kb < c.kb1; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          expect_tx(&full[stage], F::STAGE);
+          uint8_t* sa = smem + stage * F::STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          const int k0 = kb * BK;
+          if (!p.a_mn) {
+            tma_load3(&tmA, sa, &full[stage], k0, c.m0, c.b);
+          } else {
+            tma_load3(&tmA, sa, &full[stage], c.m0, k0, c.b);
+            tma_load3(&tmA, sa + 8192, &full[stage], c.m0 + 64, k0, c.b);
+          }
+          if (!p.b_mn) {
+            tma_load3(&tmB, sb, &full[stage], k0, n0, c.b);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) tma_load3(&tmB, sb + i * 8192, &full[stage], n0 + 64 * i, k0, c.b);
+          }
+          if (++stage == F::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one elected lane) ----------------
+    const uint32_t idesc = tc::idesc_bf16(BM, BN, p.a_mn != 0, p.b_mn != 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
+      const TileCoord c = decode(p, t);
+      const int acc = it & 1;
+      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
+      tc::fence_after();
+      const uint32_t dacc = tmem + (uint32_t)(acc * BN);
+      for (int kb = c.kb0; kb < c.kb1; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::fence_after();
+        const uint32_t sa = tc::smem_u32(smem + stage * F::STAGE);
+        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks)
+          tc::mma_bf16_ss_w(dacc, op_desc(sa, p.a_mn, ks), op_desc(sb, p.b_mn, ks), idesc,
+                            (kb > c.kb0 || ks > 0) ? 1u : 0u);
+        tc::mma_commit_w(&empty[stage]);  // the stage is free once these MMAs have read it
+        if (++stage == F::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      tc::mma_commit_w(&tfull[acc]);  // accumulator complete
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    constexpr int CW = OUT_F32 ? 32 : 64;  // columns per 128-byte staging row
+    const int ew = warp - 2;
+    const int quarter = warp & 3;  // TMEM lanes this warp may access
+    uint8_t* stg = smem + F::OFF_STG + ew * 2 * STG_BYTES;
+    int buf = 0;
+    uint32_t rphase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
+      const TileCoord c = decode(p, t);
+      const int acc = it & 1;
+      const int n0 = c.n0 * BN;
+      const int row0 = c.m0 + quarter * 32;
+      const int zout = p.partial ? c.split : c.b;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::fence_after();
+      const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += CW) {
+        if (n0 + cc >= p.N) break;
+        uint8_t* sbuf = stg + buf * STG_BYTES;
+        if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done
+        __syncwarp();
+        if (p.has_res && lane == 0) {
+          expect_tx(&rbar[ew], STG_BYTES);
+          tma_load3(&tmC, sbuf, &rbar[ew], n0 + cc, row0, c.b);
+        }
+        float v[CW];
+        tc::tmem_ld32(tacc + cc, *reinterpret_cast<float(*)[32]>(&v[0]));
+        if constexpr (CW == 64) tc::tmem_ld32(tacc + cc + 32, *reinterpret_cast<float(*)[32]>(&v[32]));
+        tc::wait_ld();
+        if (!p.partial) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) v[j] *= p.alpha;
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+              const int col = n0 + cc + j;
+              v[j] += col < p.N ? __ldg(p.bias + col) : 0.f;
+            }
+          }
+          if (p.relu) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = fmaxf(v[j], 0.f);
+          }
+        }
+        uint8_t* rowp = sbuf + lane * 128;
+        const int sw = lane & 7;
+        if (p.has_res) {
+          tc::mbar_wait(&rbar[ew], rphase);
+          rphase ^= 1;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 r = *reinterpret_cast<const uint4*>(rowp + ((u ^ sw) << 4));
+            if constexpr (OUT_F32) {
+              v[4 * u + 0] = fmaf(p.beta, __uint_as_float(r.x), v[4 * u + 0]);
+              v[4 * u + 1] = fmaf(p.beta, __uint_as_float(r.y), v[4 * u + 1]);
+              v[4 * u + 2] = fmaf(p.beta, __uint_as_float(r.z), v[4 * u + 2]);
+              v[4 * u + 3] = fmaf(p.beta, __uint_as_float(r.w), v[4 * u + 3]);
+            } else {
+              const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 f = tc::bf16x2_f2(w[q]);
+                v[8 * u + 2 * q] = fmaf(p.beta, f.x, v[8 * u + 2 * q]);
+                v[8 * u + 2 * q + 1] = fmaf(p.beta, f.y, v[8 * u + 2 * q + 1]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint4 w;
+          if constexpr (OUT_F32) {
+            w = make_uint4(__float_as_uint(v[4 * u]), __float_as_uint(v[4 * u + 1]), __float_as_uint(v[4 * u + 2]),
+                           __float_as_uint(v[4 * u + 3]));
+          } else {
+            w = make_uint4(tc::pack_bf16(v[8 * u], v[8 * u + 1]), tc::pack_bf16(v[8 * u + 2], v[8 * u + 3]),
+                           tc::pack_bf16(v[8 * u + 4], v[8 * u + 5]), tc::pack_bf16(v[8 * u + 6], v[8 * u + 7]));
+          }
+          *reinterpret_cast<uint4*>(rowp + ((u ^ sw) << 4)) = w;
+        }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store3(&tmD, sbuf, n0 + cc, row0, zout);
+          bulk_commit();
+        }
+        buf ^= 1;
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator may be overwritten
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 1) tc::tmem_dealloc<F::TMEM_COLS>(tmem);
+}
+
+// Split-K close-out: D = act(alpha * sum_s P[s] + bias) + beta * C, summed in
+// split order (deterministic), 4 columns per thread.
+template <typename TD>
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t M, int64_t N, TD* D,
+                                     int64_t ldd, const TD* Cin, int64_t ldc, float alpha, float beta,
+                                     const float* __restrict__ bias, int relu) {
+  const int64_t n4 = N / 4;
+  const int64_t total = M * n4;
+  const int64_t plane = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / n4, n = (e % n4) * 4;
+    float4 s = *reinterpret_cast<const float4*>(ws + m * N + n);
+    for (int k = 1; k < splits; ++k) {
+      const float4 q = *reinterpret_cast<const float4*>(ws + k * plane + m * N + n);
+      s.x += q.x;
+      s.y += q.y;
+      s.z += q.z;
+      s.w += q.w;
+    }
+    float r[4] = {s.x * alpha, s.y * alpha, s.z * alpha, s.w * alpha};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (bias) r[j] += bias[n + j];
+      if (relu) r[j] = fmaxf(r[j], 0.f);
+      if (Cin) r[j] = fmaf(beta, to_f(Cin[m * ldc + n + j]), r[j]);
+      D[m * ldd + n + j] = from_f<TD>(r[j]);
+    }
+  }
+}
+
+// --- host side ----------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 3-D tiled map over a row-major [z][rows][cols] view (cols contiguous), box
+// {box_cols, box_rows, 1}, 128-byte swizzle.  false when TMA cannot address it.
+bool make_map(CUtensorMap* m, const void* base, bool f32, int64_t cols, int64_t rows, int64_t ld, int64_t zs,
+              int64_t nz, int box_cols, int box_rows) {
+  auto enc = encode_fn();
+  if (!enc) return false;
+  const int64_t es = f32 ? 4 : 2;
+  if (((uintptr_t)base & 15) || (ld * es) % 16 || (zs * es) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * es), (cuuint64_t)((nz > 1 ? zs : rows * ld) * es)};
+  if (strides[1] == 0 || strides[1] % 16) strides[1] = (cuuint64_t)(rows * ld * es);
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct SplitWs {
+  float* ptr = nullptr;
+  size_t bytes = 0;
+};
+constexpr size_t SPLIT_WS_BYTES = size_t(32) << 20;
+
+// per-device, per-stream-slot split-K workspaces, all allocated on the first
+// use (never inside a CUDA-graph capture, which forbids cudaMalloc)
+SplitWs& split_ws(cudaStream_t s) {
+  static SplitWs ws[16][EVO_STREAM_SLOTS];
+  static std::mutex mu;
+  int dev = 0;
+  EVO_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ws[dev & 15][0].ptr) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    EVO_CUDA(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) {
+      for (int k = 0; k < EVO_STREAM_SLOTS; ++k) {
+        EVO_CUDA(cudaMalloc(&ws[dev & 15][k].ptr, SPLIT_WS_BYTES));
+        ws[dev & 15][k].bytes = SPLIT_WS_BYTES;
+      }
+    }
+  }
+  return ws[dev & 15][stream_slot(s)];
+}
+
+int64_t g_tc_gemms = 0;  // tensor-core GEMMs launched (evo_gemm_tc_launches)
+
+template <int BN, bool OUT_F32>
+void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& c, const Params& p,
+            int grid, cudaStream_t s) {
+  auto k = gemm_tc_kernel<BN, OUT_F32>;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  });
+  k<<<grid, GT_THREADS, Cfg<BN>::SMEM, s>>>(a, b, d, c, p);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+  ++g_tc_gemms;
+}
+
+bool tc_gemm_disabled() {
+  static const bool v = [] {
+    const char* e = getenv("EVO_DISABLE_TC_GEMM");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+}  // namespace
+
+// Row-major D[b] = act(alpha * op(A[b]) op(B[b]) + bias) + beta * C[b] on the
+// tensor cores; A, B bf16; D and C (may alias D) of dtype d_dtype.  Returns
+// false (caller uses the SIMT kernel) when TMA cannot address an operand.
+bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
+             int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha,
+             float beta, const void* Cin, int64_t ldc, const float* bias, int relu, int d_dtype, cudaStream_t s) {
+  if (tc_gemm_disabled()) return false;
+  if (M <= 0 || N <= 0 || K <= 0 || batch < 1) return false;
+  if (M > (1ll << 31) - BM || N > (1ll << 31) - 256 || K > (1ll << 31) - BK) return false;
+  const bool f32 = d_dtype == EVO_F32;
+  const bool has_res = Cin != nullptr && beta != 0.f;
+  const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  Params p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.batch = batch;
+  p.n_mt = (int)((M + BM - 1) / BM);
+  p.n_nt = (int)((N + BN - 1) / BN);
+  p.kblocks = (int)((K + BK - 1) / BK);
+  p.a_mn = ta ? 1 : 0;
+  p.b_mn = tb ? 0 : 1;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.bias = bias;
+  p.relu = relu;
+  p.has_res = has_res ? 1 : 0;
+  const int nsm = num_sms();
+  const int64_t base = (int64_t)batch * p.n_mt * p.n_nt;
+  if (base > (1ll << 30)) return false;
+  // split K when the output tiles cannot fill the SMs and K is long
+  int splits = 1;
+  if (batch == 1 && base < nsm && p.kblocks >= 8 && N % 4 == 0) {
+    splits = (int)((nsm + base - 1) / base);
+    if (splits > p.kblocks / 4) splits = p.kblocks / 4;
+    SplitWs& ws = split_ws(s);
+    while (splits > 1 && (size_t)splits * M * N * 4 > ws.bytes) --splits;
+    if (!ws.ptr) splits = 1;
+  }
+  p.kb_per_split = (p.kblocks + splits - 1) / splits;
+  splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.partial = splits > 1 ? 1 : 0;
+  p.tiles = (int)(base * splits);
+
+  CUtensorMap ma, mb, md, mc;
+  // A: K-major [M, K] (lda) or MN-major [K, M]
+  if (!ta) {
+    if (!make_map(&ma, A, false, K, M, lda, sa, batch, 64, BM)) return false;
+  } else if (!make_map(&ma, A, false, M, K, lda, sa, batch, 64, BK)) {
+    return false;
+  }
+  if (tb) {
+    if (!make_map(&mb, B, false, K, N, ldb, sb, batch, 64, BN)) return false;
+  } else if (!make_map(&mb, B, false, N, K, ldb, sb, batch, 64, BK)) {
+    return false;
+  }
+  float* wsp = nullptr;
+  if (p.partial) {
+    wsp = split_ws(s).ptr;
+    if (!make_map(&md, wsp, true, N, M, N, M * N, splits, 32, 32)) return false;
+  } else if (!make_map(&md, D, f32, N, M, ldd, sd, batch, f32 ? 32 : 64, 32)) {
+    return false;
+  }
+  if (has_res && !p.partial) {
+    if (!make_map(&mc, Cin, f32, N, M, ldc, sd, batch, f32 ? 32 : 64, 32)) return false;
+  } else {
+    mc = md;
+    p.has_res = 0;
+  }
+  const int grid = (int)(p.tiles < nsm ? p.tiles : nsm);
+  const bool out32 = p.partial || f32;
+  if (BN == 256) {
+    out32 ? launch<256, true>(ma, mb, md, mc, p, grid, s) : launch<256, false>(ma, mb, md, mc, p, grid, s);
+  } else if (BN == 128) {
+    out32 ? launch<128, true>(ma, mb, md, mc, p, grid, s) : launch<128, false>(ma, mb, md, mc, p, grid, s);
+  } else {
+    out32 ? launch<64, true>(ma, mb, md, mc, p, grid, s) : launch<64, false>(ma, mb, md, mc, p, grid, s);
+  }
+  if (p.partial) {
+    const int64_t work = M * (N / 4);
+    int64_t blocks = (work + 255) / 256;
+    if (blocks > (int64_t)nsm * 8) blocks = (int64_t)nsm * 8;
+    const void* cptr = has_res ? Cin : nullptr;
+    if (f32)
+      splitk_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(wsp, splits, M, N, (float*)D, ldd,
+                                                                   (const float*)cptr, ldc, alpha, beta, bias, relu);
+    else
+      splitk_reduce_kernel<bf16><<<(unsigned)blocks, 256, 0, s>>>(wsp, splits, M, N, (bf16*)D, ldd,
+                                                                  (const bf16*)cptr, ldc, alpha, beta, bias, relu);
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+  }
+  return true;
+}
+
+}  // namespace evo
+
+extern "C" int64_t evo_gemm_tc_launches(void) { return evo::g_tc_gemms; }

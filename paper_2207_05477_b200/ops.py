@@ -98,30 +98,6 @@ def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.T
     return out
 
 
-EPI_RELU_AUX_BIAS, EPI_DRELU, EPI_BGRADA = 3, 4, 5
-
-
-def relu_aux_ld(n: int) -> int:
-    """Row pitch (bits) of the ReLU bit mask of an [M, n] output."""
-    return (n + 127) // 128 * 128
-
-
-def gemm_epilogue(a, b, d, epi, vec=None, aux=None, aux_ld=0, beta=0.0, ta=False, tb=False) -> bool:
-    """Fused training epilogue (see evo_gemm_epilogue); False when no fused
-    kernel exists for the problem (the caller runs the unfused sequence)."""
-    M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
-    Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
-    if K != Kb or tuple(d.shape) != (M, N):
-        raise ValueError("gemm_epilogue shape mismatch")
-    rc = _lib.lib().evo_gemm_epilogue(M, N, K, ptr(a), a.stride(0), int(ta), ptr(b), b.stride(0), int(tb),
-                                      ptr(d), d.stride(0), beta, epi, ptr(vec), ptr(aux), aux_ld, dcode(a),
-                                      dcode(d), stream())
-    if rc == 3:  # EVO_ERR_UNSUPPORTED
-        return False
-    _lib.check(rc)
-    return True
-
-
 def gemm_batched(a, b, c, batch, sa, sb, sc, ta=False, tb=False, alpha=1.0, beta=0.0):
     """Strided-batched row-major GEMM on flat buffers: operand k of batch i is
     the matrix at data_ptr + i*s (elements); a, b, c are 2-D views of batch 0."""

@@ -24,7 +24,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import rel_err
+from conftest import grad_err, rel_err
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -75,12 +75,13 @@ def _check(res, ref, tol_out, tol_grad, floor):
     assert e_pair <= tol_out, ("pair", e_pair)
     assert abs(loss - oloss) <= tol_out * abs(oloss), (loss, oloss)
     gmax = max(float(np.abs(g).max()) for g in ograds.values())   # G of SURVEY section 8c
-    errs = {n: rel_err(grads[n].reshape(g.shape), g, floor * gmax) for n, g in ograds.items()}
+    errs = {n: grad_err(grads[n].reshape(g.shape), g, n, floor, gmax) for n, g in ograds.items()}
     worst = max(errs, key=errs.get)
     assert errs[worst] <= tol_grad, (worst, errs[worst], sorted(errs.values())[-5:])
-    # the analytically-zero bias_ln_b gradients aside, every slot got a gradient
-    live = [n for n, g in grads.items() if np.abs(g).max() > 0]
-    assert len(live) >= len(grads) - sum("bias_ln_b" in n for n in grads)
+    # every slot the oracle gives a gradient got one (recycling parameters
+    # have none with one cycle; bias_ln_b is analytically zero)
+    dead = [n for n, g in ograds.items() if np.abs(g).max() > 1e-6 * gmax and not np.abs(grads[n]).max() > 0]
+    assert not dead, dead
 
 
 def test_bench_shape_bf16_matches_oracle(oracle_I):

@@ -254,7 +254,7 @@ def test_layernorm_bwd_ex_fused_outputs():
 @pytest.mark.parametrize("T,K,N", [(32768, 256, 256), (65536, 128, 512), (8192, 1024, 128)])
 def test_gemm_bias_fused_epilogue_vs_torch(relu, with_res, T, K, N):
     """Projection + module epilogue (bias [+ residual] or bias + ReLU) in one
-    kernel (evo_gemm_bias, cuBLASLt epilogue) against fp32 torch, at the
+    kernel (evo_gemm_bias, tcgen05 GEMM epilogue) against fp32 torch, at the
     bench shapes where the fused path is taken."""
     from paper_2207_05477_b200 import ops
     torch.manual_seed(T + K + N)
@@ -270,35 +270,6 @@ def test_gemm_bias_fused_epilogue_vs_torch(relu, with_res, T, K, N):
     if relu:
         ref = ref.clamp_min(0)
     assert rel(out.float(), ref) <= 1e-2
-
-
-def test_gemm_training_epilogues_vs_torch():
-    """evo_gemm_epilogue: ReLU with bit mask (fwd), dReLU from that mask, and
-    the bias gradient computed in the weight-gradient GEMM."""
-    from paper_2207_05477_b200 import ops
-    torch.manual_seed(3)
-    T, C, F = 32768, 128, 512
-    xl = torch.randn(T, C, device="cuda").bfloat16()
-    w1 = (torch.randn(C, F, device="cuda") / C ** 0.5).bfloat16()
-    w2 = (torch.randn(F, C, device="cuda") / F ** 0.5).bfloat16()
-    b1 = torch.randn(F, device="cuda") * 0.1
-    h = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
-    ld = ops.relu_aux_ld(F)
-    aux = torch.empty(T, ld // 8, dtype=torch.uint8, device="cuda")
-    if not ops.gemm_epilogue(xl, w1, h, ops.EPI_RELU_AUX_BIAS, vec=b1, aux=aux, aux_ld=ld):
-        pytest.skip("no fused ReLU-aux kernel for this problem")
-    pre = xl.float() @ w1.float() + b1
-    assert rel(h.float(), pre.clamp_min(0)) <= 1e-2
-    d_act = torch.randn(T, C, device="cuda").bfloat16()
-    dh = torch.empty(T, F, device="cuda", dtype=torch.bfloat16)
-    assert ops.gemm_epilogue(d_act, w2, dh, ops.EPI_DRELU, aux=aux, aux_ld=ld, tb=True)
-    ref_dh = (d_act.float() @ w2.float().t()) * (h.float() > 0)  # the mask the forward produced
-    assert rel(dh.float(), ref_dh) <= 1e-2
-    dw1 = torch.empty(C, F, device="cuda")
-    db1 = torch.empty(F, device="cuda")
-    assert ops.gemm_epilogue(xl, dh, dw1, ops.EPI_BGRADA, vec=db1, ta=True)
-    assert rel(dw1, xl.float().t() @ dh.float()) <= 1e-3
-    assert rel(db1, dh.float().sum(0)) <= 1e-3
 
 
 @pytest.mark.parametrize("geom", ["row", "col", "tri_start", "tri_end"])
