@@ -144,8 +144,10 @@ def test_gemm_batched_trimul_form(ta, tb):
 def test_gemm_fp32_is_true_fp32():
     """fp32 operands use FFMA (no TF32): a product TF32 would round is exact."""
     from paper_2207_05477_b200 import ops
-    a = torch.full((64, 32), 1.0 + 2 ** -20, device="cuda")
-    b = torch.ones((32, 64), device="cuda")
+    # 1 + 2^-12 needs 12 mantissa bits (TF32 keeps 10); every partial sum
+    # k (1 + 2^-12), k <= 8, is exact in fp32
+    a = torch.full((64, 8), 1.0 + 2 ** -12, device="cuda")
+    b = torch.ones((8, 64), device="cuda")
     c = torch.empty((64, 64), device="cuda")
     ops.gemm(a, b, c)
-    assert torch.all(c == 32 * (1.0 + 2 ** -20))
+    assert torch.all(c == 8 * (1.0 + 2 ** -12))
