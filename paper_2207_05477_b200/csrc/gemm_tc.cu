@@ -8,15 +8,16 @@
 // src/model.py:361-378 OPM projections and w_out) and their data / weight
 // gradients, plus TriangleMultiplication's channel-batched contractions.
 //
-// Structure (one CTA per SM, 6 warps):
+// Structure (one CTA per SM, 10 warps):
 //   warp 0      TMA producer: A and B k-blocks (BK = 64 bf16 = one 128-byte
 //               swizzle row) into a STAGES-deep shared-memory ring
 //               (mbarrier full/empty pairs, transaction-count completion);
 //   warp 1      allocates TMEM and issues tcgen05.mma (M = 128, N = BN,
 //               K = 16) from one elected lane into one of two TMEM
 //               accumulators, committing each stage back to the producer;
-//   warps 2..5  epilogue: tcgen05.ld of the accumulator (lane quarter =
-//               warp % 4), alpha / bias / ReLU / residual (beta * C, the
+//   warps 2..9  epilogue: tcgen05.ld of the accumulator (lane quarter =
+//               warp % 4, one column half each), alpha / bias / ReLU /
+//               residual (beta * C, the
 //               residual tile itself fetched by TMA), conversion, and a TMA
 //               store through a swizzled, double-buffered staging tile.
 // Operands may be K-major or MN-major in HBM (the weight-gradient GEMMs read
@@ -43,8 +44,8 @@ namespace {
 using bf16 = __nv_bfloat16;
 
 constexpr int BM = 128, BK = 64;
-constexpr int GT_THREADS = 192;
-constexpr int EPI_WARPS = 4;
+constexpr int EPI_WARPS = 8;                    // 2 per TMEM lane quarter (column halves)
+constexpr int GT_THREADS = 64 + 32 * EPI_WARPS;  // + producer and MMA warps
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int STG_BYTES = 32 * 128;   // one staging tile: 32 rows x 128 B
 
@@ -52,7 +53,7 @@ template <int BN>
 struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 6);
   static constexpr int OFF_STG = STAGES * STAGE;
   static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * 2 * STG_BYTES;
   static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS;
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], EPI_WARPS);
+      tc::mbar_init(&tempty[a], (BN == 64 && !OUT_F32) ? EPI_WARPS / 2 : EPI_WARPS);
     }
     for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
   }
@@ -235,8 +236,13 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   } else {
     // ---------------- epilogue ----------------
     constexpr int CW = OUT_F32 ? 32 : 64;  // columns per 128-byte staging row
+    // column halves of the tile (a 64-column bf16 tile has one: half the warps idle)
+    constexpr int HALVES = (BN / 2 >= CW) ? 2 : 1;
+    constexpr int HCOLS = BN / HALVES;
     const int ew = warp - 2;
     const int quarter = warp & 3;  // TMEM lanes this warp may access
+    const int half = ew >> 2;
+    if (half < HALVES) {
     uint8_t* stg = smem + F::OFF_STG + ew * 2 * STG_BYTES;
     int buf = 0;
     uint32_t rphase = 0;
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       tc::fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += CW) {
+      for (int cc = half * HCOLS; cc < (half + 1) * HCOLS; cc += CW) {
         if (n0 + cc >= p.N) break;
         uint8_t* sbuf = stg + buf * STG_BYTES;
         if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done
@@ -268,10 +274,22 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < CW; ++j) v[j] *= p.alpha;
           if (p.bias) {
+            if (n0 + cc + CW <= p.N && (p.N & 3) == 0) {  // 16-B vector loads of the bias slice
+              const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0 + cc);
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-              const int col = n0 + cc + j;
-              v[j] += col < p.N ? __ldg(p.bias + col) : 0.f;
+              for (int j = 0; j < CW / 4; ++j) {
+                const float4 b = __ldg(b4 + j);
+                v[4 * j] += b.x;
+                v[4 * j + 1] += b.y;
+                v[4 * j + 2] += b.z;
+                v[4 * j + 3] += b.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < CW; ++j) {
+                const int col = n0 + cc + j;
+                v[j] += col < p.N ? __ldg(p.bias + col) : 0.f;
+              }
             }
           }
           if (p.relu) {
@@ -328,6 +346,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator may be overwritten
     }
     if (lane == 0) bulk_wait_all();
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -335,33 +354,54 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   if (warp == 1) tc::tmem_dealloc<F::TMEM_COLS>(tmem);
 }
 
-// Split-K close-out: D = act(alpha * sum_s P[s] + bias) + beta * C, summed in
-// split order (deterministic), 4 columns per thread.
+// Split-K close-out: D = act(alpha * sum_s P[s] + bias) + beta * C.  A block
+// owns 128 consecutive output columns of one row (32 float4 lanes); its 8 warps
+// sum interleaved subsets of the splits (s = w, w + 8, ...) and the 8 partial
+// sums are combined in warp order through shared memory -- a fixed summation
+// order, so results are deterministic, with 8 x 32 loads in flight per block.
 template <typename TD>
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t M, int64_t N, TD* D,
-                                     int64_t ldd, const TD* Cin, int64_t ldc, float alpha, float beta,
-                                     const float* __restrict__ bias, int relu) {
-  const int64_t n4 = N / 4;
-  const int64_t total = M * n4;
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t M,
+                                                            int64_t N, TD* D, int64_t ldd, const TD* Cin,
+                                                            int64_t ldc, float alpha, float beta,
+                                                            const float* __restrict__ bias, int relu) {
+  __shared__ float4 part[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t cblocks = (N + 127) / 128;
+  const int64_t m = blockIdx.x / cblocks;
+  const int64_t n = (blockIdx.x % cblocks) * 128 + lane * 4;
+  const bool ok = n < N;  // N % 4 == 0
   const int64_t plane = M * N;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = e / n4, n = (e % n4) * 4;
-    float4 s = *reinterpret_cast<const float4*>(ws + m * N + n);
-    for (int k = 1; k < splits; ++k) {
-      const float4 q = *reinterpret_cast<const float4*>(ws + k * plane + m * N + n);
-      s.x += q.x;
-      s.y += q.y;
-      s.z += q.z;
-      s.w += q.w;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) {
+    const float* src = ws + m * N + n;
+#pragma unroll 4
+    for (int k = w; k < splits; k += 8) {
+      const float4 q = *reinterpret_cast<const float4*>(src + k * plane);
+      acc.x += q.x;
+      acc.y += q.y;
+      acc.z += q.z;
+      acc.w += q.w;
     }
-    float r[4] = {s.x * alpha, s.y * alpha, s.z * alpha, s.w * alpha};
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w != 0 || !ok) return;
+  float4 t = part[0][lane];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (bias) r[j] += bias[n + j];
-      if (relu) r[j] = fmaxf(r[j], 0.f);
-      if (Cin) r[j] = fmaf(beta, to_f(Cin[m * ldc + n + j]), r[j]);
-      D[m * ldd + n + j] = from_f<TD>(r[j]);
-    }
+  for (int k = 1; k < 8; ++k) {
+    const float4 q = part[k][lane];
+    t.x += q.x;
+    t.y += q.y;
+    t.z += q.z;
+    t.w += q.w;
+  }
+  float r[4] = {t.x * alpha, t.y * alpha, t.z * alpha, t.w * alpha};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (bias) r[j] += bias[n + j];
+    if (relu) r[j] = fmaxf(r[j], 0.f);
+    if (Cin) r[j] = fmaf(beta, to_f(Cin[m * ldc + n + j]), r[j]);
+    D[m * ldd + n + j] = from_f<TD>(r[j]);
   }
 }
 
@@ -452,6 +492,28 @@ bool tc_gemm_disabled() {
 
 }  // namespace
 
+// Split-K workspace of the stream's slot (nullptr before the first non-capturing
+// GEMM) and its close-out; shared with the CUDA-core GEMM (gemm_simt.cu).
+float* gemm_split_ws(cudaStream_t s, size_t* bytes) {
+  SplitWs& w = split_ws(s);
+  *bytes = w.bytes;
+  return w.ptr;
+}
+
+void splitk_reduce(const float* ws, int splits, int64_t M, int64_t N, void* D, int64_t ldd, const void* Cin,
+                   int64_t ldc, float alpha, float beta, const float* bias, int relu, int d_dtype, cudaStream_t s) {
+  const int64_t blocks = M * ((N + 127) / 128);
+  EVO_REQUIRE(N % 4 == 0 && blocks < (1ll << 31), EVO_ERR_ARG, "split-K reduce: bad extents");
+  if (d_dtype == EVO_F32)
+    splitk_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(ws, splits, M, N, (float*)D, ldd,
+                                                                 (const float*)Cin, ldc, alpha, beta, bias, relu);
+  else
+    splitk_reduce_kernel<bf16><<<(unsigned)blocks, 256, 0, s>>>(ws, splits, M, N, (bf16*)D, ldd, (const bf16*)Cin,
+                                                                ldc, alpha, beta, bias, relu);
+  EVO_LAUNCH_CHECK();
+  count_launch(1);
+}
+
 // Row-major D[b] = act(alpha * op(A[b]) op(B[b]) + bias) + beta * C[b] on the
 // tensor cores; A, B bf16; D and C (may alias D) of dtype d_dtype.  Returns
 // false (caller uses the SIMT kernel) when TMA cannot address an operand.
@@ -484,9 +546,11 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   if (base > (1ll << 30)) return false;
   // split K when the output tiles cannot fill the SMs and K is long
   int splits = 1;
-  if (batch == 1 && base < nsm && p.kblocks >= 8 && N % 4 == 0) {
+  if (batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
+    // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes
     splits = (int)((nsm + base - 1) / base);
-    if (splits > p.kblocks / 4) splits = p.kblocks / 4;
+    if (splits > p.kblocks / 8) splits = p.kblocks / 8;
+    if (splits > 64) splits = 64;
     SplitWs& ws = split_ws(s);
     while (splits > 1 && (size_t)splits * M * N * 4 > ws.bytes) --splits;
     if (!ws.ptr) splits = 1;
@@ -530,20 +594,8 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   } else {
     out32 ? launch<64, true>(ma, mb, md, mc, p, grid, s) : launch<64, false>(ma, mb, md, mc, p, grid, s);
   }
-  if (p.partial) {
-    const int64_t work = M * (N / 4);
-    int64_t blocks = (work + 255) / 256;
-    if (blocks > (int64_t)nsm * 8) blocks = (int64_t)nsm * 8;
-    const void* cptr = has_res ? Cin : nullptr;
-    if (f32)
-      splitk_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(wsp, splits, M, N, (float*)D, ldd,
-                                                                   (const float*)cptr, ldc, alpha, beta, bias, relu);
-    else
-      splitk_reduce_kernel<bf16><<<(unsigned)blocks, 256, 0, s>>>(wsp, splits, M, N, (bf16*)D, ldd,
-                                                                  (const bf16*)cptr, ldc, alpha, beta, bias, relu);
-    EVO_LAUNCH_CHECK();
-    count_launch(1);
-  }
+  if (p.partial) splitk_reduce(wsp, splits, M, N, D, ldd, has_res ? Cin : nullptr, ldc, alpha, beta, bias, relu,
+                               d_dtype, s);
   return true;
 }
 

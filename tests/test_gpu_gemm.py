@@ -151,3 +151,23 @@ def test_gemm_fp32_is_true_fp32():
     c = torch.empty((64, 64), device="cuda")
     ops.gemm(a, b, c)
     assert torch.all(c == 8 * (1.0 + 2 ** -12))
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 128, 65536), (8, 256, 32768), (100, 36, 4100)])
+def test_gemm_fp32_split_k(M, N, K):
+    """The embedding weight gradients (fp32, 8 x C outputs, K = tokens) take
+    the CUDA-core kernel's split-K path; deterministic and true fp32."""
+    from paper_2207_05477_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((K, M), device="cuda", generator=g)
+    b = torch.randn((K, N), device="cuda", generator=g)
+    ref = a.double().t() @ b.double()
+    c = torch.empty((M, N), device="cuda")
+    ops.gemm(a, b, c, ta=True)
+    assert float((c.double() - ref).abs().max() / ref.abs().max()) <= 1e-5
+    c2 = torch.full_like(c, 1.0)
+    ops.gemm(a, b, c2, ta=True, beta=1.0)
+    assert float((c2.double() - ref - 1.0).abs().max() / ref.abs().max()) <= 1e-5
+    c3 = torch.empty_like(c)
+    ops.gemm(a, b, c3, ta=True)
+    assert torch.equal(c, c3)

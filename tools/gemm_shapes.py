@@ -28,7 +28,12 @@ def main():
             M, N, K = args[0], args[1], args[2]
             ta, tb, batch = args[5], args[9], args[14]
             ad, cd = args[17], args[18]
-            calls.append((M, N, K, ta, tb, batch, ad, cd))
+            calls.append((M, N, K, ta, tb, batch, ad, cd, 0))
+        elif name == "evo_gemm_bias":
+            M, N, K = args[0], args[1], args[2]
+            ta, tb = args[5], args[8]
+            epi = 2 if args[13] else (3 if args[9] else 1)   # relu / residual / bias only
+            calls.append((M, N, K, ta, tb, 1, args[16], args[17], epi))
         return orig(name, *args)
 
     ops.call = rec
@@ -39,19 +44,27 @@ def main():
     dt = {0: torch.float32, 1: torch.bfloat16}
     tot_t = tot_f = 0.0
     rows = []
-    for (M, N, K, ta, tb, batch, ad, cd), n in cnt.items():
+    for (M, N, K, ta, tb, batch, ad, cd, epi), n in cnt.items():
         a = torch.randn((K, M) if ta else (M, K), device="cuda").to(dt.get(ad, torch.bfloat16))
         b = torch.randn((N, K) if tb else (K, N), device="cuda").to(dt.get(ad, torch.bfloat16))
         c = torch.empty((M, N), device="cuda", dtype=dt.get(cd, torch.float32))
         if batch != 1:
             continue
+        bias = torch.zeros(N, device="cuda")
+        res = torch.zeros_like(c) if epi == 3 else None
+
+        def run():
+            if epi:
+                ops.gemm_bias(a, b, c, bias, res=res, relu=epi == 2, ta=bool(ta), tb=bool(tb))
+            else:
+                ops.gemm(a, b, c, ta=bool(ta), tb=bool(tb))
         for _ in range(3):
-            ops.gemm(a, b, c, ta=bool(ta), tb=bool(tb))
+            run()
         torch.cuda.synchronize()
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr):
             for _ in range(20):
-                ops.gemm(a, b, c, ta=bool(ta), tb=bool(tb))
+                run()
         gr.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -63,10 +76,12 @@ def main():
         fl = 2.0 * M * N * K
         tot_t += us * n
         tot_f += fl * n
-        rows.append((us * n, M, N, K, ta, tb, ad, cd, n, us, fl / us / 1e6))
+        es = 2 if cd == 1 else 4
+        byt = (M * K + K * N) * (2 if ad == 1 else 4) + M * N * es * (2 if epi == 3 else 1)
+        rows.append((us * n, M, N, K, ta, tb, ad, cd, n, us, fl / us / 1e6, epi, byt / us / 1e3))
     for r in sorted(rows, reverse=True):
-        print(f"M={r[1]:6d} N={r[2]:6d} K={r[3]:6d} ta={r[4]} tb={r[5]} a{r[6]} c{r[7]} x{r[8]}  "
-              f"{r[9]:8.1f} us  {r[10]:7.1f} TF/s  total {r[0]:8.1f} us")
+        print(f"M={r[1]:6d} N={r[2]:6d} K={r[3]:6d} ta={r[4]} tb={r[5]} a{r[6]} c{r[7]} epi{r[11]} x{r[8]}  "
+              f"{r[9]:8.1f} us  {r[10]:7.1f} TF/s {r[12]:7.0f} GB/s  total {r[0]:8.1f} us")
     print(f"per block: {tot_t:.1f} us, {tot_f / tot_t / 1e6:.1f} TF/s")
 
 
