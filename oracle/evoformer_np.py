@@ -310,6 +310,11 @@ def attention_fwd(x, mask, nb, p):
     logits += maskbias[:, :, None, None, :]                      # :154
     if nb is not None:
         logits += nb[None, None]                                 # :156
+    if logits.dtype != np.float32:
+        # float64 evaluation (serial_grads_f64): keep the fp32 mask-bias
+        # semantics -- at -1e9 every logit of a fully-masked row rounds to the
+        # same fp32 value, so the row is uniform
+        logits = logits.astype(np.float32).astype(logits.dtype)
     m = logits.max(axis=-1, keepdims=True)                       # :159-161
     e = np.exp(logits - m)
     w = (e / e.sum(axis=-1, keepdims=True)).astype(F32)
@@ -751,6 +756,25 @@ def serial_grads(cfg, P, feats, n_cycles=1):
     out = {name: grads.get(name, np.zeros(shape, F32)).astype(F32)
            for name, shape, _ in param_specs(cfg)}
     return loss, out, (msa, pair)
+
+
+def serial_grads_f64(cfg, P, feats, n_cycles=1):
+    """``serial_grads`` evaluated in float64 (inputs and parameters are the
+    fp32 ones, promoted; the fp32 rounding of the masked logits is kept).  The
+    fp32 restatement's own deviation from this bounds what any fp32
+    implementation can be expected to match it to: long reductions at the
+    initial-training shape (65,536-term weight gradients, 128-sequence bias
+    gradients) leave ~1e-4 relative rounding in a few small gradients."""
+    global F32
+    saved = F32
+    F32 = np.float64
+    try:
+        P64 = {k: np.asarray(v, np.float64) for k, v in P.items()}
+        f64 = Features(**{k: np.asarray(getattr(feats, k), np.float64)
+                          for k in ("msa_feat", "pair_feat", "msa_mask", "pair_mask")})
+        return serial_grads(cfg, P64, f64, n_cycles)
+    finally:
+        F32 = saved
 
 
 # ---------------------------------------------------------------------------
