@@ -547,10 +547,16 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   // split K when the output tiles cannot fill the SMs and K is long
   int splits = 1;
   if (batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
-    // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes
-    splits = (int)((nsm + base - 1) / base);
+    // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes; the
+    // split tiles must fit one wave of the persistent grid (a second, mostly
+    // idle wave doubles the kernel time)
+    splits = (int)(nsm / base);
     if (splits > p.kblocks / 8) splits = p.kblocks / 8;
     if (splits > 64) splits = 64;
+    if (const char* e = getenv("EVO_GEMM_SPLITS")) {  // tuning sweeps (tools/splitk_sweep.py)
+      const int f = atoi(e);
+      if (f > 0) splits = f < p.kblocks ? f : p.kblocks;
+    }
     SplitWs& ws = split_ws(s);
     while (splits > 1 && (size_t)splits * M * N * 4 > ws.bytes) --splits;
     if (!ws.ptr) splits = 1;

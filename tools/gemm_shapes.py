@@ -42,7 +42,7 @@ def main():
     torch.cuda.synchronize()
     cnt = Counter(calls)
     dt = {0: torch.float32, 1: torch.bfloat16}
-    tot_t = tot_f = 0.0
+    tot_t = tot_f = tot_cb = 0.0
     rows = []
     for (M, N, K, ta, tb, batch, ad, cd, epi), n in cnt.items():
         a = torch.randn((K, M) if ta else (M, K), device="cuda").to(dt.get(ad, torch.bfloat16))
@@ -73,16 +73,33 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 20 * 1e3
+        # cuBLAS (torch.matmul, bf16 out) on the same operands, for comparison only
+        at = a.t() if ta else a
+        bt = b.t() if tb else b
+        for _ in range(3):
+            torch.matmul(at, bt)
+        gr2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr2):
+            for _ in range(20):
+                torch.matmul(at, bt)
+        gr2.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        gr2.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us_cublas = e0.elapsed_time(e1) / 20 * 1e3
         fl = 2.0 * M * N * K
         tot_t += us * n
         tot_f += fl * n
         es = 2 if cd == 1 else 4
         byt = (M * K + K * N) * (2 if ad == 1 else 4) + M * N * es * (2 if epi == 3 else 1)
-        rows.append((us * n, M, N, K, ta, tb, ad, cd, n, us, fl / us / 1e6, epi, byt / us / 1e3))
+        rows.append((us * n, M, N, K, ta, tb, ad, cd, n, us, fl / us / 1e6, epi, byt / us / 1e3, us_cublas))
+        tot_cb += us_cublas * n
     for r in sorted(rows, reverse=True):
         print(f"M={r[1]:6d} N={r[2]:6d} K={r[3]:6d} ta={r[4]} tb={r[5]} a{r[6]} c{r[7]} epi{r[11]} x{r[8]}  "
-              f"{r[9]:8.1f} us  {r[10]:7.1f} TF/s {r[12]:7.0f} GB/s  total {r[0]:8.1f} us")
-    print(f"per block: {tot_t:.1f} us, {tot_f / tot_t / 1e6:.1f} TF/s")
+              f"{r[9]:8.1f} us  {r[10]:7.1f} TF/s {r[12]:7.0f} GB/s  total {r[0]:8.1f} us  cublas {r[13]:8.1f} us")
+    print(f"per block: {tot_t:.1f} us, {tot_f / tot_t / 1e6:.1f} TF/s; cublas (bf16 out) {tot_cb:.1f} us")
 
 
 if __name__ == "__main__":
