@@ -241,6 +241,12 @@ class PackPlan:
              self.unpack, stream())
 
 
+def scale_(y, s):
+    """y *= s in place (fp32)."""
+    call("evo_scale_inplace", ptr(y), float(s), y.numel(), stream())
+    return y
+
+
 def cast(x, y):
     call("evo_cast", ptr(x), dcode(x), ptr(y), dcode(y), x.numel(), stream())
     return y
