@@ -49,16 +49,30 @@ constexpr int GT_THREADS = 64 + 32 * EPI_WARPS;  // + producer and MMA warps
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int STG_BYTES = 32 * 128;   // one staging tile: 32 rows x 128 B
 
-template <int BN>
+constexpr int KB_RES = 4;             // B-resident mode: K <= 256 (four 64-wide k-blocks)
+constexpr int SMEM_LIMIT = 232448;     // 227 KB of dynamic shared memory per CTA
+
+// BRES (B resident): the whole [BN x K] B tile of the CTA's fixed N-tile is
+// loaded once and stays in shared memory; only A k-blocks stream through
+// the ring.  For the K <= 256 projections this halves-to-thirds the bytes
+// each MMA waits for (the streamed operand is the MMA's latency bound).
+template <int BN, bool BRES>
 struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 6);
-  static constexpr int OFF_STG = STAGES * STAGE;
-  static constexpr int OFF_BAR = OFF_STG + EPI_WARPS * 2 * STG_BYTES;
-  static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS;
+  static constexpr int BRES_BYTES = BRES ? KB_RES * B_BYTES : 0;
+  static constexpr int STAGE = BRES ? A_BYTES : A_BYTES + B_BYTES;
+  static constexpr int STG_BUFS = (BRES && BN == 256) ? 1 : 2;  // epilogue staging buffers per warp
+  static constexpr int STG_TOTAL = EPI_WARPS * STG_BUFS * STG_BYTES;
+  static constexpr int FIT = (SMEM_LIMIT - 1024 - 512 - BRES_BYTES - STG_TOTAL) / STAGE;
+  static constexpr int STAGES = BRES ? (FIT > 8 ? 8 : FIT) : (BN == 256 ? 3 : (BN == 128 ? 5 : 6));
+  static constexpr int OFF_RING = BRES_BYTES;
+  static constexpr int OFF_STG = OFF_RING + STAGES * STAGE;
+  static constexpr int OFF_BAR = OFF_STG + STG_TOTAL;
+  static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS + 1;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // +1 KB: runtime 1024-B alignment
   static constexpr int TMEM_COLS = 2 * BN;                      // two accumulators (128/256/512)
+  static_assert(SMEM <= SMEM_LIMIT, "shared memory budget");
+  static_assert(STAGES >= 2, "ring depth");
 };
 
 struct Params {
@@ -87,7 +101,8 @@ __device__ __forceinline__ void tma_store3(const CUtensorMap* m, const void* src
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
@@ -135,11 +150,11 @@ __device__ __forceinline__ TileCoord decode(const Params& p, int t) {
   return c;
 }
 
-template <int BN, bool OUT_F32>
+template <int BN, bool OUT_F32, bool BRES>
 __global__ void __launch_bounds__(GT_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmC, Params p) {
-  using F = Cfg<BN>;
+  using F = Cfg<BN, BRES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + F::OFF_BAR);
@@ -147,7 +162,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   uint64_t* tfull = empty + F::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(rbar + EPI_WARPS);
+  uint64_t* bfull = rbar + EPI_WARPS;  // resident B landed (BRES)
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -164,6 +180,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       tc::mbar_init(&tempty[a], (BN == 64 && !OUT_F32) ? EPI_WARPS / 2 : EPI_WARPS);
     }
     for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
+    tc::mbar_init(bfull, 1);
   }
   if (warp == 1) tc::tmem_alloc<F::TMEM_COLS>(slot);
   tc::fence_before();
@@ -174,6 +191,19 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
+      auto load_b = [&](uint8_t* sb, uint64_t* bar, int k0, int n0, int b) {
+        if (!p.b_mn) {
+          tma_load3(&tmB, sb, bar, k0, n0, b);
+        } else {
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i) tma_load3(&tmB, sb + i * 8192, bar, n0 + 64 * i, k0, b);
+        }
+      };
+      if constexpr (BRES) {  // the CTA's N-tile is fixed (gridDim.x % n_nt == 0): load its B once
+        const TileCoord c = decode(p, blockIdx.x);
+        expect_tx(bfull, (uint32_t)(p.kblocks * F::B_BYTES));
+        for (int kb = 0; kb < p.kblocks; ++kb) load_b(smem + kb * F::B_BYTES, bfull, kb * BK, c.n0 * BN, c.b);
+      }
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -182,8 +212,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         for (int kb = c.kb0; kb < c.kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           expect_tx(&full[stage], F::STAGE);
-          uint8_t* sa = smem + stage * F::STAGE;
-          uint8_t* sb = sa + A_BYTES;
+          uint8_t* sa = smem + F::OFF_RING + stage * F::STAGE;
           const int k0 = kb * BK;
           if (!p.a_mn) {
             tma_load3(&tmA, sa, &full[stage], k0, c.m0, c.b);
@@ -191,12 +220,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             tma_load3(&tmA, sa, &full[stage], c.m0, k0, c.b);
             tma_load3(&tmA, sa + 8192, &full[stage], c.m0 + 64, k0, c.b);
           }
-          if (!p.b_mn) {
-            tma_load3(&tmB, sb, &full[stage], k0, n0, c.b);
-          } else {
-#pragma unroll
-            for (int i = 0; i < BN / 64; ++i) tma_load3(&tmB, sb + i * 8192, &full[stage], n0 + 64 * i, k0, c.b);
-          }
+          if constexpr (!BRES) load_b(sa + A_BYTES, &full[stage], k0, n0, c.b);
           if (++stage == F::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -207,6 +231,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (one elected lane) ----------------
     const uint32_t idesc = tc::idesc_bf16(BM, BN, p.a_mn != 0, p.b_mn != 0);
+    if constexpr (BRES) {
+      tc::mbar_wait(bfull, 0);
+      tc::fence_after();
+    }
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -219,8 +247,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       for (int kb = c.kb0; kb < c.kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::fence_after();
-        const uint32_t sa = tc::smem_u32(smem + stage * F::STAGE);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t sa = tc::smem_u32(smem + F::OFF_RING + stage * F::STAGE);
+        const uint32_t sb = BRES ? tc::smem_u32(smem + kb * F::B_BYTES) : sa + A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK / 16; ++ks)
           tc::mma_bf16_ss_w(dacc, op_desc(sa, p.a_mn, ks), op_desc(sb, p.b_mn, ks), idesc,
@@ -243,7 +271,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     const int quarter = warp & 3;  // TMEM lanes this warp may access
     const int half = ew >> 2;
     if (half < HALVES) {
-    uint8_t* stg = smem + F::OFF_STG + ew * 2 * STG_BYTES;
+    uint8_t* stg = smem + F::OFF_STG + ew * F::STG_BUFS * STG_BYTES;
     int buf = 0;
     uint32_t rphase = 0;
     int it = 0;
@@ -260,7 +288,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       for (int cc = half * HCOLS; cc < (half + 1) * HCOLS; cc += CW) {
         if (n0 + cc >= p.N) break;
         uint8_t* sbuf = stg + buf * STG_BYTES;
-        if (lane == 0) bulk_wait_read1();  // the store that last read this buffer is done
+        if (lane == 0) bulk_wait_read<F::STG_BUFS - 1>();  // the store that last read this buffer is done
         __syncwarp();
         if (p.has_res && lane == 0) {
           expect_tx(&rbar[ew], STG_BYTES);
@@ -272,7 +300,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         tc::wait_ld();
         if (!p.partial) {
 #pragma unroll
-          for (int j = 0; j < CW; ++j) v[j] *= p.alpha;
+          for (int j = 0; j < CW; ++j) v[j] = p.alpha == 1.f ? v[j] : v[j] * p.alpha;
           if (p.bias) {
             if (n0 + cc + CW <= p.N && (p.N & 3) == 0) {  // 16-B vector loads of the bias slice
               const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0 + cc);
@@ -339,7 +367,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
           tma_store3(&tmD, sbuf, n0 + cc, row0, zout);
           bulk_commit();
         }
-        buf ^= 1;
+        if constexpr (F::STG_BUFS == 2) buf ^= 1;
       }
       tc::fence_before();
       __syncwarp();
@@ -468,18 +496,23 @@ SplitWs& split_ws(cudaStream_t s) {
 
 int64_t g_tc_gemms = 0;  // tensor-core GEMMs launched (evo_gemm_tc_launches)
 
-template <int BN, bool OUT_F32>
+template <int BN, bool OUT_F32, bool BRES>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& c, const Params& p,
             int grid, cudaStream_t s) {
-  auto k = gemm_tc_kernel<BN, OUT_F32>;
+  auto k = gemm_tc_kernel<BN, OUT_F32, BRES>;
   static std::once_flag once;
   std::call_once(once, [&] {
-    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, BRES>::SMEM));
   });
-  k<<<grid, GT_THREADS, Cfg<BN>::SMEM, s>>>(a, b, d, c, p);
+  k<<<grid, GT_THREADS, Cfg<BN, BRES>::SMEM, s>>>(a, b, d, c, p);
   EVO_LAUNCH_CHECK();
   count_launch(1);
   ++g_tc_gemms;
+}
+
+bool bres_disabled() {  // A/B switch for measurements (EVO_GEMM_BRES=0)
+  const char* e = getenv("EVO_GEMM_BRES");
+  return e && e[0] == '0';
 }
 
 bool tc_gemm_disabled() {
@@ -591,14 +624,25 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
     mc = md;
     p.has_res = 0;
   }
-  const int grid = (int)(p.tiles < nsm ? p.tiles : nsm);
+  int grid = (int)(p.tiles < nsm ? p.tiles : nsm);
   const bool out32 = p.partial || f32;
+  // B resident: short K, several M-tiles per CTA; the grid is a multiple of
+  // the N-tile count so each CTA keeps one N-tile (tile t -> n = t % n_nt)
+  const bool bres = !p.partial && BN >= 128 && p.kblocks <= KB_RES && p.n_nt <= nsm &&
+                    p.tiles >= 2 * nsm && !bres_disabled();
+  if (bres) grid = (nsm / p.n_nt) * p.n_nt;
   if (BN == 256) {
-    out32 ? launch<256, true>(ma, mb, md, mc, p, grid, s) : launch<256, false>(ma, mb, md, mc, p, grid, s);
+    if (bres)
+      out32 ? launch<256, true, true>(ma, mb, md, mc, p, grid, s) : launch<256, false, true>(ma, mb, md, mc, p, grid, s);
+    else
+      out32 ? launch<256, true, false>(ma, mb, md, mc, p, grid, s) : launch<256, false, false>(ma, mb, md, mc, p, grid, s);
   } else if (BN == 128) {
-    out32 ? launch<128, true>(ma, mb, md, mc, p, grid, s) : launch<128, false>(ma, mb, md, mc, p, grid, s);
+    if (bres)
+      out32 ? launch<128, true, true>(ma, mb, md, mc, p, grid, s) : launch<128, false, true>(ma, mb, md, mc, p, grid, s);
+    else
+      out32 ? launch<128, true, false>(ma, mb, md, mc, p, grid, s) : launch<128, false, false>(ma, mb, md, mc, p, grid, s);
   } else {
-    out32 ? launch<64, true>(ma, mb, md, mc, p, grid, s) : launch<64, false>(ma, mb, md, mc, p, grid, s);
+    out32 ? launch<64, true, false>(ma, mb, md, mc, p, grid, s) : launch<64, false, false>(ma, mb, md, mc, p, grid, s);
   }
   if (p.partial) splitk_reduce(wsp, splits, M, N, D, ldd, has_res ? Cin : nullptr, ldc, alpha, beta, bias, relu,
                                d_dtype, s);
