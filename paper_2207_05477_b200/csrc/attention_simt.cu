@@ -330,6 +330,8 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
 int64_t attn_bwd_tc_workspace(const AttnGeom& g, int dtype);
 bool attn_fwd_tc_kb_try(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx,
                         void* gate, void* gated, float* lse, const AttnGeom& g, int dtype, cudaStream_t s);
+bool attn_fwd_tc2_try(const void* qkvg, const float* mask, const void* nb, const float* bg, void* ctx, void* gate,
+                      void* gated, float* lse, const AttnGeom& g, int dtype, cudaStream_t s);
 
 static AttnGeom make_geom(int64_t B, int64_t L, int64_t H, int64_t D, int64_t sb, int64_t sl,
                           int64_t ld, int64_t msb, int64_t msl) {
@@ -363,6 +365,7 @@ int evo_attn_fwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t m
   EVO_API_BEGIN
   AttnGeom g = make_geom(B, L, H, D, tok_sb, tok_sl, ld_qkvg, mask_sb, mask_sl);
   cudaStream_t s = (cudaStream_t)stream;
+  if (attn_fwd_tc2_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
   if (attn_fwd_tc_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
   if (attn_fwd_tc_kb_try(qkvg, mask, nb, bg, ctx, gate, gated, lse, g, dtype, s)) return EVO_OK;
   const float scale = (float)(1.0 / sqrt((double)D));

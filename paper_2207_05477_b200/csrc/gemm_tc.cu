@@ -61,14 +61,14 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int BRES_BYTES = BRES ? KB_RES * B_BYTES : 0;
   static constexpr int STAGE = BRES ? A_BYTES : A_BYTES + B_BYTES;
-  static constexpr int STG_BUFS = (BRES && BN == 256) ? 1 : 2;  // epilogue staging buffers per warp
+  static constexpr int STG_BUFS = 2;  // epilogue staging buffers per warp (store i+1 staged while i drains)
   static constexpr int STG_TOTAL = EPI_WARPS * STG_BUFS * STG_BYTES;
   static constexpr int FIT = (SMEM_LIMIT - 1024 - 512 - BRES_BYTES - STG_TOTAL) / STAGE;
   static constexpr int STAGES = BRES ? (FIT > 8 ? 8 : FIT) : (BN == 256 ? 3 : (BN == 128 ? 5 : 6));
   static constexpr int OFF_RING = BRES_BYTES;
   static constexpr int OFF_STG = OFF_RING + STAGES * STAGE;
   static constexpr int OFF_BAR = OFF_STG + STG_TOTAL;
-  static constexpr int NBAR = 2 * STAGES + 4 + EPI_WARPS + 1;
+  static constexpr int NBAR = 2 * STAGES + 4 + 2 * EPI_WARPS + 1;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // +1 KB: runtime 1024-B alignment
   static constexpr int TMEM_COLS = 2 * BN;                      // two accumulators (128/256/512)
   static_assert(SMEM <= SMEM_LIMIT, "shared memory budget");
@@ -103,6 +103,7 @@ __device__ __forceinline__ void tma_store3(const CUtensorMap* m, const void* src
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   uint64_t* tfull = empty + F::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rbar = tempty + 2;
-  uint64_t* bfull = rbar + EPI_WARPS;  // resident B landed (BRES)
+  uint64_t* bfull = rbar + 2 * EPI_WARPS;  // resident B landed (BRES)
   uint32_t* slot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], (BN == 64 && !OUT_F32) ? EPI_WARPS / 2 : EPI_WARPS);
     }
-    for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
+    for (int w = 0; w < 2 * EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
     tc::mbar_init(bfull, 1);
   }
   if (warp == 1) tc::tmem_alloc<F::TMEM_COLS>(slot);
@@ -281,18 +282,34 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       const int n0 = c.n0 * BN;
       const int row0 = c.m0 + quarter * 32;
       const int zout = p.partial ? c.split : c.b;
+      // residual tiles of the first two chunks are fetched before the
+      // accumulator is ready, so their latency hides under this tile's MMAs
+      const int nchunk = max(0, min(HCOLS, p.N - n0 - half * HCOLS) + CW - 1) / CW;
+      if (p.has_res) {
+        if (lane == 0) {
+          bulk_wait_all_read();  // both staging buffers free
+          for (int j = 0; j < nchunk && j < 2; ++j) {
+            const int b = buf ^ j;
+            expect_tx(&rbar[2 * ew + b], STG_BYTES);
+            tma_load3(&tmC, stg + b * STG_BYTES, &rbar[2 * ew + b], n0 + half * HCOLS + j * CW, row0, c.b);
+          }
+        }
+        __syncwarp();
+      }
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int cc = half * HCOLS; cc < (half + 1) * HCOLS; cc += CW) {
-        if (n0 + cc >= p.N) break;
+      for (int ch = 0; ch < nchunk; ++ch) {
+        const int cc = half * HCOLS + ch * CW;
         uint8_t* sbuf = stg + buf * STG_BYTES;
-        if (lane == 0) bulk_wait_read<F::STG_BUFS - 1>();  // the store that last read this buffer is done
-        __syncwarp();
-        if (p.has_res && lane == 0) {
-          expect_tx(&rbar[ew], STG_BYTES);
-          tma_load3(&tmC, sbuf, &rbar[ew], n0 + cc, row0, c.b);
+        if (!p.has_res || ch >= 2) {
+          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+          __syncwarp();
+          if (p.has_res && lane == 0) {
+            expect_tx(&rbar[2 * ew + buf], STG_BYTES);
+            tma_load3(&tmC, sbuf, &rbar[2 * ew + buf], n0 + cc, row0, c.b);
+          }
         }
         float v[CW];
         tc::tmem_ld32(tacc + cc, *reinterpret_cast<float(*)[32]>(&v[0]));
@@ -328,8 +345,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         uint8_t* rowp = sbuf + lane * 128;
         const int sw = lane & 7;
         if (p.has_res) {
-          tc::mbar_wait(&rbar[ew], rphase);
-          rphase ^= 1;
+          tc::mbar_wait(&rbar[2 * ew + buf], (rphase >> buf) & 1);
+          rphase ^= 1u << buf;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const uint4 r = *reinterpret_cast<const uint4*>(rowp + ((u ^ sw) << 4));
@@ -367,7 +384,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
           tma_store3(&tmD, sbuf, n0 + cc, row0, zout);
           bulk_commit();
         }
-        if constexpr (F::STG_BUFS == 2) buf ^= 1;
+        buf ^= 1;
       }
       tc::fence_before();
       __syncwarp();
@@ -382,60 +399,125 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   if (warp == 1) tc::tmem_dealloc<F::TMEM_COLS>(tmem);
 }
 
-// Split-K close-out: D = act(alpha * sum_s P[s] + bias) + beta * C.  A block
-// owns 128 consecutive output columns of one row (32 float4 lanes); its 8 warps
-// sum interleaved subsets of the splits (s = w, w + 8, ...) and the 8 partial
-// sums are combined in warp order through shared memory -- a fixed summation
-// order, so results are deterministic, with 8 x 32 loads in flight per block.
+__device__ __forceinline__ void store4(float* p, const float (&r)[4]) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p[j] = r[j];
+  }
+}
+__device__ __forceinline__ void store4(bf16* p, const float (&r)[4]) {
+  if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(tc::pack_bf16(r[0], r[1]), tc::pack_bf16(r[2], r[3]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p[j] = __float2bfloat16(r[j]);
+  }
+}
+
+// Split-K close-out: D = act(alpha * sum_s P[s] + bias) + beta * C, summed
+// in split-index order (a fixed order: results are deterministic).
 template <typename TD>
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t M,
-                                                            int64_t N, TD* D, int64_t ldd, const TD* Cin,
-                                                            int64_t ldc, float alpha, float beta,
-                                                            const float* __restrict__ bias, int relu) {
+__device__ __forceinline__ void splitk_finish(float4 t, int64_t m, int64_t n, TD* D, int64_t ldd, const TD* Cin,
+                                              int64_t ldc, float alpha, float beta, const float* __restrict__ bias,
+                                              int relu) {
+  float r[4] = {t.x * alpha, t.y * alpha, t.z * alpha, t.w * alpha};
+  if (bias) {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(bias + n));
+    r[0] += b.x;
+    r[1] += b.y;
+    r[2] += b.z;
+    r[3] += b.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (relu) r[j] = fmaxf(r[j], 0.f);
+    if (Cin) r[j] = fmaf(beta, to_f(Cin[m * ldc + n + j]), r[j]);
+  }
+  store4(D + m * ldd + n, r);
+}
+
+__device__ __forceinline__ void add4(float4& t, const float4 v) {
+  t.x += v.x;
+  t.y += v.y;
+  t.z += v.z;
+  t.w += v.w;
+}
+
+// Few splits, many outputs (e.g. OPM d(a), d(c): 4 splits of a 128 x 8192
+// plane): one thread per 4 consecutive columns of one row walks all splits
+// with up to eight 16-byte loads in flight.
+template <typename TD>
+__global__ void __launch_bounds__(256) splitk_reduce_quad_kernel(const float* __restrict__ ws, int splits, int64_t M,
+                                                                 int64_t N, TD* D, int64_t ldd, const TD* Cin,
+                                                                 int64_t ldc, float alpha, float beta,
+                                                                 const float* __restrict__ bias, int relu) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nq = N >> 2;
+  if (q >= M * nq) return;
+  const int64_t m = q / nq;
+  const int64_t n = (q - m * nq) * 4;
+  const int64_t plane = M * N;
+  const float* src = ws + m * N + n;
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = 0;
+  for (; k + 8 <= splits; k += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(src + (k + u) * plane));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add4(t, v[u]);
+  }
+  for (; k < splits; ++k) add4(t, __ldcs(reinterpret_cast<const float4*>(src + k * plane)));
+  splitk_finish(t, m, n, D, ldd, Cin, ldc, alpha, beta, bias, relu);
+}
+
+// Many splits, few outputs (weight gradients: up to 64 splits of a small
+// plane): a block owns 32 quads (128 columns) of one row; warp w sums splits
+// w, w + 8, ... (four loads in flight), and the 8 warp partials are added in
+// warp order through shared memory.
+template <typename TD>
+__global__ void __launch_bounds__(256) splitk_reduce_wide_kernel(const float* __restrict__ ws, int splits, int64_t M,
+                                                                 int64_t N, TD* D, int64_t ldd, const TD* Cin,
+                                                                 int64_t ldc, float alpha, float beta,
+                                                                 const float* __restrict__ bias, int relu) {
   __shared__ float4 part[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t cblocks = (N + 127) / 128;
   const int64_t m = blockIdx.x / cblocks;
   const int64_t n = (blockIdx.x % cblocks) * 128 + lane * 4;
-  const bool ok = n < N;  // N % 4 == 0
+  const bool ok = n < N;
   const int64_t plane = M * N;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (ok) {
     const float* src = ws + m * N + n;
-#pragma unroll 4
-    for (int k = w; k < splits; k += 8) {
-      const float4 q = *reinterpret_cast<const float4*>(src + k * plane);
-      acc.x += q.x;
-      acc.y += q.y;
-      acc.z += q.z;
-      acc.w += q.w;
+    int k = w;
+    for (; k + 24 < splits; k += 32) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(reinterpret_cast<const float4*>(src + (k + 8 * u) * plane));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) add4(acc, v[u]);
     }
+    for (; k < splits; k += 8) add4(acc, __ldcs(reinterpret_cast<const float4*>(src + k * plane)));
   }
   part[w][lane] = acc;
   __syncthreads();
   if (w != 0 || !ok) return;
   float4 t = part[0][lane];
 #pragma unroll
-  for (int k = 1; k < 8; ++k) {
-    const float4 q = part[k][lane];
-    t.x += q.x;
-    t.y += q.y;
-    t.z += q.z;
-    t.w += q.w;
-  }
-  float r[4] = {t.x * alpha, t.y * alpha, t.z * alpha, t.w * alpha};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (bias) r[j] += bias[n + j];
-    if (relu) r[j] = fmaxf(r[j], 0.f);
-    if (Cin) r[j] = fmaf(beta, to_f(Cin[m * ldc + n + j]), r[j]);
-    D[m * ldd + n + j] = from_f<TD>(r[j]);
-  }
+  for (int k = 1; k < 8; ++k) add4(t, part[k][lane]);
+  splitk_finish(t, m, n, D, ldd, Cin, ldc, alpha, beta, bias, relu);
 }
 
 // --- host side ----------------------------------------------------------------
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+}  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda);
+// shared with the attention kernels (attention_tc_fwd2.cu)
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -447,11 +529,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+namespace {
+
 // 3-D tiled map over a row-major [z][rows][cols] view (cols contiguous), box
 // {box_cols, box_rows, 1}, 128-byte swizzle.  false when TMA cannot address it.
 bool make_map(CUtensorMap* m, const void* base, bool f32, int64_t cols, int64_t rows, int64_t ld, int64_t zs,
               int64_t nz, int box_cols, int box_rows) {
-  auto enc = encode_fn();
+  auto enc = tmap_encoder();
   if (!enc) return false;
   const int64_t es = f32 ? 4 : 2;
   if (((uintptr_t)base & 15) || (ld * es) % 16 || (zs * es) % 16) return false;
@@ -515,6 +599,14 @@ bool bres_disabled() {  // A/B switch for measurements (EVO_GEMM_BRES=0)
   return e && e[0] == '0';
 }
 
+int forced_bn() {  // tile-width sweeps (tools/gemm_sweep.py): EVO_GEMM_BN=64|128
+  static const int v = [] {
+    const char* e = getenv("EVO_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  return v == 64 || v == 128 ? v : 0;
+}
+
 bool tc_gemm_disabled() {
   static const bool v = [] {
     const char* e = getenv("EVO_DISABLE_TC_GEMM");
@@ -535,14 +627,18 @@ float* gemm_split_ws(cudaStream_t s, size_t* bytes) {
 
 void splitk_reduce(const float* ws, int splits, int64_t M, int64_t N, void* D, int64_t ldd, const void* Cin,
                    int64_t ldc, float alpha, float beta, const float* bias, int relu, int d_dtype, cudaStream_t s) {
-  const int64_t blocks = M * ((N + 127) / 128);
-  EVO_REQUIRE(N % 4 == 0 && blocks < (1ll << 31), EVO_ERR_ARG, "split-K reduce: bad extents");
-  if (d_dtype == EVO_F32)
-    splitk_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(ws, splits, M, N, (float*)D, ldd,
-                                                                 (const float*)Cin, ldc, alpha, beta, bias, relu);
-  else
-    splitk_reduce_kernel<bf16><<<(unsigned)blocks, 256, 0, s>>>(ws, splits, M, N, (bf16*)D, ldd, (const bf16*)Cin,
-                                                                ldc, alpha, beta, bias, relu);
+  EVO_REQUIRE(N % 4 == 0, EVO_ERR_ARG, "split-K reduce: N % 4 != 0");
+  const bool wide = splits >= 8;
+  const int64_t blocks = wide ? M * ((N + 127) / 128) : (M * (N / 4) + 255) / 256;
+  EVO_REQUIRE(blocks < (1ll << 31), EVO_ERR_ARG, "split-K reduce: bad extents");
+#define EVO_SPLITK(KERN, T) \
+  KERN<T><<<(unsigned)blocks, 256, 0, s>>>(ws, splits, M, N, (T*)D, ldd, (const T*)Cin, ldc, alpha, beta, bias, relu)
+  if (d_dtype == EVO_F32) {
+    if (wide) EVO_SPLITK(splitk_reduce_wide_kernel, float); else EVO_SPLITK(splitk_reduce_quad_kernel, float);
+  } else {
+    if (wide) EVO_SPLITK(splitk_reduce_wide_kernel, bf16); else EVO_SPLITK(splitk_reduce_quad_kernel, bf16);
+  }
+#undef EVO_SPLITK
   EVO_LAUNCH_CHECK();
   count_launch(1);
 }
@@ -558,7 +654,13 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   if (M > (1ll << 31) - BM || N > (1ll << 31) - 256 || K > (1ll << 31) - BK) return false;
   const bool f32 = d_dtype == EVO_F32;
   const bool has_res = Cin != nullptr && beta != 0.f;
-  const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  // split-K problems (few output tiles, long K): 128-wide tiles give twice
+  // the tiles per split and halve each CTA's B stream (measured faster on
+  // every weight-gradient shape of the block)
+  if (BN == 256 && batch == 1 && ((M + BM - 1) / BM) * ((N + 255) / 256) < num_sms() && (K + BK - 1) / BK >= 16)
+    BN = 128;
+  if (const int f = forced_bn(); f && f < BN) BN = f;
   Params p{};
   p.M = (int)M;
   p.N = (int)N;
