@@ -61,9 +61,13 @@ struct F2 {
   static constexpr int OFF_K = Q_B, OFF_V = Q_B + K_B, OFF_M = Q_B + 2 * K_B, OFF_G = OFF_M + M_B;
   static constexpr int STAGE = OFF_G + Q_B;       // + G, laid out like Q
   static constexpr int NSTG = (D == 16) ? 3 : 2;
+  // D = 16: the bias joins S on the tensor core, S += 4 I_128 . nb (c^-1/2 = 1/4,
+  // so the identity coefficient is exact); D = 32 adds it in the softmax
+  static constexpr bool MMAB = BIAS && D == 16;
   static constexpr int OFF_BIAS = NSTG * STAGE;
   static constexpr int BIAS_B = BIAS ? 128 * LP * 2 : 0;
-  static constexpr int OFF_AM = OFF_BIAS + BIAS_B;
+  static constexpr int OFF_ID = OFF_BIAS + BIAS_B;  // identity operand (zero padded, 7.5 KB used)
+  static constexpr int OFF_AM = OFF_ID + (MMAB ? 8192 : 0);
   static constexpr int OUT_B = 32 * D * 2;        // one warp's [32 rows x D] output tile
   static constexpr int OFF_OUT = OFF_AM + 4096;   // 8 softmax warps x 2 staging tiles
   static constexpr int OFF_FLAG = OFF_OUT + 8 * 2 * OUT_B;
@@ -144,8 +148,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
       uint4* mz = reinterpret_cast<uint4*>(smem + s * F::STAGE + F::OFF_M);
       for (int e = tid; e < F::M_B / 16; e += F2_THREADS) mz[e] = make_uint4(0u, 0u, 0u, 0u);
     }
-    uint4* z = reinterpret_cast<uint4*>(smem + F::OFF_AM);
-    for (int e = tid; e < 4096 / 16; e += F2_THREADS) z[e] = make_uint4(0u, 0u, 0u, 0u);
+    uint4* z = reinterpret_cast<uint4*>(smem + F::OFF_ID);
+    for (int e = tid; e < (F::OFF_AM + 4096 - F::OFF_ID) / 16; e += F2_THREADS) z[e] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (BIAS) {
     // nb[h, q0 + r, :] -> swizzled row-major tile (zero beyond L)
@@ -153,7 +157,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     const bool vec_ok = (L % 8) == 0;
     for (int e = tid; e < 128 * CPR; e += F2_THREADS) {
       const int r = e / CPR, c = e % CPR;
-      bf16* dst = reinterpret_cast<bf16*>(smem + F::OFF_BIAS + bias_off<LP>(r, c));
+      // MMA operand: MN-major core matrices, (key group c, query group r/8) at
+      // (r/8) * LP/8 * 128 + c * 128, query r % 8 at +16 (r % 8); softmax: swizzled rows
+      const int off = F::MMAB ? (r >> 3) * CPR * 128 + c * 128 + (r & 7) * 16 : bias_off<LP>(r, c);
+      bf16* dst = reinterpret_cast<bf16*>(smem + F::OFF_BIAS + off);
       const int qq = q0 + r, k = c * 8;
       if (qq < L && vec_ok && k + 8 <= L) {
         tc::cp_async16(dst, nb + ((size_t)h * L + qq) * L + k);
@@ -170,6 +177,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     // A_mask [128 x 16] K-major: column 0 ones (core (g, 0) at 256 g, row r at +16 r)
     const int r = tid;
     *reinterpret_cast<bf16*>(smem + F::OFF_AM + (r >> 3) * 256 + (r & 7) * 16) = __float2bfloat16(1.0f);
+  }
+  if (F::MMAB && tid < 16) {
+    // identity operand for query chunk c: base OFF_ID + 3584 - 512 c (LBO 128,
+    // SBO 256) puts its two diagonal cores at OFF_ID + 3584 and + 3968
+    const int r = tid & 7, which = tid >> 3;
+    *reinterpret_cast<bf16*>(smem + F::OFF_ID + 3584 + which * 384 + r * 16 + r * 2) = __float2bfloat16(4.0f);
   }
   if (tid == 0) {
     for (int s = 0; s < F::NSTG; ++s) {
@@ -254,6 +267,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                           tc::sdesc(st + F::OFF_K + m * 2 * LP * 16, LP * 16, 128), id_s, m > 0 ? 1u : 0u);
       tc::mma_bf16_ss_w(tm, tc::sdesc(s0 + F::OFF_AM, 128, 256), tc::sdesc(st + F::OFF_M, (LP / 8) * 128, 128), id_m,
                         1u);
+      if constexpr (F::MMAB) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tc::mma_bf16_ss_w(tm, tc::sdesc(s0 + F::OFF_ID + 3584 - 512 * c, 128, 256),
+                            tc::sdesc(s0 + F::OFF_BIAS + 2 * c * (LP / 8) * 128, (LP / 8) * 128, 128), id_m, 1u);
+      }
       tc::mma_commit_w(&sfull[n & 1]);
     };
     if (nbt > 0) issue_s(0);
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     const float2 sc2 = make_float2(scale, scale), l2e = make_float2(tc::LOG2E_F, tc::LOG2E_F);
     const uint8_t* brow = smem + F::OFF_BIAS + row * LP * 2;
     float bmax = 0.f;  // max of this query row's bias (the tile is the same for every batch)
-    if (BIAS) {
+    if (BIAS && !F::MMAB) {
       bmax = -INFINITY;
       const int nk = L < LP ? L : LP;
       for (int k = 0; k < nk; ++k) {
@@ -332,14 +351,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         // m = (max_k s_k c^-1/2 + max_k nb_k) log2 e bounds every logit from
         // above (a stabiliser only: P and the sum share it, and the backward
         // recomputes P from the saved (m, 1/sum))
-        mx2 = fmaf(fmaxf(mm.x, mm.y), scale, bmax) * tc::LOG2E_F;
+        mx2 = F::MMAB ? (fmaxf(mm.x, mm.y) * scale) * tc::LOG2E_F : fmaf(fmaxf(mm.x, mm.y), scale, bmax) * tc::LOG2E_F;
         if (quarter == 2) F2T(16 * n + 2);
         // ---- pass 2: t = s c^-1/2 + nb (the backward's inner FFMA), P = 2^(t log2e - m),
         // packed bf16 pairs over the consumed columns ----
         const float2 nm = make_float2(-mx2, -mx2);
         auto expo = [&](const float (&x)[32], int c) {
+          constexpr bool SB = BIAS && !F::MMAB;  // bias added here
           uint32_t braw[16];
-          if (BIAS) {
+          if (SB) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint4 u = *reinterpret_cast<const uint4*>(brow + (((c >> 3) + k) ^ (row & 7)) * 16);
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            const float2 nbv = BIAS ? tc::bf16x2_f2(braw[e / 2]) : make_float2(0.f, 0.f);
+            const float2 nbv = SB ? tc::bf16x2_f2(braw[e / 2]) : make_float2(0.f, 0.f);
             const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, nbv);
             const float2 p = ex2x2(__ffma2_rn(t, l2e, nm));
             sum2 = __fadd2_rn(sum2, p);
