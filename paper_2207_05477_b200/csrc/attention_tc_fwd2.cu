@@ -309,6 +309,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(wg * 256);
     const int64_t cb = h * D;
     const float2 sc2 = make_float2(scale, scale), l2e = make_float2(tc::LOG2E_F, tc::LOG2E_F);
+    const float cexp = scale * tc::LOG2E_F;  // the backward's constant (attention_tc_bwd.cu)
+    const float2 ce2 = make_float2(cexp, cexp);
     const uint8_t* brow = smem + F::OFF_BIAS + row * LP * 2;
     float bmax = 0.f;  // max of this query row's bias (the tile is the same for every batch)
     if (BIAS && !F::MMAB) {
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         // m = (max_k s_k c^-1/2 + max_k nb_k) log2 e bounds every logit from
         // above (a stabiliser only: P and the sum share it, and the backward
         // recomputes P from the saved (m, 1/sum))
-        mx2 = F::MMAB ? (fmaxf(mm.x, mm.y) * scale) * tc::LOG2E_F : fmaf(fmaxf(mm.x, mm.y), scale, bmax) * tc::LOG2E_F;
+        mx2 = F::MMAB ? fmaxf(mm.x, mm.y) * cexp : fmaf(fmaxf(mm.x, mm.y), scale, bmax) * tc::LOG2E_F;
         if (quarter == 2) F2T(16 * n + 2);
         // ---- pass 2: t = s c^-1/2 + nb (the backward's inner FFMA), P = 2^(t log2e - m),
         // packed bf16 pairs over the consumed columns ----
@@ -370,8 +372,13 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const float2 nbv = SB ? tc::bf16x2_f2(braw[e / 2]) : make_float2(0.f, 0.f);
-            const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, nbv);
-            const float2 p = ex2x2(__ffma2_rn(t, l2e, nm));
+            float2 p;
+            if constexpr (F::MMAB) {  // S = s + 4 nb + mask: x = S c^-1/2 log2e - m in one FFMA
+              p = ex2x2(__ffma2_rn(make_float2(x[e], x[e + 1]), ce2, nm));
+            } else {
+              const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, nbv);
+              p = ex2x2(__ffma2_rn(t, l2e, nm));
+            }
             sum2 = __fadd2_rn(sum2, p);
             pk[e / 2] = tc::pack_bf16(p.x, p.y);
           }
