@@ -330,16 +330,22 @@ def run_ours(args):
         grid = GridConfig.for_world(world)
         bp_comm, world_comm = build_groups(grid)
 
+    comms = []
+    if grid is not None and grid.dap > 1:
+        comms = [dap_comm, world_comm]
+        trainer.attach_parallel(lambda e, f, n, s: dap_step(e, f, world_comm, grid, n_cycles=n, step=s)[0], comms)
+    elif grid is not None and grid.bp == 2:
+        comms = [bp_comm, world_comm]
+        trainer.attach_parallel(lambda e, f, n, s: bp_step(e, f, bp_comm, world_comm, grid, cfg.n_blocks,
+                                                           step=s, n_cycles=n), comms)
+    elif grid is not None:
+        comms = [world_comm]
+        trainer.attach_parallel(lambda e, f, n, s: dp_step(e, f, world_comm, grid, n_cycles=n, step=s), comms)
+    step_no = [0]
+
     def eager_step():
-        if grid is None:
-            loss, _ = trainer.engine.forward_backward(trainer.feats, 1)
-        elif grid.dap > 1:
-            loss, _ = dap_step(trainer.engine, trainer.feats, world_comm, grid)
-        elif grid.bp == 2:
-            loss = bp_step(trainer.engine, trainer.feats, bp_comm, world_comm, grid, cfg.n_blocks)
-        else:
-            loss = dp_step(trainer.engine, trainer.feats, world_comm, grid)
-        trainer.store.step()
+        loss = trainer.device_step(1, h2d=False, step=step_no[0])
+        step_no[0] += 1
         return loss
 
     use_graph = not args.no_graph and world == 1
@@ -400,6 +406,17 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = float(t[0]), float(t[1])
 
+    comm = None
+    if comms:
+        from paper_2207_05477_b200.parallel import dump_comm_csv
+        recs = trainer.comm_records()
+        comm = {"records": len(recs), "steps_run": step_no[0], "records_per_step": len(recs) / max(1, step_no[0]),
+                "bytes_per_step": sum(r.bytes for r in recs) / max(1, step_no[0])}
+        if args.comm_csv:   # the reference's trace columns (src/harness.py:91-101), one file per rank
+            path = args.comm_csv.format(rank=rank)
+            os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+            dump_comm_csv(recs, path)
+            comm["csv"] = path
     samples = args.steps * (grid.dp if grid is not None else 1)  # a BP pair / DAP group shares one sample
     value = samples / dev_s
     e2e_value = samples / e2e_s
@@ -473,7 +490,7 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": 4},
                 "gpu_launches": launches_per_step * args.steps,
-                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu_baseline,
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu_baseline, "comm": comm,
                 "loss_last": losses[-1] if losses else None,
                 "loss_finite": bool(losses) and all(np.isfinite(losses))}
         if not line["loss_finite"]:
@@ -518,6 +535,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override n_blocks (debug only)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm-csv", default=None,
+                    help="multi-rank runs: write each rank's CommRecord trace here ({rank} is substituted)")
     ap.add_argument("--dap", type=int, default=1,
                     help="N>1: Dynamic Axial Parallelism groups of this size (dp = N / dap) "
                          "instead of the default BP x DP grid")

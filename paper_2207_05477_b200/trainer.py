@@ -120,14 +120,32 @@ class Trainer:
         feats = feats or make_features(self.cfg, step_feature_seed(self.plan.seed, step))
         self.host.fill(feats)
 
-    def device_step(self, n_cycles: int, h2d: bool = True):
+    def attach_parallel(self, step_fn, comms):
+        """Route ``device_step`` through a multi-rank step -- ``step_fn(engine,
+        feats, n_cycles, step)`` returning the device loss after the gradient
+        exchange (parallel.bp_step / dp_step, dap.dap_step) -- and count the
+        CommRecords its ``comms`` endpoints log as the step's ``comm_records``
+        (src/trainer.py:192-247, src/harness.py:79-101)."""
+        self.parallel_step = step_fn
+        self.comms = list(comms)
+
+    def comm_records(self):
+        """Every CommRecord logged so far, all endpoints (dump with
+        parallel.dump_comm_csv)."""
+        return [r for c in getattr(self, "comms", ()) for r in c.records]
+
+    def device_step(self, n_cycles: int, h2d: bool = True, step: int = 0):
         """H2D of the staged features (unless ``h2d`` is False: the features
         already in HBM are used), fwd+bwd, optimizer; returns the device loss
         tensor (no host sync)."""
         if h2d:
             self.feats.copy_from_host(self.host)
-        loss, _ = self.engine.forward_backward(self.feats, n_cycles,
-                                               recompute=self.plan.recompute_on)
+        par = getattr(self, "parallel_step", None)
+        if par is not None:   # the step's own collective already synced the grad region
+            loss = par(self.engine, self.feats, n_cycles, step)
+        else:
+            loss, _ = self.engine.forward_backward(self.feats, n_cycles,
+                                                   recompute=self.plan.recompute_on)
         self.store.grad_sync(None)
         self.store.step()
         return loss
@@ -175,7 +193,8 @@ class Trainer:
         dev = torch.device(self.store.device)
         live_before = torch.cuda.memory_allocated(dev)
         torch.cuda.reset_peak_memory_stats(dev)
-        loss_t = self.device_step(n_rec)
+        recs_before = len(self.comm_records())
+        loss_t = self.device_step(n_rec, step=step)
         loss = float(loss_t.item())
         if not math.isfinite(loss):
             raise TrainingAborted(step, f"non-finite loss {loss!r}")
@@ -183,7 +202,7 @@ class Trainer:
         launches = {k: self.store.launches.counts[k] - launches_before.get(k, 0)
                     for k in self.store.launches.PHASES}
         metrics = {"step": step, "loss": loss, "grad_norm": grad_norm, "n_recycles": n_rec,
-                   "launches": launches, "comm_records": 0,
+                   "launches": launches, "comm_records": len(self.comm_records()) - recs_before,
                    "ledger_peak_bytes": int(torch.cuda.max_memory_allocated(dev) - live_before),
                    "op_count": int(_lib.launch_count() - ops_before),
                    "blocks_executed": self.cfg.n_blocks * n_rec}

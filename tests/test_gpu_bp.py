@@ -97,3 +97,38 @@ def test_bp_matches_unsharded(world, dtype):
     block = [r for r in map(tuple, res["recs"]) if r[0] in ("opm", "msa_stack", "pair_stack")]
     assert len(block) == 4 * CFG["n_blocks"]
     assert sum(1 for r in block if r[1] == "broadcast") == 3 * CFG["n_blocks"]
+
+
+@pytest.mark.timeout(900)
+def test_bench_multirank_bp_comm_trace(tmp_path):
+    """``bench.py --gpus 2`` spawns its own ranks (torchrun-equivalent, here
+    two ranks sharing the box's one GPU over gloo) and runs the BP step through
+    Trainer.attach_parallel; each rank's CommRecord trace is written with the
+    reference's CSV columns (src/harness.py:91-101) and the JSON line carries
+    the per-step record count: 3 broadcasts + 1 all-reduce per block, the
+    closing d(msa) broadcast and the grad all-reduce."""
+    import csv
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pattern = str(tmp_path / "comm_r{rank}.csv")
+    env = dict(os.environ, EVO_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+                          "--warmup", "1", "--blocks", "2", "--no-cpu-baseline", "--comm-csv", pattern],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=840)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dp1xbp2"
+    comm = line["comm"]
+    per_block, closing = 4, 2          # opm, msa', pair' broadcasts + d(pair) all-reduce; msa_grad + grad_sync
+    assert comm["records_per_step"] == 2 * per_block + closing, comm
+    for r in range(2):
+        rows = list(csv.reader(open(pattern.format(rank=r))))
+        assert rows[0] == ["step", "phase", "group_axis", "group_id", "seq", "primitive", "bytes", "module"]
+        body = rows[1:]
+        assert len(body) == comm["records"]
+        assert {b[1] for b in body} == {"fwd", "bwd", "grad-sync"}
+        fwd = [b for b in body if b[0] == "0" and b[1] == "fwd"]
+        assert [b[7] for b in fwd] == ["opm", "msa_stack", "pair_stack"] * 2
