@@ -35,6 +35,18 @@ METRIC = "Evoformer fwd+bwd samples/s (N_res=256,N_seq=128 bf16) 1-8 B200; % of 
 SHAPE = dict(n_blocks=48, n_seq=128, n_res=256, c_m=256, c_z=128, heads=8, opm_dim=32)
 
 
+def bench_shape(args):
+    """The workload: the initial-training shape; ``--trimul`` adds the
+    TriangleMultiplication extension (outgoing + incoming, c_hidden = c_z) to
+    every block -- SURVEY A14, 31.14 TFLOP per sample."""
+    shape = dict(SHAPE)
+    if getattr(args, "trimul", False):
+        shape["trimul"] = True
+    if getattr(args, "blocks", 0):
+        shape["n_blocks"] = args.blocks
+    return shape
+
+
 def flops_per_block_fwd(S, R, cm, cz, H, k, trimul=False, ch=None):
     """Algorithmic forward FLOPs per block."""
     N = S * R
@@ -52,7 +64,8 @@ def flops_per_block_fwd(S, R, cm, cz, H, k, trimul=False, ch=None):
 
 def sample_flops(shape):
     return 3 * shape["n_blocks"] * flops_per_block_fwd(
-        shape["n_seq"], shape["n_res"], shape["c_m"], shape["c_z"], shape["heads"], shape["opm_dim"])
+        shape["n_seq"], shape["n_res"], shape["c_m"], shape["c_z"], shape["heads"], shape["opm_dim"],
+        trimul=shape.get("trimul", False))
 
 
 def load_peaks():
@@ -155,7 +168,8 @@ def cpu_block_sample(shape, threads=None, reps=1):
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     from oracle import evoformer_np as O
     cfg = O.ModelConfig(n_blocks=1, n_seq=shape["n_seq"], n_res=shape["n_res"], c_m=shape["c_m"],
-                        c_z=shape["c_z"], heads=shape["heads"], opm_dim=shape["opm_dim"])
+                        c_z=shape["c_z"], heads=shape["heads"], opm_dim=shape["opm_dim"],
+                        trimul=shape.get("trimul", False))
     P = O.init_params(cfg, 32)
     feats = O.make_features(cfg, 3)
     masks = O.make_masks(feats)
@@ -175,6 +189,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    SHAPE = bench_shape(args)
     cores = os.cpu_count() or 1
     times = []
     for _ in range(args.warmup):
@@ -264,6 +279,16 @@ def kernel_candidates(trainer):
     fl2 = S * H * 4 * R * R * Dm
     t = timeit(lambda: ops.attn_fwd(q2, m2, R, 1, bias, torch.zeros(cm, device=dev), S, R, H, Dm, R, 1))
     out.append(("attn_fwd[row]", t, nblk, fl2, "TFLOP/s"))
+    if cfg.trimul:
+        # TriangleMultiplication contraction: per channel c, o = a b^T over the
+        # residue axis (R x R x R), 2 R^3 flop per channel, channel-batched
+        ch = cfg.c_hidden_mul
+        a = (torch.randn(ch, R * R, device=dev) * 0.5).to(dt)
+        b = (torch.randn(ch, R * R, device=dev) * 0.5).to(dt)
+        o = torch.empty(ch, R * R, device=dev, dtype=dt)
+        A0, B0, O0 = a[0].view(R, R), b[0].view(R, R), o[0].view(R, R)
+        t = timeit(lambda: ops.gemm_batched(A0, B0, O0, ch, R * R, R * R, R * R, tb=True))
+        out.append(("trimul_contraction", t, 6 * nblk, 2 * R ** 3 * ch, "TFLOP/s"))
     # LayerNorm (bandwidth-bound): read + write storage bytes
     x = torch.randn(R * R, cz, device=dev).to(dt)
     g1, b1 = torch.ones(cz, device=dev), torch.zeros(cz, device=dev)
@@ -300,9 +325,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group(backend)
     _lib.lib()
-    shape = dict(SHAPE)
-    if args.blocks:
-        shape["n_blocks"] = args.blocks
+    shape = bench_shape(args)
     cfg = ModelConfig(**shape)
     plan = ExecutionPlan(act_dtype="bf16", seed=32, fixed_recycles=1)
     trainer = Trainer.create(cfg, plan)
@@ -482,7 +505,9 @@ def run_ours(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
                 "data": "synthetic (reference PRNG features, random-init weights)",
                 "config": {"workload": "48-block Evoformer training step (fwd+bwd+fused Adam), "
-                                       "initial shape, 1 recycle", **shape,
+                                       "initial shape, 1 recycle"
+                                       + (", TriangleMultiplication in every block" if shape.get("trimul") else ""),
+                           **shape,
                            "parallelism": ((f"dp{grid.dp}xdap{grid.dap}" if grid.dap > 1 else
                                             f"dp{grid.dp}xbp{grid.bp}") if grid is not None else "single"),
                            "l2": "working set (~tens of GB of activations) >> 126 MB L2",
@@ -535,6 +560,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=0, help="override n_blocks (debug only)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trimul", action="store_true",
+                    help="workload with the TriangleMultiplication extension in every block (SURVEY A14)")
     ap.add_argument("--comm-csv", default=None,
                     help="multi-rank runs: write each rank's CommRecord trace here ({rank} is substituted)")
     ap.add_argument("--dap", type=int, default=1,
