@@ -56,15 +56,21 @@ constexpr int SMEM_LIMIT = 232448;     // 227 KB of dynamic shared memory per CT
 // loaded once and stays in shared memory; only A k-blocks stream through
 // the ring.  For the K <= 256 projections this halves-to-thirds the bytes
 // each MMA waits for (the streamed operand is the MMA's latency bound).
-template <int BN, bool BRES>
+// CG2 (CTA pair, tcgen05 cta_group::2): a 256 x BN tile per pair; each CTA
+// holds its 128 rows of A and half (BN/2 columns) of B, the leader's MMAs
+// read both CTAs' halves and each CTA's TMEM receives its 128 rows x BN.
+template <int BN, bool BRES, bool CG2 = false>
 struct Cfg {
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (CG2 ? BN / 2 : BN) * BK * 2;
   static constexpr int BRES_BYTES = BRES ? KB_RES * B_BYTES : 0;
   static constexpr int STAGE = BRES ? A_BYTES : A_BYTES + B_BYTES;
-  static constexpr int STG_BUFS = 2;  // epilogue staging buffers per warp (store i+1 staged while i drains)
+  // epilogue staging buffers per warp: two (store i+1 staged while i drains)
+  // for the short-K B-resident tiles, one elsewhere -- long-K tiles spend the
+  // shared memory better on a deeper operand ring (more bytes in flight)
+  static constexpr int STG_BUFS = BRES ? 2 : 1;
   static constexpr int STG_TOTAL = EPI_WARPS * STG_BUFS * STG_BYTES;
   static constexpr int FIT = (SMEM_LIMIT - 1024 - 512 - BRES_BYTES - STG_TOTAL) / STAGE;
-  static constexpr int STAGES = BRES ? (FIT > 8 ? 8 : FIT) : (BN == 256 ? 3 : (BN == 128 ? 5 : 6));
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
   static constexpr int OFF_RING = BRES_BYTES;
   static constexpr int OFF_STG = OFF_RING + STAGES * STAGE;
   static constexpr int OFF_BAR = OFF_STG + STG_TOTAL;
@@ -100,6 +106,62 @@ __device__ __forceinline__ void tma_store3(const CUtensorMap* m, const void* src
                "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(src))
                : "memory");
 }
+// TMA load whose completion is signalled on the pair leader's mbarrier
+// (``bar_cluster`` is a shared::cluster address, from mapa)
+__device__ __forceinline__ void tma_load3_pair(const CUtensorMap* m, void* dst, uint32_t bar_cluster, int c0, int c1,
+                                               int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank0(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(tc::smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mma2_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// completion of the pair's MMAs arrives on ``bar`` in both CTAs
+__device__ __forceinline__ void mma2_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          tc::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc2(uint32_t* slot_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(slot_smem)),
+               "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS));
+}
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -137,25 +199,27 @@ struct TileCoord {
   int b, m0, n0, kb0, kb1, split;
 };
 
-__device__ __forceinline__ TileCoord decode(const Params& p, int t) {
-  const int per_split = p.batch * p.n_mt * p.n_nt;
+// pair mode: tiles count M-tile pairs; ``crank`` picks the CTA's M-tile
+__device__ __forceinline__ TileCoord decode(const Params& p, int t, int pair = 0, int crank = 0) {
+  const int n_m = pair ? (p.n_mt + 1) / 2 : p.n_mt;
+  const int per_split = p.batch * n_m * p.n_nt;
   TileCoord c;
   c.split = t / per_split;
   int r = t - c.split * per_split;
-  c.b = r / (p.n_mt * p.n_nt);
-  r -= c.b * p.n_mt * p.n_nt;
-  c.m0 = (r / p.n_nt) * BM;
+  c.b = r / (n_m * p.n_nt);
+  r -= c.b * n_m * p.n_nt;
+  c.m0 = (pair ? 2 * (r / p.n_nt) + crank : r / p.n_nt) * BM;
   c.n0 = (r % p.n_nt);
   c.kb0 = c.split * p.kb_per_split;
   c.kb1 = min(p.kblocks, c.kb0 + p.kb_per_split);
   return c;
 }
 
-template <int BN, bool OUT_F32, bool BRES>
+template <int BN, bool OUT_F32, bool BRES, bool CG2>
 __global__ void __launch_bounds__(GT_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmC, Params p) {
-  using F = Cfg<BN, BRES>;
+  using F = Cfg<BN, BRES, CG2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + F::OFF_BAR);
@@ -166,6 +230,11 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   uint64_t* bfull = rbar + 2 * EPI_WARPS;  // resident B landed (BRES)
   uint32_t* slot = reinterpret_cast<uint32_t*>(bfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // CG2: CTA pair on adjacent M-tiles; rank 0 (the leader) issues the MMAs
+  // and owns the smem-full and accumulator-empty barriers the pair shares
+  const int crank = CG2 ? (int)cluster_rank() : 0;
+  const int cid = CG2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncl = CG2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -178,14 +247,18 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
-      tc::mbar_init(&tempty[a], (BN == 64 && !OUT_F32) ? EPI_WARPS / 2 : EPI_WARPS);
+      tc::mbar_init(&tempty[a], ((BN == 64 && !OUT_F32) ? EPI_WARPS / 2 : EPI_WARPS) * (CG2 ? 2 : 1));
     }
     for (int w = 0; w < 2 * EPI_WARPS; ++w) tc::mbar_init(&rbar[w], 1);
     tc::mbar_init(bfull, 1);
   }
-  if (warp == 1) tc::tmem_alloc<F::TMEM_COLS>(slot);
+  if (warp == 1) {
+    if constexpr (CG2) tmem_alloc2<F::TMEM_COLS>(slot);
+    else tc::tmem_alloc<F::TMEM_COLS>(slot);
+  }
   tc::fence_before();
   __syncthreads();
+  if constexpr (CG2) cluster_sync_all();  // the leader's barriers exist before the peer signals them
   tc::fence_after();
   const uint32_t tmem = *slot;
 
@@ -207,21 +280,41 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-        const TileCoord c = decode(p, t);
+      for (int t = cid; t < p.tiles; t += ncl) {
+        const TileCoord c = decode(p, t, CG2, crank);
         const int n0 = c.n0 * BN;
         for (int kb = c.kb0; kb < c.kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          expect_tx(&full[stage], F::STAGE);
           uint8_t* sa = smem + F::OFF_RING + stage * F::STAGE;
           const int k0 = kb * BK;
-          if (!p.a_mn) {
-            tma_load3(&tmA, sa, &full[stage], k0, c.m0, c.b);
+          if constexpr (CG2) {
+            // both CTAs' halves complete on the leader's full barrier
+            const uint32_t fb = mapa_rank0(&full[stage]);
+            if (crank == 0) expect_tx(&full[stage], 2 * F::STAGE);
+            if (!p.a_mn) {
+              tma_load3_pair(&tmA, sa, fb, k0, c.m0, c.b);
+            } else {
+              tma_load3_pair(&tmA, sa, fb, c.m0, k0, c.b);
+              tma_load3_pair(&tmA, sa + 8192, fb, c.m0 + 64, k0, c.b);
+            }
+            uint8_t* sb = sa + A_BYTES;
+            const int nh = n0 + crank * (BN / 2);  // this CTA's half of the N-tile
+            if (!p.b_mn) {
+              tma_load3_pair(&tmB, sb, fb, k0, nh, c.b);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 128; ++i) tma_load3_pair(&tmB, sb + i * 8192, fb, nh + 64 * i, k0, c.b);
+            }
           } else {
-            tma_load3(&tmA, sa, &full[stage], c.m0, k0, c.b);
-            tma_load3(&tmA, sa + 8192, &full[stage], c.m0 + 64, k0, c.b);
+            expect_tx(&full[stage], F::STAGE);
+            if (!p.a_mn) {
+              tma_load3(&tmA, sa, &full[stage], k0, c.m0, c.b);
+            } else {
+              tma_load3(&tmA, sa, &full[stage], c.m0, k0, c.b);
+              tma_load3(&tmA, sa + 8192, &full[stage], c.m0 + 64, k0, c.b);
+            }
+            if constexpr (!BRES) load_b(sa + A_BYTES, &full[stage], k0, n0, c.b);
           }
-          if constexpr (!BRES) load_b(sa + A_BYTES, &full[stage], k0, n0, c.b);
           if (++stage == F::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -230,37 +323,45 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one elected lane) ----------------
-    const uint32_t idesc = tc::idesc_bf16(BM, BN, p.a_mn != 0, p.b_mn != 0);
+    // ---------------- MMA issuer (one elected lane; CG2: the leader only) ----------------
+    const uint32_t idesc = tc::idesc_bf16(CG2 ? 2 * BM : BM, BN, p.a_mn != 0, p.b_mn != 0);
     if constexpr (BRES) {
       tc::mbar_wait(bfull, 0);
       tc::fence_after();
     }
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      const TileCoord c = decode(p, t);
-      const int acc = it & 1;
-      tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);  // epilogue has drained this accumulator
-      tc::fence_after();
-      const uint32_t dacc = tmem + (uint32_t)(acc * BN);
-      for (int kb = c.kb0; kb < c.kb1; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
+    if (!CG2 || crank == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < p.tiles; t += ncl, ++it) {
+        const TileCoord c = decode(p, t, CG2, crank);
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);  // epilogue(s) drained this accumulator
         tc::fence_after();
-        const uint32_t sa = tc::smem_u32(smem + F::OFF_RING + stage * F::STAGE);
-        const uint32_t sb = BRES ? tc::smem_u32(smem + kb * F::B_BYTES) : sa + A_BYTES;
+        const uint32_t dacc = tmem + (uint32_t)(acc * BN);
+        for (int kb = c.kb0; kb < c.kb1; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::fence_after();
+          const uint32_t sa = tc::smem_u32(smem + F::OFF_RING + stage * F::STAGE);
+          const uint32_t sb = BRES ? tc::smem_u32(smem + kb * F::B_BYTES) : sa + A_BYTES;
 #pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks)
-          tc::mma_bf16_ss_w(dacc, op_desc(sa, p.a_mn, ks), op_desc(sb, p.b_mn, ks), idesc,
-                            (kb > c.kb0 || ks > 0) ? 1u : 0u);
-        tc::mma_commit_w(&empty[stage]);  // the stage is free once these MMAs have read it
-        if (++stage == F::STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int ks = 0; ks < BK / 16; ++ks) {
+            const uint32_t accum = (kb > c.kb0 || ks > 0) ? 1u : 0u;
+            if constexpr (CG2)
+              mma2_ss_w(dacc, op_desc(sa, p.a_mn, ks), op_desc(sb, p.b_mn, ks), idesc, accum);
+            else
+              tc::mma_bf16_ss_w(dacc, op_desc(sa, p.a_mn, ks), op_desc(sb, p.b_mn, ks), idesc, accum);
+          }
+          if constexpr (CG2) mma2_commit_w(&empty[stage]);  // both CTAs' stage is free once read
+          else tc::mma_commit_w(&empty[stage]);             // the stage is free once these MMAs have read it
+          if (++stage == F::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
+        if constexpr (CG2) mma2_commit_w(&tfull[acc]);  // accumulator complete, in both CTAs' TMEM
+        else tc::mma_commit_w(&tfull[acc]);
       }
-      tc::mma_commit_w(&tfull[acc]);  // accumulator complete
     }
   } else {
     // ---------------- epilogue ----------------
@@ -276,8 +377,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     int buf = 0;
     uint32_t rphase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, ++it) {
-      const TileCoord c = decode(p, t);
+    for (int t = cid; t < p.tiles; t += ncl, ++it) {
+      const TileCoord c = decode(p, t, CG2, crank);
       const int acc = it & 1;
       const int n0 = c.n0 * BN;
       const int row0 = c.m0 + quarter * 32;
@@ -288,7 +389,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       if (p.has_res) {
         if (lane == 0) {
           bulk_wait_all_read();  // both staging buffers free
-          for (int j = 0; j < nchunk && j < 2; ++j) {
+          for (int j = 0; j < nchunk && j < F::STG_BUFS; ++j) {
             const int b = buf ^ j;
             expect_tx(&rbar[2 * ew + b], STG_BYTES);
             tma_load3(&tmC, stg + b * STG_BYTES, &rbar[2 * ew + b], n0 + half * HCOLS + j * CW, row0, c.b);
@@ -303,8 +404,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       for (int ch = 0; ch < nchunk; ++ch) {
         const int cc = half * HCOLS + ch * CW;
         uint8_t* sbuf = stg + buf * STG_BYTES;
-        if (!p.has_res || ch >= 2) {
-          if (lane == 0) bulk_wait_read<1>();  // the store that last read this buffer is done
+        if (!p.has_res || ch >= F::STG_BUFS) {
+          if (lane == 0) bulk_wait_read<F::STG_BUFS - 1>();  // the store that last read this buffer is done
           __syncwarp();
           if (p.has_res && lane == 0) {
             expect_tx(&rbar[2 * ew + buf], STG_BYTES);
@@ -384,19 +485,26 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
           tma_store3(&tmD, sbuf, n0 + cc, row0, zout);
           bulk_commit();
         }
-        buf ^= 1;
+        if constexpr (F::STG_BUFS == 2) buf ^= 1;
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);  // accumulator may be overwritten
+      if (lane == 0) {  // accumulator may be overwritten (CG2: on the leader's barrier)
+        if constexpr (CG2) mbar_arrive_cluster(mapa_rank0(&tempty[acc]));
+        else tc::mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait_all();
     }
   }
   tc::fence_before();
   __syncthreads();
+  if constexpr (CG2) cluster_sync_all();  // neither CTA leaves while the pair's MMAs / signals are in flight
   tc::fence_after();
-  if (warp == 1) tc::tmem_dealloc<F::TMEM_COLS>(tmem);
+  if (warp == 1) {
+    if constexpr (CG2) tmem_dealloc2<F::TMEM_COLS>(tmem);
+    else tc::tmem_dealloc<F::TMEM_COLS>(tmem);
+  }
 }
 
 __device__ __forceinline__ void store4(float* p, const float (&r)[4]) {
@@ -580,18 +688,41 @@ SplitWs& split_ws(cudaStream_t s) {
 
 int64_t g_tc_gemms = 0;  // tensor-core GEMMs launched (evo_gemm_tc_launches)
 
-template <int BN, bool OUT_F32, bool BRES>
+template <int BN, bool OUT_F32, bool BRES, bool CG2 = false>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& d, const CUtensorMap& c, const Params& p,
             int grid, cudaStream_t s) {
-  auto k = gemm_tc_kernel<BN, OUT_F32, BRES>;
+  using F = Cfg<BN, BRES, CG2>;
+  auto k = gemm_tc_kernel<BN, OUT_F32, BRES, CG2>;
   static std::once_flag once;
-  std::call_once(once, [&] {
-    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, BRES>::SMEM));
-  });
-  k<<<grid, GT_THREADS, Cfg<BN, BRES>::SMEM, s>>>(a, b, d, c, p);
+  std::call_once(once, [&] { EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM)); });
+  if constexpr (CG2) {  // CTA pairs: a 2 x 1 x 1 cluster
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(GT_THREADS);
+    cfg.dynamicSmemBytes = F::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EVO_CUDA(cudaLaunchKernelEx(&cfg, k, a, b, d, c, p));
+  } else {
+    k<<<grid, GT_THREADS, F::SMEM, s>>>(a, b, d, c, p);
+  }
   EVO_LAUNCH_CHECK();
   count_launch(1);
   ++g_tc_gemms;
+}
+
+bool cg2_disabled() {  // A/B switch (EVO_GEMM_CG2=0): single-CTA kernels only
+  static const bool v = [] {
+    const char* e = getenv("EVO_GEMM_CG2");
+    return e && e[0] == '0';
+  }();
+  return v;
 }
 
 bool bres_disabled() {  // A/B switch for measurements (EVO_GEMM_BRES=0)
@@ -700,6 +831,16 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   splits = (p.kblocks + p.kb_per_split - 1) / p.kb_per_split;
   p.partial = splits > 1 ? 1 : 0;
   p.tiles = (int)(base * splits);
+  // B resident: short K, several M-tiles per CTA; the grid is a multiple of
+  // the N-tile count so each CTA keeps one N-tile (tile t -> n = t % n_nt)
+  const bool bres = !p.partial && BN >= 128 && p.kblocks <= KB_RES && p.n_nt <= nsm &&
+                    p.tiles >= 2 * nsm && !bres_disabled();
+  // otherwise CTA pairs (tcgen05 cta_group::2, 256 x BN per pair, each CTA
+  // receiving half the B bytes per k-block) for the 256-wide, K >= 512,
+  // unsplit problems: measured 5-9% faster there (tools/gemm_shapes.py),
+  // neutral-to-slower for 128-wide tiles, short K and split-K partials
+  const bool cg2 = !bres && BN == 256 && !p.partial && p.kblocks >= 8 && p.n_mt >= 2 && !cg2_disabled();
+  if (cg2) p.tiles = (int)((int64_t)batch * ((p.n_mt + 1) / 2) * p.n_nt * splits);
 
   CUtensorMap ma, mb, md, mc;
   // A: K-major [M, K] (lda) or MN-major [K, M]
@@ -709,7 +850,7 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
     return false;
   }
   if (tb) {
-    if (!make_map(&mb, B, false, K, N, ldb, sb, batch, 64, BN)) return false;
+    if (!make_map(&mb, B, false, K, N, ldb, sb, batch, 64, cg2 ? BN / 2 : BN)) return false;
   } else if (!make_map(&mb, B, false, N, K, ldb, sb, batch, 64, BK)) {
     return false;
   }
@@ -728,24 +869,22 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   }
   int grid = (int)(p.tiles < nsm ? p.tiles : nsm);
   const bool out32 = p.partial || f32;
-  // B resident: short K, several M-tiles per CTA; the grid is a multiple of
-  // the N-tile count so each CTA keeps one N-tile (tile t -> n = t % n_nt)
-  const bool bres = !p.partial && BN >= 128 && p.kblocks <= KB_RES && p.n_nt <= nsm &&
-                    p.tiles >= 2 * nsm && !bres_disabled();
   if (bres) grid = (nsm / p.n_nt) * p.n_nt;
+  if (cg2) grid = 2 * (p.tiles < nsm / 2 ? p.tiles : nsm / 2);
+#define EVO_GL(BNV, BR, C2) \
+  (out32 ? launch<BNV, true, BR, C2>(ma, mb, md, mc, p, grid, s) : launch<BNV, false, BR, C2>(ma, mb, md, mc, p, grid, s))
   if (BN == 256) {
-    if (bres)
-      out32 ? launch<256, true, true>(ma, mb, md, mc, p, grid, s) : launch<256, false, true>(ma, mb, md, mc, p, grid, s);
-    else
-      out32 ? launch<256, true, false>(ma, mb, md, mc, p, grid, s) : launch<256, false, false>(ma, mb, md, mc, p, grid, s);
+    if (bres) EVO_GL(256, true, false);
+    else if (cg2) EVO_GL(256, false, true);
+    else EVO_GL(256, false, false);
   } else if (BN == 128) {
-    if (bres)
-      out32 ? launch<128, true, true>(ma, mb, md, mc, p, grid, s) : launch<128, false, true>(ma, mb, md, mc, p, grid, s);
-    else
-      out32 ? launch<128, true, false>(ma, mb, md, mc, p, grid, s) : launch<128, false, false>(ma, mb, md, mc, p, grid, s);
+    if (bres) EVO_GL(128, true, false);
+    else if (cg2) EVO_GL(128, false, true);
+    else EVO_GL(128, false, false);
   } else {
-    out32 ? launch<64, true, false>(ma, mb, md, mc, p, grid, s) : launch<64, false, false>(ma, mb, md, mc, p, grid, s);
+    EVO_GL(64, false, false);
   }
+#undef EVO_GL
   if (p.partial) splitk_reduce(wsp, splits, M, N, D, ldd, has_res ? Cin : nullptr, ldc, alpha, beta, bias, relu,
                                d_dtype, s);
   return true;
