@@ -759,7 +759,9 @@ float* gemm_split_ws(cudaStream_t s, size_t* bytes) {
 void splitk_reduce(const float* ws, int splits, int64_t M, int64_t N, void* D, int64_t ldd, const void* Cin,
                    int64_t ldc, float alpha, float beta, const float* bias, int relu, int d_dtype, cudaStream_t s) {
   EVO_REQUIRE(N % 4 == 0, EVO_ERR_ARG, "split-K reduce: N % 4 != 0");
-  const bool wide = splits >= 8;
+  // thread per quad when that alone fills the GPU (each thread then keeps up to
+  // eight split loads in flight); the split-parallel layout for few outputs
+  const bool wide = splits >= 8 && M * (N / 4) < (int64_t)num_sms() * 128;
   const int64_t blocks = wide ? M * ((N + 127) / 128) : (M * (N / 4) + 255) / 256;
   EVO_REQUIRE(blocks < (1ll << 31), EVO_ERR_ARG, "split-K reduce: bad extents");
 #define EVO_SPLITK(KERN, T) \
