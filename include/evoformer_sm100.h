@@ -288,6 +288,24 @@ int evo_adam_clip_ema_dev(float* p, const float* g, float* m, float* v, float* e
                           float lr, float b1, float omb1, float b2, float omb2, float eps,
                           const float* bc, float decay, float omdecay, void* stream);
 
+/* ---- unfused gated-attention baseline (src/attention.py:78-115) -----------
+ * gated_attention_reference: the reference's fine-grained composition with
+ * materialised logits, the oracle of the fused operator
+ * (tests/test_acceptance.py:46-71); fp32; its GEMMs are evo_gemm.
+ * x [BS, H, R, R] logits -> softmax_j(x + (mask[bs*mask_sb + j*mask_sl] - 1)*1e9
+ * + nb[h, i, j]) in place (:99-106; nb nullable). */
+int evo_softmax_masked_rows(float* x, const float* mask, int64_t mask_sb, int64_t mask_sl, const float* nb,
+                            int64_t BS, int64_t H, int64_t R, void* stream);
+/* g <- w * (g - sum_j g * w) per row of R (softmax backward, in place) */
+int evo_softmax_rows_bwd(const float* w, float* g, int64_t rows, int64_t R, void* stream);
+/* gate = sigmoid(gp), gated = ctx * gate (:111-113), elementwise over n */
+int evo_gate_fwd(const float* gp, const float* ctx, float* gate, float* gated, int64_t n, void* stream);
+/* dctx = dgated * gate, dgp = dgated * ctx * gate * (1 - gate) */
+int evo_gate_bwd(const float* dgated, const float* gate, const float* ctx, float* dctx, float* dgp, int64_t n,
+                 void* stream);
+/* out[c] (+)= sum_r x[r, c] over [rows, cols] fp32, rows in order (deterministic) */
+int evo_sum_rows(const float* x, int64_t rows, int64_t cols, float* out, int accumulate, void* stream);
+
 /* ---- triangle multiplication (extension; AF2 Supplementary Alg. 11/12) -----
  * Absent from the reference (planner inventory only, src/planner.py:37-45).
  * proj: [R*R, ld] token-major with column blocks [ap | ag | bp | bg] (width ch);

@@ -56,6 +56,11 @@ SIGNATURES = {
     "evo_attn_fwd": (_i, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p,
                           _i64, _i64, _i64, _i64, _i64, _i64, _i, _p]),
     "evo_attn_bwd_workspace": (_i64, [_i64, _i64, _i64, _i64, _i]),
+    "evo_softmax_masked_rows": (_i, [_p, _p, _i64, _i64, _p, _i64, _i64, _i64, _p]),
+    "evo_softmax_rows_bwd": (_i, [_p, _p, _i64, _i64, _p]),
+    "evo_gate_fwd": (_i, [_p, _p, _p, _p, _i64, _p]),
+    "evo_gate_bwd": (_i, [_p, _p, _p, _p, _p, _i64, _p]),
+    "evo_sum_rows": (_i, [_p, _i64, _i64, _p, _i, _p]),
     "evo_attn_bwd": (_i, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _i, _p, _sz,
                           _i64, _i64, _i64, _i64, _i64, _i64, _i, _p]),
     "evo_pair_bias_fwd": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i, _p]),

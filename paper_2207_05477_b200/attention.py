@@ -13,6 +13,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import ops
@@ -123,9 +124,99 @@ def gated_attention_fused(inp: AttentionInput, p: AttentionParams,
     return _GatedAttention.apply(inp.x, inp.mask, inp.nonbatched_bias, *p.all(), act_dtype)
 
 
-# the GPU path is always the fused operator; the reference's fine-grained
-# composition exists there only as its own baseline (src/attention.py:78-115)
-gated_attention_reference = gated_attention_fused
+class _ReferenceAttention(torch.autograd.Function):
+    """src/attention.py:78-115, the unfused baseline on the library's fp32
+    kernels: q/k/v/gate projections, per-head logits materialised as
+    [B*S, H, R, R] (q scaled before the product, :93), mask bias and pair bias
+    added, softmax, context, gate, output projection -- each a separate GEMM
+    or elementwise kernel; the backward is the same chain reversed."""
+
+    @staticmethod
+    def forward(ctx, x, mask, nb, wq, wk, wv, wg, bg, wo, bo):
+        b, s, r, C = x.shape
+        H, D = wq.shape[1], wq.shape[2]
+        HD, T, BS = H * D, b * s * r, b * s
+        dev, f32 = x.device, torch.float32
+        x2 = x.reshape(T, C).float().contiguous()
+        ws = [w.reshape(C, HD).float().contiguous() for w in (wq, wk, wv, wg)]
+        scale = float(1.0 / np.sqrt(D))
+        q, k, v = (torch.empty((T, HD), dtype=f32, device=dev) for _ in range(3))
+        ops.gemm(x2, ws[0], q, alpha=scale)
+        ops.gemm(x2, ws[1], k)
+        ops.gemm(x2, ws[2], v)
+        w = torch.empty((BS, H, r, r), dtype=f32, device=dev)          # logits, then weights
+        for h in range(H):
+            cs = slice(h * D, (h + 1) * D)
+            ops.gemm_batched(q[:r, cs], k[:r, cs], w[0, h], BS, r * HD, r * HD, H * r * r, tb=True)
+        maskf = mask.reshape(BS, r).float().contiguous()
+        nbf = nb.float().contiguous() if nb is not None else None
+        ops.softmax_masked_rows(w, maskf, r, 1, nbf, BS, H, r)
+        ctx_ = torch.empty((T, HD), dtype=f32, device=dev)
+        for h in range(H):
+            cs = slice(h * D, (h + 1) * D)
+            ops.gemm_batched(w[0, h], v[:r, cs], ctx_[:r, cs], BS, H * r * r, r * HD, r * HD)
+        gp = torch.empty((T, HD), dtype=f32, device=dev)
+        ops.gemm_bias(x2, ws[3], gp, bg.reshape(HD).float().contiguous())
+        gate = torch.empty_like(gp)
+        gated = torch.empty_like(gp)
+        ops.gate_fwd(gp, ctx_, gate, gated)
+        wo2 = wo.reshape(HD, C).float().contiguous()
+        out = torch.empty((T, C), dtype=f32, device=dev)
+        ops.gemm_bias(gated, wo2, out, bo.float().contiguous())
+        ctx.save_for_backward(x2, q, k, v, w, ctx_, gate, gated, wo2, *ws)
+        ctx.dims = (b, s, r, C, H, D)
+        ctx.has_bias = nb is not None
+        return out.view(b, s, r, C)
+
+    @staticmethod
+    def backward(ctx, gout):
+        x2, q, k, v, w, ctx_, gate, gated, wo2, wq2, wk2, wv2, wg2 = ctx.saved_tensors
+        b, s, r, C, H, D = ctx.dims
+        HD, T, BS = H * D, b * s * r, b * s
+        dev, f32 = x2.device, torch.float32
+        scale = float(1.0 / np.sqrt(D))
+        g2 = gout.reshape(T, C).float().contiguous()
+        dbo = ops.sum_rows(g2, torch.empty(C, dtype=f32, device=dev))
+        dwo = torch.empty((HD, C), dtype=f32, device=dev)
+        ops.gemm(gated, g2, dwo, ta=True)
+        dgated = torch.empty((T, HD), dtype=f32, device=dev)
+        ops.gemm(g2, wo2, dgated, tb=True)
+        dctx, dgp = torch.empty_like(dgated), torch.empty_like(dgated)
+        ops.gate_bwd(dgated, gate, ctx_, dctx, dgp)
+        dw = torch.empty_like(w)
+        dv = torch.empty((T, HD), dtype=f32, device=dev)
+        for h in range(H):
+            cs = slice(h * D, (h + 1) * D)
+            ops.gemm_batched(dctx[:r, cs], v[:r, cs], dw[0, h], BS, r * HD, r * HD, H * r * r, tb=True)
+            ops.gemm_batched(w[0, h], dctx[:r, cs], dv[:r, cs], BS, H * r * r, r * HD, r * HD, ta=True)
+        ops.softmax_rows_bwd(w, dw, BS * H * r, r)                        # dw -> d(logits)
+        dnb = None
+        if ctx.has_bias:
+            dnb = ops.sum_rows(dw.view(BS, H * r * r), torch.empty(H * r * r, dtype=f32, device=dev)).view(H, r, r)
+        dq, dk = torch.empty_like(dv), torch.empty_like(dv)           # dq: d(scaled q)
+        for h in range(H):
+            cs = slice(h * D, (h + 1) * D)
+            ops.gemm_batched(dw[0, h], k[:r, cs], dq[:r, cs], BS, H * r * r, r * HD, r * HD)
+            ops.gemm_batched(dw[0, h], q[:r, cs], dk[:r, cs], BS, H * r * r, r * HD, r * HD, ta=True)
+        dws = [torch.empty((C, HD), dtype=f32, device=dev) for _ in range(4)]
+        ops.gemm(x2, dq, dws[0], ta=True, alpha=scale)
+        ops.gemm(x2, dk, dws[1], ta=True)
+        ops.gemm(x2, dv, dws[2], ta=True)
+        ops.gemm(x2, dgp, dws[3], ta=True)
+        dbg = ops.sum_rows(dgp, torch.empty(HD, dtype=f32, device=dev))
+        dx = torch.empty((T, C), dtype=f32, device=dev)
+        ops.gemm(dq, wq2, dx, tb=True, alpha=scale)
+        for dgr, wr in ((dk, wk2), (dv, wv2), (dgp, wg2)):
+            ops.gemm(dgr, wr, dx, tb=True, beta=1.0)
+        return (dx.view(b, s, r, C), None, dnb, *[d.view(C, H, D) for d in dws], dbg.view(H, D),
+                dwo.view(H, D, C), dbo)
+
+
+def gated_attention_reference(inp: AttentionInput, p: AttentionParams) -> torch.Tensor:
+    """src/attention.py:78-115 -- the unfused fp32 baseline (materialised
+    logits), the reference's oracle for ``gated_attention_fused``."""
+    _check_shapes(inp, p)
+    return _ReferenceAttention.apply(inp.x, inp.mask, inp.nonbatched_bias, *p.all())
 
 
 def subbatch_apply(f, x: torch.Tensor, dim: int, chunk: int, companions=()):

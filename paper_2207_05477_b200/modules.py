@@ -472,11 +472,15 @@ def _attn_module(kind, x, pair, mask, mod: AttnModuleParams):
 
 
 def _run_attention(inp: AttentionInput, p: AttentionParams, policy: ExecPolicy, chunk: int = 0):
-    """src/model.py:300-309: the fused operator (``policy.fused``; the GPU
-    path has one implementation), chunked over dim 1 with the mask as
-    companion and the bias shared when ``chunk`` > 0."""
-    f = gated_attention_fused if policy.fused else gated_attention_reference
+    """src/model.py:300-309: the fused operator, or with ``policy.fused``
+    False the unfused fp32 baseline (materialised logits), chunked over dim 1
+    with the mask as companion and the bias shared when ``chunk`` > 0."""
     dt = inp.x.dtype if inp.x.dtype in (F32, BF16) else F32
+    if policy.fused:
+        f = gated_attention_fused
+    else:
+        def f(i, pp, act_dtype=None):  # the baseline computes in fp32 (src/attention.py:78-115)
+            return gated_attention_reference(i, pp)
     if chunk:
         nb = inp.nonbatched_bias
         return subbatch_apply(lambda xc, mc: f(AttentionInput(xc, mc, nb), p, act_dtype=dt),

@@ -256,6 +256,32 @@ def cast(x, y):
 # attention core
 
 
+# -- unfused attention baseline pieces (gated_attention_reference) ----------
+
+
+def softmax_masked_rows(x, mask, msb, msl, nb, BS, H, R):
+    """In place on fp32 logits [BS, H, R, R]: softmax_j(x + (mask - 1) * 1e9 + nb)."""
+    call("evo_softmax_masked_rows", ptr(x), ptr(mask), msb, msl, ptr(nb), BS, H, R, stream())
+
+
+def softmax_rows_bwd(w, g, rows, R):
+    call("evo_softmax_rows_bwd", ptr(w), ptr(g), rows, R, stream())
+
+
+def gate_fwd(gp, ctx, gate, gated):
+    call("evo_gate_fwd", ptr(gp), ptr(ctx), ptr(gate), ptr(gated), gp.numel(), stream())
+
+
+def gate_bwd(dgated, gate, ctx, dctx, dgp):
+    call("evo_gate_bwd", ptr(dgated), ptr(gate), ptr(ctx), ptr(dctx), ptr(dgp), dgated.numel(), stream())
+
+
+def sum_rows(x, out, accumulate=False):
+    rows, cols = x.shape
+    call("evo_sum_rows", ptr(x), rows, cols, ptr(out), int(accumulate), stream())
+    return out
+
+
 def attn_fwd(qkvg, mask, msb, msl, nb, bg, B, L, H, D, sb, sl):
     """nb: [H, L, L] (query, key) in qkvg's dtype, or None."""
     T = qkvg.shape[0]

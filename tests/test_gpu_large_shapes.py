@@ -1,4 +1,4 @@
-"""Parity beyond the bench shape (SURVEY.md section 8 configs[4], A5 and (f)1).
+"""Parity beyond the bench shape (SURVEY.md section 8 configs[4], A4, A5 and (f)1).
 
 * Fine-tune shape F (N_seq=512, N_res=384): one Evoformer block fwd+bwd in
   bf16 against the fp32 CPU oracle.  Rows longer than 256 keys take the
@@ -10,6 +10,8 @@
   4 heads of 32, padded residues) through ``subbatch_apply`` with chunk 32
   (src/attention.py:236-267) on a 64-row subset, bf16 against the oracle's
   ``gated_attention_fused`` forward (src/attention.py:121-174) on the same rows.
+* ``gated_attention_reference`` (A4): the unfused fp32 baseline with
+  materialised logits, forward and gradients against the oracle.
 """
 
 import numpy as np
@@ -92,3 +94,47 @@ def test_inference_shape_tri_attention_subbatch_matches_oracle():
     torch.cuda.synchronize()
     assert out.shape == (1, NI, R, C)
     assert rel_err(out.cpu().numpy(), ref) <= 3e-2
+
+
+def test_gated_attention_reference_unfused_fwd_bwd():
+    """``gated_attention_reference`` (src/attention.py:78-115): the unfused
+    fp32 composition with materialised [B*S, H, R, R] logits on the library's
+    GEMM / softmax / gate kernels.  Forward and every gradient against the
+    oracle (the reference's own parity bound for the pair: forward 1e-5,
+    gradients 1e-4, tests/test_acceptance.py:46-71), and against the fused
+    operator in fp32 and bf16."""
+    from oracle import evoformer_np as O
+    from paper_2207_05477_b200.attention import (AttentionInput, AttentionParams, gated_attention_fused,
+                                                 gated_attention_reference)
+    rng = np.random.default_rng(7)
+    S, R, C, H, D = 6, 80, 64, 4, 16
+    x = rng.standard_normal((1, S, R, C)).astype(np.float32)
+    mask = np.ones((1, S, R), np.float32)
+    mask[:, :, 70:] = 0.0
+    mask[:, 2, :] = 0.0                      # a fully-masked row
+    nb = (0.5 * rng.standard_normal((H, R, R))).astype(np.float32)
+    names = ("wq", "wk", "wv", "wg", "bg", "wo", "bo")
+    pa = _attn_params(rng, C, H, D)
+    ref, cache = O.attention_fwd(x, mask, nb, dict(zip(names, pa)))
+    gout = rng.standard_normal(ref.shape).astype(np.float32)
+    odx, odp, odnb = O.attention_bwd(gout, cache)
+    ograds = dict(odp, x=odx, nb=odnb)
+
+    dev = lambda a, g=True: torch.from_numpy(a).cuda().requires_grad_(g)
+    xt, nbt = dev(x), dev(nb)
+    pt = AttentionParams(*[dev(a) for a in pa])
+    out = gated_attention_reference(AttentionInput(xt, dev(mask, False), nbt), pt)
+    out.backward(torch.from_numpy(gout).cuda())
+    torch.cuda.synchronize()
+    assert rel_err(out.detach().cpu().numpy(), ref) <= 1e-5
+    got = dict(zip(("x", "nb") + names, [t.grad.cpu().numpy() for t in (xt, nbt, *pt.all())]))
+    for name in ("x", "nb") + names:
+        want = ograds[name]
+        assert rel_err(got[name].reshape(want.shape), want) <= 1e-4, name
+    with torch.no_grad():
+        inp = AttentionInput(xt.detach(), dev(mask, False), nbt.detach())
+        pd = AttentionParams(*[t.detach() for t in pt.all()])
+        fused32 = gated_attention_fused(inp, pd)
+        fused16 = gated_attention_fused(inp, pd, act_dtype=torch.bfloat16)
+    assert rel_err(fused32.cpu().numpy(), out.detach().cpu().numpy()) <= 1e-5
+    assert rel_err(fused16.float().cpu().numpy(), out.detach().cpu().numpy()) <= 3e-2

@@ -233,10 +233,10 @@ def test_run_attention_chunked_bitwise_equal():
     ref = Mo._run_attention(AttentionInput(x, mask, nb), p, Mo.ExecPolicy())
     out = Mo._run_attention(AttentionInput(x, mask, nb), p, Mo.ExecPolicy(), chunk=4)
     assert torch.equal(out, ref)
-    # policy.fused=False selects gated_attention_reference: the GPU path has
-    # one implementation of the operator, so it is the same result
+    # policy.fused=False selects gated_attention_reference, the unfused fp32
+    # baseline (materialised logits): the same function within fp32 rounding
     out = Mo._run_attention(AttentionInput(x, mask, nb), p, Mo.ExecPolicy(fused=False))
-    assert torch.equal(out, ref)
+    assert rel_err(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
