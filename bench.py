@@ -463,13 +463,13 @@ def run_ours(args):
             peak = peaks["hbm_gbs"]
             bound = "hbm"
         traffic, traffic_src = None, None
-        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
                 tr = json.load(f).get(name)
             if tr:
                 traffic = tr["traffic_bytes"]
-                traffic_src = f"profiles/r01_traffic.json ({tr['kernel']}, ncu --set full, per launch)"
+                traffic_src = f"profiles/r02_traffic.json ({tr['kernel']}, ncu --set full, per launch)"
         # the attention cores at head dims 16/32 are bound by the softmax exps
         # (MUFU ex2, 16/clk/SM) and small-N tcgen05 issue, not by tensor FLOPs:
         # report the ex2 roofline beside the tensor one

@@ -656,6 +656,10 @@ struct BwdPlan {
 BwdPlan bwd_plan(const AttnGeom& g) {
   BwdPlan p{};
   p.LP = g.L <= 128 ? 128 : 256;
+  if (const char* e = getenv("EVO_ATTN_BWD_LP")) {  // key-window width sweeps (128 or 256)
+    const int f = atoi(e);
+    if (f == 128 || f == 256) p.LP = f;
+  }
   p.NQT = (int)((g.L + 127) / 128);
   p.NKW = (int)((g.L + p.LP - 1) / p.LP);
   int per = (int)(g.H * p.NQT * p.NKW);
