@@ -39,6 +39,17 @@
 #include "tc_common.cuh"
 
 namespace evo {
+
+#ifdef EVO_GEMM_TRACE
+// per-tile phase stamps of CTA 0 (tools/gemm_trace.py): [it][0] MMA waits the
+// accumulator, [1] MMA has it, [2] MMAs issued, [3] epilogue warp 2 sees tfull,
+// [4] epilogue done; [it][5] producer starts the tile, [6] producer done
+__device__ long long g_gemm_trace[4096];
+#define GT_STAMP(it, k) do { if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (it) < 512) g_gemm_trace[(it) * 8 + (k)] = clock64(); } while (0)
+#else
+#define GT_STAMP(it, k) do {} while (0)
+#endif
+
 namespace {
 
 using bf16 = __nv_bfloat16;
@@ -232,6 +243,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // CG2: CTA pair on adjacent M-tiles; rank 0 (the leader) issues the MMAs
   // and owns the smem-full and accumulator-empty barriers the pair shares
+  GT_STAMP(511, 7);
   const int crank = CG2 ? (int)cluster_rank() : 0;
   const int cid = CG2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int ncl = CG2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
@@ -280,9 +292,11 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < p.tiles; t += ncl) {
+      int pit = 0;
+      for (int t = cid; t < p.tiles; t += ncl, ++pit) {
         const TileCoord c = decode(p, t, CG2, crank);
         const int n0 = c.n0 * BN;
+        GT_STAMP(pit, 5);
         for (int kb = c.kb0; kb < c.kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + F::OFF_RING + stage * F::STAGE;
@@ -336,7 +350,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       for (int t = cid; t < p.tiles; t += ncl, ++it) {
         const TileCoord c = decode(p, t, CG2, crank);
         const int acc = it & 1;
+        GT_STAMP(it, 0);
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);  // epilogue(s) drained this accumulator
+        GT_STAMP(it, 1);
         tc::fence_after();
         const uint32_t dacc = tmem + (uint32_t)(acc * BN);
         for (int kb = c.kb0; kb < c.kb1; ++kb) {
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             phase ^= 1;
           }
         }
+        GT_STAMP(it, 2);
         if constexpr (CG2) mma2_commit_w(&tfull[acc]);  // accumulator complete, in both CTAs' TMEM
         else tc::mma_commit_w(&tfull[acc]);
       }
@@ -398,6 +415,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         __syncwarp();
       }
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      if (warp == 2) GT_STAMP(it, 3);
       tc::fence_after();
       const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
@@ -492,6 +510,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
       if (lane == 0) {  // accumulator may be overwritten (CG2: on the leader's barrier)
         if constexpr (CG2) mbar_arrive_cluster(mapa_rank0(&tempty[acc]));
         else tc::mbar_arrive(&tempty[acc]);
+        if (warp == 2) GT_STAMP(it, 4);
       }
     }
     if (lane == 0) bulk_wait_all();
@@ -841,7 +860,11 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   // receiving half the B bytes per k-block) for the 256-wide, K >= 512,
   // unsplit problems: measured 5-9% faster there (tools/gemm_shapes.py),
   // neutral-to-slower for 128-wide tiles, short K and split-K partials
-  const bool cg2 = !bres && BN == 256 && !p.partial && p.kblocks >= 8 && p.n_mt >= 2 && !cg2_disabled();
+  static const int cg2_minkb = [] {  // sweeps: EVO_GEMM_CG2_MINKB
+    const char* e = getenv("EVO_GEMM_CG2_MINKB");
+    return e ? atoi(e) : 8;
+  }();
+  const bool cg2 = !bres && BN == 256 && !p.partial && p.kblocks >= cg2_minkb && p.n_mt >= 2 && !cg2_disabled();
   if (cg2) p.tiles = (int)((int64_t)batch * ((p.n_mt + 1) / 2) * p.n_nt * splits);
 
   CUtensorMap ma, mb, md, mc;
@@ -895,3 +918,9 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
 }  // namespace evo
 
 extern "C" int64_t evo_gemm_tc_launches(void) { return evo::g_tc_gemms; }
+
+#ifdef EVO_GEMM_TRACE
+extern "C" int evo_gemm_trace_read(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, evo::g_gemm_trace, sizeof(long long) * n);
+}
+#endif
