@@ -27,22 +27,35 @@ static __global__ void __launch_bounds__(256) finalize_batch_kernel(const __grid
 }
 
 // ---------------------------------------------------------------------------
-// Streams map to one of EVO_STREAM_SLOTS slots; per-stream scratch (the
-// tensor-core GEMM's split-K workspace) is indexed by slot, so kernels on
-// concurrently running streams (the two branch streams of the engine) never
-// share a workspace.  Slots are assigned on first sight; the workspaces are
-// allocated on the first GEMM, before CUDA-graph capture (the eager warm-up
-// step touches every stream).
+// Per-stream scratch (split-K partials, column-sum partials) lives in one of
+// EVO_STREAM_SLOTS slots.  A stream keeps its slot while it is in use; when a
+// new stream arrives and every slot is taken, the least recently used slot is
+// handed over -- its previous stream has gone quiet (old trainers / finished
+// tests), whereas hashing could give two live, concurrently running streams
+// (a capture stream and a branch stream) the same scratch.  The workspaces of
+// all slots are allocated on the first GEMM, before any CUDA-graph capture.
 int stream_slot(cudaStream_t s) {
   static thread_local cudaStream_t seen[EVO_STREAM_SLOTS] = {};
+  static thread_local uint64_t used[EVO_STREAM_SLOTS] = {};
+  static thread_local uint64_t tick = 0;
   static thread_local int n = 0;
+  ++tick;
   for (int i = 0; i < n; ++i)
-    if (seen[i] == s) return i;
+    if (seen[i] == s) {
+      used[i] = tick;
+      return i;
+    }
+  int slot = n;
   if (n < EVO_STREAM_SLOTS) {
-    seen[n] = s;
-    return n++;
+    ++n;
+  } else {
+    slot = 0;
+    for (int i = 1; i < EVO_STREAM_SLOTS; ++i)
+      if (used[i] < used[slot]) slot = i;
   }
-  return (int)(((uintptr_t)s >> 4) % EVO_STREAM_SLOTS);
+  seen[slot] = s;
+  used[slot] = tick;
+  return slot;
 }
 
 // vectorised glue (glue.cu); return false -> scalar kernels below

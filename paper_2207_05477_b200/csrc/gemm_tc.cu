@@ -100,6 +100,11 @@ struct Params {
   int has_res, relu, partial;
   float alpha, beta;
   const float* bias;
+  // OPM layouts (k = 32): 1 = outn (rows (i, p), cols (j, q), scale rec[i*R + j]),
+  // 2 = dnum (rows (i, j), cols (p, q), scale rec[row]); D is then a 4-D view
+  // written through [2][32][32] staging tiles (see gemm_tc_opm)
+  int pmode, R;
+  const float* rec;
 };
 
 // --- TMA / bulk-async helpers -------------------------------------------------
@@ -171,6 +176,13 @@ __device__ __forceinline__ void tmem_alloc2(uint32_t* slot_smem) {
 template <int NCOLS>
 __device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS));
+}
+
+__device__ __forceinline__ void tma_store4(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tc::smem_u32(src))
+               : "memory");
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -483,6 +495,45 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 v[8 * u + 2 * q + 1] = fmaf(p.beta, f.y, v[8 * u + 2 * q + 1]);
               }
             }
+          }
+        }
+        if constexpr (!OUT_F32 && CW == 64) {
+          if (p.pmode != 0) {
+            // OPM layouts: scale, then this lane's two 32-value runs go to
+            // [g][lane][32] (g = the chunk's two 32-column groups), the order
+            // of the 4-D TMA box
+            if (p.pmode == 1) {
+              const int i = (c.m0 >> 5) + quarter, jc = (n0 + cc) >> 5;
+              const float r0 = __ldg(p.rec + (int64_t)i * p.R + jc), r1 = __ldg(p.rec + (int64_t)i * p.R + jc + 1);
+#pragma unroll
+              for (int e = 0; e < 32; ++e) v[e] *= r0, v[32 + e] *= r1;
+            } else {
+              const float r = __ldg(p.rec + row0 + lane);
+#pragma unroll
+              for (int e = 0; e < 64; ++e) v[e] *= r;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              // 16-B piece (u & 3) of row g*32 + lane, 64-B swizzled (the map's
+              // SWIZZLE_64B: piece ^= (row >> 1) & 3) -- at most 4-way conflicts
+              const int g = u >> 2, row = g * 32 + lane;
+              const int e0 = g * 32 + (u & 3) * 8;
+              *reinterpret_cast<uint4*>(sbuf + row * 64 + (((u & 3) ^ ((row >> 1) & 3)) << 4)) =
+                  make_uint4(tc::pack_bf16(v[e0], v[e0 + 1]), tc::pack_bf16(v[e0 + 2], v[e0 + 3]),
+                             tc::pack_bf16(v[e0 + 4], v[e0 + 5]), tc::pack_bf16(v[e0 + 6], v[e0 + 7]));
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              if (p.pmode == 1) {
+                tma_store4(&tmD, sbuf, 0, 0, (n0 + cc) >> 5, (c.m0 >> 5) + quarter);
+              } else {
+                tma_store4(&tmD, sbuf, 0, row0 % p.R, (n0 + cc) >> 5, row0 / p.R);
+              }
+              bulk_commit();
+            }
+            if constexpr (F::STG_BUFS == 2) buf ^= 1;
+            continue;
           }
         }
 #pragma unroll
@@ -798,9 +849,67 @@ void splitk_reduce(const float* ws, int splits, int64_t M, int64_t N, void* D, i
 // Row-major D[b] = act(alpha * op(A[b]) op(B[b]) + bias) + beta * C[b] on the
 // tensor cores; A, B bf16; D and C (may alias D) of dtype d_dtype.  Returns
 // false (caller uses the SIMT kernel) when TMA cannot address an operand.
+namespace {
+// OPM output layouts of gemm_tc_impl (k = 32 only)
+struct OpmOut {
+  int mode;          // 1 = outn, 2 = dnum
+  const float* rec;  // outn: [NI*R] by (i, j); dnum: [NI*R] by the GEMM row
+  int64_t R, NI;
+};
+
+// 4-D views of the OPM outputs for TMA stores of [2][32][32] bf16 boxes,
+// 64-byte swizzled (inner extent 64 B):
+//   outn [NI*R, k*k]:  (q, p, j, i), strides (1, k, k*k, R*k*k)
+//   dnum [NI*k, R*k]:  (q, j, p, i), strides (1, k, R*k, k*R*k)
+bool opm_map(CUtensorMap* m, void* base, const OpmOut& o) {
+  auto enc = tmap_encoder();
+  if (!enc || ((uintptr_t)base & 15)) return false;
+  const cuuint64_t k = 32, R = (cuuint64_t)o.R, NI = (cuuint64_t)o.NI;
+  cuuint64_t dims[4], strides[3];
+  if (o.mode == 1) {
+    dims[0] = k, dims[1] = k, dims[2] = R, dims[3] = NI;
+    strides[0] = k * 2, strides[1] = k * k * 2, strides[2] = R * k * k * 2;
+  } else {
+    dims[0] = k, dims[1] = R, dims[2] = k, dims[3] = NI;
+    strides[0] = k * 2, strides[1] = R * k * 2, strides[2] = k * R * k * 2;
+  }
+  cuuint32_t box[4] = {32, 32, 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+}  // namespace
+
+static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
+                         const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
+                         float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
+                         int d_dtype, cudaStream_t s, const OpmOut* opm);
+
 bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha,
              float beta, const void* Cin, int64_t ldc, const float* bias, int relu, int d_dtype, cudaStream_t s) {
+  return gemm_tc_impl(M, N, K, A, lda, ta, sa, B, ldb, tb, sb, D, ldd, sd, batch, alpha, beta, Cin, ldc, bias, relu,
+                      d_dtype, s, nullptr);
+}
+
+// The OPM contractions with the normalisation and re-layout in the epilogue
+// (src/model.py:366-378):
+//   outn[i*R + j, p*k + q] = rec[i*R + j] * sum_s a[s, i*k + p] c[s, j*k + q]      (mode 1)
+//   dnum[i*k + p, j*k + q] = rec[i*R + j] * sum_c d[(i, j), c] w_out[p*k + q, c]   (mode 2)
+bool gemm_tc_opm(int mode, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, const void* B,
+                 int64_t ldb, int tb, void* D, const float* rec, int64_t R, int64_t NI, cudaStream_t s) {
+  if (mode == 1 && (M != NI * 32 || N != R * 32)) return false;
+  if (mode == 2 && (M != NI * R || N != 32 * 32 || R % BM)) return false;
+  const OpmOut o{mode, rec, R, NI};
+  return gemm_tc_impl(M, N, K, A, lda, ta, 0, B, ldb, tb, 0, D, N, 0, 1, 1.f, 0.f, nullptr, 0, nullptr, 0, EVO_BF16, s,
+                      &o);
+}
+
+static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
+                         const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
+                         float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
+                         int d_dtype, cudaStream_t s, const OpmOut* opm) {
   if (tc_gemm_disabled()) return false;
   if (M <= 0 || N <= 0 || K <= 0 || batch < 1) return false;
   if (M > (1ll << 31) - BM || N > (1ll << 31) - 256 || K > (1ll << 31) - BK) return false;
@@ -833,7 +942,7 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
   if (base > (1ll << 30)) return false;
   // split K when the output tiles cannot fill the SMs and K is long
   int splits = 1;
-  if (batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
+  if (!opm && batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
     // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes; the
     // split tiles must fit one wave of the persistent grid (a second, mostly
     // idle wave doubles the kernel time)
@@ -880,7 +989,12 @@ bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta
     return false;
   }
   float* wsp = nullptr;
-  if (p.partial) {
+  if (opm) {
+    p.pmode = opm->mode;
+    p.rec = opm->rec;
+    p.R = (int)opm->R;
+    if (!opm_map(&md, D, *opm)) return false;
+  } else if (p.partial) {
     wsp = split_ws(s).ptr;
     if (!make_map(&md, wsp, true, N, M, N, M * N, splits, 32, 32)) return false;
   } else if (!make_map(&md, D, f32, N, M, ldd, sd, batch, f32 ? 32 : 64, 32)) {

@@ -391,11 +391,11 @@ def opm_norm_fwd(num, mask, S, R, k, out_dtype, i0=0, ni=None, rec=None):
 
 def opm_dnum(d_act, w_out, rec, R, k, ni=None):
     """d(num) straight from d(pair): the w_out data-gradient GEMM with the OPM
-    normalisation and re-layout in its tcgen05 epilogue.  None when the shape
+    normalisation and re-layout in its tcgen05 epilogue (gemm_tc.cu OPM mode).  None when the shape
     is not covered (the caller runs GEMM + opm_norm_bwd)."""
     ni = R if ni is None else ni
     C = d_act.shape[1]
-    if (d_act.dtype != torch.bfloat16 or w_out.dtype != torch.bfloat16 or C != 128 or k != 32
+    if (d_act.dtype != torch.bfloat16 or w_out.dtype != torch.bfloat16 or C % 8 or k != 32
             or R % 128 or not d_act.is_contiguous() or not w_out.is_contiguous()):
         return None
     dnum = torch.empty((ni * k, R * k), dtype=torch.bfloat16, device=d_act.device)
@@ -409,8 +409,8 @@ def opm_outn(a, c, rec, S, R, k, ni=None):
     GEMM with the normalisation and re-layout in its epilogue.  None when the
     shape is not covered (the caller runs GEMM + opm_norm_fwd)."""
     ni = R if ni is None else ni
-    if (a.dtype != torch.bfloat16 or c.dtype != torch.bfloat16 or S != 128 or k != 32 or (R * k) % 256
-            or (ni * k) % 128 or not a.is_contiguous() or not c.is_contiguous()):
+    if (a.dtype != torch.bfloat16 or c.dtype != torch.bfloat16 or S % 8 or k != 32 or ni != R
+            or not a.is_contiguous() or not c.is_contiguous()):
         return None
     outn = torch.empty((ni * R, k * k), dtype=torch.bfloat16, device=a.device)
     call("evo_opm_outn", ptr(a), ptr(c), ptr(rec), ptr(outn), S, R, k, ni, dcode(a), stream())

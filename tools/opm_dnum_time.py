@@ -24,3 +24,15 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def outn():
+    S, R, k = 128, 256, 32
+    a = torch.randn(S, R * k, device="cuda").bfloat16()
+    c = torch.randn(S, R * k, device="cuda").bfloat16()
+    rec = torch.rand(R * R, device="cuda")
+    print("fused opm_outn        ", timeit(lambda: ops.opm_outn(a, c, rec, S, R, k)))
+
+
+if __name__ == "__main__":
+    outn()
