@@ -95,6 +95,13 @@ int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
                   const float* bias, const void* bias_bf16, int relu, void* out, int64_t ldo,
                   int ab_dtype, int c_dtype, void* stream);
 
+/* D[M, N] = (h > 0) ? op(A) op(B) : 0 -- the transition's ReLU backward in the
+ * epilogue of the d(hidden) projection (src/model.py:344-348 differentiated);
+ * h is the saved ReLU output, [M, N] contiguous like D.  bf16 on the tensor
+ * cores; EVO_ERR_UNSUPPORTED otherwise (the caller masks separately). */
+int evo_gemm_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
+                       int64_t ldb, int trans_b, const void* h, void* D, int dtype, void* stream);
+
 /* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
  * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */
 int evo_layernorm_fwd(const void* x, int x_dtype, const float* gamma, const float* beta,

@@ -105,6 +105,7 @@ struct Params {
   // written through [2][32][32] staging tiles (see gemm_tc_opm)
   int pmode, R;
   const float* rec;
+  int cmask;  // the C tile masks instead of adding: D = (C > 0) ? acc : 0 (ReLU backward)
 };
 
 // --- TMA / bulk-async helpers -------------------------------------------------
@@ -482,17 +483,23 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
           for (int u = 0; u < 8; ++u) {
             const uint4 r = *reinterpret_cast<const uint4*>(rowp + ((u ^ sw) << 4));
             if constexpr (OUT_F32) {
-              v[4 * u + 0] = fmaf(p.beta, __uint_as_float(r.x), v[4 * u + 0]);
-              v[4 * u + 1] = fmaf(p.beta, __uint_as_float(r.y), v[4 * u + 1]);
-              v[4 * u + 2] = fmaf(p.beta, __uint_as_float(r.z), v[4 * u + 2]);
-              v[4 * u + 3] = fmaf(p.beta, __uint_as_float(r.w), v[4 * u + 3]);
+              const float rr[4] = {__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z),
+                                   __uint_as_float(r.w)};
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                v[4 * u + q] = p.cmask ? (rr[q] > 0.f ? v[4 * u + q] : 0.f) : fmaf(p.beta, rr[q], v[4 * u + q]);
             } else {
               const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float2 f = tc::bf16x2_f2(w[q]);
-                v[8 * u + 2 * q] = fmaf(p.beta, f.x, v[8 * u + 2 * q]);
-                v[8 * u + 2 * q + 1] = fmaf(p.beta, f.y, v[8 * u + 2 * q + 1]);
+                if (p.cmask) {
+                  v[8 * u + 2 * q] = f.x > 0.f ? v[8 * u + 2 * q] : 0.f;
+                  v[8 * u + 2 * q + 1] = f.y > 0.f ? v[8 * u + 2 * q + 1] : 0.f;
+                } else {
+                  v[8 * u + 2 * q] = fmaf(p.beta, f.x, v[8 * u + 2 * q]);
+                  v[8 * u + 2 * q + 1] = fmaf(p.beta, f.y, v[8 * u + 2 * q + 1]);
+                }
               }
             }
           }
@@ -884,7 +891,7 @@ bool opm_map(CUtensorMap* m, void* base, const OpmOut& o) {
 static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                          const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
                          float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
-                         int d_dtype, cudaStream_t s, const OpmOut* opm);
+                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask = 0);
 
 bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha,
@@ -906,15 +913,23 @@ bool gemm_tc_opm(int mode, int64_t M, int64_t N, int64_t K, const void* A, int64
                       &o);
 }
 
+// D = (h > 0) ? op(A) op(B) : 0 -- the ReLU backward in the epilogue of the
+// d(hidden) GEMM (h: the saved ReLU output, [M, N] like D)
+bool gemm_tc_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, const void* B,
+                       int64_t ldb, int tb, const void* h, void* D, int d_dtype, cudaStream_t s) {
+  return gemm_tc_impl(M, N, K, A, lda, ta, 0, B, ldb, tb, 0, D, N, 0, 1, 1.f, 0.f, h, N, nullptr, 0, d_dtype, s,
+                      nullptr, 1);
+}
+
 static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                          const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
                          float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
-                         int d_dtype, cudaStream_t s, const OpmOut* opm) {
+                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask) {
   if (tc_gemm_disabled()) return false;
   if (M <= 0 || N <= 0 || K <= 0 || batch < 1) return false;
   if (M > (1ll << 31) - BM || N > (1ll << 31) - 256 || K > (1ll << 31) - BK) return false;
   const bool f32 = d_dtype == EVO_F32;
-  const bool has_res = Cin != nullptr && beta != 0.f;
+  const bool has_res = Cin != nullptr && (beta != 0.f || cmask);
   int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   // split-K problems (few output tiles, long K): 128-wide tiles give twice
   // the tiles per split and halve each CTA's B stream (measured faster on
@@ -937,12 +952,13 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
   p.bias = bias;
   p.relu = relu;
   p.has_res = has_res ? 1 : 0;
+  p.cmask = cmask;
   const int nsm = num_sms();
   const int64_t base = (int64_t)batch * p.n_mt * p.n_nt;
   if (base > (1ll << 30)) return false;
   // split K when the output tiles cannot fill the SMs and K is long
   int splits = 1;
-  if (!opm && batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
+  if (!opm && !cmask && batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
     // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes; the
     // split tiles must fit one wave of the persistent grid (a second, mostly
     // idle wave doubles the kernel time)

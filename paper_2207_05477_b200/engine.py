@@ -319,9 +319,13 @@ class BlockEngine:
         ops.colsum_cast(d, self.G(f"{prefix}.b2"), y=d_act)
         ops.gemm(h, d_act, self.Gm(f"{prefix}.w2", F), ta=True)
         dh = torch.empty((T, F), dtype=dt, device=d.device)
-        ops.gemm(d_act, self.W(f"{prefix}.w2", F), dh, tb=True)
+        if dt == torch.bfloat16:  # ReLU mask in the GEMM epilogue, then a read-only column sum
+            ops.gemm_relu_mask(d_act, self.W(f"{prefix}.w2", F), h, dh, tb=True)
+            ops.colsum_cast(dh, self.G(f"{prefix}.b1"))
+        else:
+            ops.gemm(d_act, self.W(f"{prefix}.w2", F), dh, tb=True)
+            ops.relu_bwd_colsum_(dh, h, self.G(f"{prefix}.b1"))
         del d_act
-        ops.relu_bwd_colsum_(dh, h, self.G(f"{prefix}.b1"))
         ops.gemm(sv["xl"], dh, self.Gm(f"{prefix}.w1", C), ta=True)
         dxl = torch.empty((T, C), dtype=F32, device=d.device)
         ops.gemm(dh, self.W(f"{prefix}.w1", C), dxl, tb=True)

@@ -98,6 +98,20 @@ def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.T
     return out
 
 
+def gemm_relu_mask(a, b, h, out, ta=False, tb=False):
+    """out = (h > 0) * (op(a) @ op(b)): the ReLU backward fused into the
+    d(hidden) GEMM's epilogue (bf16 only)."""
+    M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
+    Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
+    if K != Kb or tuple(out.shape) != (M, N) or tuple(h.shape) != (M, N):
+        raise ValueError("gemm_relu_mask shape mismatch")
+    if not (h.is_contiguous() and out.is_contiguous()):
+        raise ValueError("gemm_relu_mask: h and out must be contiguous")
+    call("evo_gemm_relu_mask", M, N, K, ptr(a), a.stride(0), int(ta), ptr(b), b.stride(0), int(tb), ptr(h),
+         ptr(out), dcode(out), stream())
+    return out
+
+
 def gemm_batched(a, b, c, batch, sa, sb, sc, ta=False, tb=False, alpha=1.0, beta=0.0):
     """Strided-batched row-major GEMM on flat buffers: operand k of batch i is
     the matrix at data_ptr + i*s (elements); a, b, c are 2-D views of batch 0."""

@@ -171,3 +171,21 @@ def test_gemm_fp32_split_k(M, N, K):
     c3 = torch.empty_like(c)
     ops.gemm(a, b, c3, ta=True)
     assert torch.equal(c, c3)
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 1024, 256), (8192, 512, 128), (1000, 384, 64)])
+def test_gemm_relu_mask_epilogue(M, N, K):
+    """D = (h > 0) * (A B^T): the transition's ReLU backward in the GEMM
+    epilogue (the mask tile fetched by TMA like a residual) == fp32 torch,
+    masked entries exactly zero."""
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(M + N)
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    h = torch.relu(torch.randn(M, N, device="cuda")).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm_relu_mask(a, b, h, out, tb=True)
+    ref = (a.float() @ b.float().t()) * (h.float() > 0)
+    assert torch.all(out[h == 0] == 0)
+    err = (out.float() - ref).abs().max() / ref.abs().max()
+    assert err <= 1e-2, float(err)
