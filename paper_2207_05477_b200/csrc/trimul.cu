@@ -10,6 +10,7 @@
 //   gated residual  out = z + sigmoid(gp + bg) * (y + by) and its backward
 #include "common.cuh"
 #include "reduce.cuh"
+#include "vec.cuh"
 
 namespace evo {
 
@@ -129,6 +130,149 @@ __global__ void gated_residual_bwd_kernel(const float* __restrict__ dout, const 
   }
 }
 
+// ---- 16-byte vector forms (ch % 32 == 0, RR % 8 == 0, 16-B aligned rows) ----
+// A block covers 64 tokens x 32 channels: the token-major side is read /
+// written as 8-channel vectors (thread = token, channel group), the
+// channel-major side as 8-token vectors, through a transposing smem tile.
+
+template <typename T>
+__global__ void __launch_bounds__(256) trimul_gate_fwd_vec_kernel(
+    const T* __restrict__ proj, int64_t ld, const float* __restrict__ bap, const float* __restrict__ bag,
+    const float* __restrict__ bbp, const float* __restrict__ bbg, const float* __restrict__ mask,
+    T* __restrict__ a_cm, T* __restrict__ b_cm, int64_t RR, int ch) {
+  __shared__ float sa[32][65], sb[32][65];
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int c0 = blockIdx.y * 32;
+  {
+    const int tt = threadIdx.x >> 2, cg = threadIdx.x & 3;
+    const int64_t t = t0 + tt;
+    const int c = c0 + cg * 8;
+    float ap[8], ag[8], bp[8], bgv[8];
+    if (t < RR) {
+      const T* row = proj + t * ld;
+      ld8(row + c, ap);
+      ld8(row + ch + c, ag);
+      ld8(row + 2 * ch + c, bp);
+      ld8(row + 3 * ch + c, bgv);
+      const float m = mask[t];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        sa[cg * 8 + u][tt] = sigm(ag[u] + bag[c + u]) * (ap[u] + bap[c + u]) * m;
+        sb[cg * 8 + u][tt] = sigm(bgv[u] + bbg[c + u]) * (bp[u] + bbp[c + u]) * m;
+      }
+    }
+  }
+  __syncthreads();
+  const int r = threadIdx.x >> 3, seg = threadIdx.x & 7;
+  const int64_t tb = t0 + seg * 8;
+  if (tb < RR) {  // RR % 8 == 0
+    float va[8], vb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) va[u] = sa[r][seg * 8 + u], vb[u] = sb[r][seg * 8 + u];
+    st8(a_cm + (int64_t)(c0 + r) * RR + tb, va);
+    st8(b_cm + (int64_t)(c0 + r) * RR + tb, vb);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) trimul_gate_bwd_vec_kernel(
+    const T* __restrict__ proj, int64_t ld, const float* __restrict__ bap, const float* __restrict__ bag,
+    const float* __restrict__ bbp, const float* __restrict__ bbg, const float* __restrict__ mask,
+    const T* __restrict__ da_cm, const T* __restrict__ db_cm, T* __restrict__ dproj, int64_t RR, int ch) {
+  __shared__ float sa[32][65], sb[32][65];
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int c0 = blockIdx.y * 32;
+  {
+    const int r = threadIdx.x >> 3, seg = threadIdx.x & 7;
+    const int64_t tb = t0 + seg * 8;
+    float va[8], vb[8];
+    if (tb < RR) {
+      ld8(da_cm + (int64_t)(c0 + r) * RR + tb, va);
+      ld8(db_cm + (int64_t)(c0 + r) * RR + tb, vb);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) va[u] = vb[u] = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sa[r][seg * 8 + u] = va[u], sb[r][seg * 8 + u] = vb[u];
+  }
+  __syncthreads();
+  const int tt = threadIdx.x >> 2, cg = threadIdx.x & 3;
+  const int64_t t = t0 + tt;
+  if (t >= RR) return;
+  const int c = c0 + cg * 8;
+  const T* row = proj + t * ld;
+  T* drow = dproj + t * 4 * ch;
+  float ap[8], ag[8], bp[8], bgv[8], o0[8], o1[8], o2[8], o3[8];
+  ld8(row + c, ap);
+  ld8(row + ch + c, ag);
+  ld8(row + 2 * ch + c, bp);
+  ld8(row + 3 * ch + c, bgv);
+  const float m = mask[t];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const float da = sa[cg * 8 + u][tt] * m, db = sb[cg * 8 + u][tt] * m;
+    const float a_p = ap[u] + bap[c + u], sa_ = sigm(ag[u] + bag[c + u]);
+    const float b_p = bp[u] + bbp[c + u], sb_ = sigm(bgv[u] + bbg[c + u]);
+    o0[u] = da * sa_;
+    o1[u] = da * a_p * sa_ * (1.0f - sa_);
+    o2[u] = db * sb_;
+    o3[u] = db * b_p * sb_ * (1.0f - sb_);
+  }
+  st8(drow + c, o0);
+  st8(drow + ch + c, o1);
+  st8(drow + 2 * ch + c, o2);
+  st8(drow + 3 * ch + c, o3);
+}
+
+// gated residual, 8 elements of one row per thread
+template <typename T>
+__global__ void gated_residual_vec_kernel(const T* __restrict__ res, const T* __restrict__ gp, int64_t ld_gp,
+                                          const float* __restrict__ bg, const T* __restrict__ y,
+                                          const float* __restrict__ by, T* __restrict__ g_out, T* __restrict__ out,
+                                          int64_t rows, int64_t C) {
+  const int64_t n8 = rows * C / 8;
+  for (int64_t e8 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e8 < n8;
+       e8 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e8 * 8, r = e / C, c = e % C;
+    float rv[8], gv[8], yv[8], go[8], ov[8];
+    ld8(res + e, rv);
+    ld8(gp + r * ld_gp + c, gv);
+    ld8(y + e, yv);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      go[u] = sigm(gv[u] + bg[c + u]);
+      ov[u] = rv[u] + go[u] * (yv[u] + by[c + u]);
+    }
+    st8(g_out + e, go);
+    st8(out + e, ov);
+  }
+}
+
+template <typename T>
+__global__ void gated_residual_bwd_vec_kernel(const float* __restrict__ dout, const T* __restrict__ g,
+                                              const T* __restrict__ y, const float* __restrict__ by,
+                                              T* __restrict__ dyb, T* __restrict__ dgp, int64_t rows, int64_t C) {
+  const int64_t n8 = rows * C / 8;
+  for (int64_t e8 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e8 < n8;
+       e8 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e8 * 8, c = e % C;
+    float dv[8], gv[8], yv[8], a[8], b[8];
+    ld8(dout + e, dv);
+    ld8(g + e, gv);
+    ld8(y + e, yv);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[u] = dv[u] * gv[u];
+      b[u] = dv[u] * (yv[u] + by[c + u]) * gv[u] * (1.0f - gv[u]);
+    }
+    st8(dyb + e, a);
+    st8(dgp + e, b);
+  }
+}
+
+bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
 }  // namespace
 }  // namespace evo
 
@@ -140,6 +284,17 @@ int evo_trimul_gate_fwd(const void* proj, int64_t ld, const float* b_ap, const f
                         const float* b_bp, const float* b_bg, const float* mask, void* a_cm,
                         void* b_cm, int64_t RR, int64_t ch, int dtype, void* stream) {
   EVO_API_BEGIN
+  const int64_t es = dtype == EVO_F32 ? 4 : 2;
+  if (ch % 32 == 0 && RR % 8 == 0 && (ld * es) % 16 == 0 && al16(proj) && al16(a_cm) && al16(b_cm)) {
+    dim3 g2(cdiv(RR, 64), (unsigned)(ch / 32));
+    EVO_DISPATCH_T(dtype, T, {
+      trimul_gate_fwd_vec_kernel<T><<<g2, 256, 0, (cudaStream_t)stream>>>(
+          (const T*)proj, ld, b_ap, b_ag, b_bp, b_bg, mask, (T*)a_cm, (T*)b_cm, RR, (int)ch);
+    });
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+    return EVO_OK;
+  }
   dim3 grid(cdiv(RR, TT), cdiv(ch, TT));
   EVO_DISPATCH_T(dtype, T, {
     trimul_gate_fwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
@@ -155,6 +310,19 @@ int evo_trimul_gate_bwd(const void* proj, int64_t ld, const float* b_ap, const f
                         const void* db_cm, void* dproj, int64_t RR, int64_t ch, int dtype,
                         void* stream) {
   EVO_API_BEGIN
+  const int64_t es = dtype == EVO_F32 ? 4 : 2;
+  if (ch % 32 == 0 && RR % 8 == 0 && (ld * es) % 16 == 0 && al16(proj) && al16(da_cm) && al16(db_cm) &&
+      al16(dproj)) {
+    dim3 g2(cdiv(RR, 64), (unsigned)(ch / 32));
+    EVO_DISPATCH_T(dtype, T, {
+      trimul_gate_bwd_vec_kernel<T><<<g2, 256, 0, (cudaStream_t)stream>>>(
+          (const T*)proj, ld, b_ap, b_ag, b_bp, b_bg, mask, (const T*)da_cm, (const T*)db_cm, (T*)dproj, RR,
+          (int)ch);
+    });
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+    return EVO_OK;
+  }
   dim3 grid(cdiv(RR, TT), cdiv(ch, TT));
   EVO_DISPATCH_T(dtype, T, {
     trimul_gate_bwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
@@ -183,6 +351,17 @@ int evo_gated_residual(const void* res, const void* gp, int64_t ld_gp, const flo
                        void* stream) {
   EVO_API_BEGIN
   const int64_t n = rows * C;
+  const int64_t es = dtype == EVO_F32 ? 4 : 2;
+  if (C % 8 == 0 && (ld_gp * es) % 16 == 0 && al16(res) && al16(gp) && al16(y) && al16(g_out) && al16(out)) {
+    const unsigned g8 = (unsigned)imin64((n / 8 + 255) / 256, (int64_t)num_sms() * 16);
+    EVO_DISPATCH_T(dtype, T, {
+      gated_residual_vec_kernel<T><<<g8, 256, 0, (cudaStream_t)stream>>>(
+          (const T*)res, (const T*)gp, ld_gp, bg, (const T*)y, by, (T*)g_out, (T*)out, rows, C);
+    });
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+    return EVO_OK;
+  }
   const unsigned grid = (unsigned)imin64((n + 255) / 256, (int64_t)num_sms() * 16);
   EVO_DISPATCH_T(dtype, T, {
     gated_residual_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
@@ -197,6 +376,16 @@ int evo_gated_residual_bwd(const float* dout, const void* g, const void* y, cons
                            void* dgp, int64_t rows, int64_t C, int dtype, void* stream) {
   EVO_API_BEGIN
   const int64_t n = rows * C;
+  if (C % 8 == 0 && al16(dout) && al16(g) && al16(y) && al16(dyb) && al16(dgp)) {
+    const unsigned g8 = (unsigned)imin64((n / 8 + 255) / 256, (int64_t)num_sms() * 16);
+    EVO_DISPATCH_T(dtype, T, {
+      gated_residual_bwd_vec_kernel<T><<<g8, 256, 0, (cudaStream_t)stream>>>(
+          dout, (const T*)g, (const T*)y, by, (T*)dyb, (T*)dgp, rows, C);
+    });
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+    return EVO_OK;
+  }
   const unsigned grid = (unsigned)imin64((n + 255) / 256, (int64_t)num_sms() * 16);
   EVO_DISPATCH_T(dtype, T, {
     gated_residual_bwd_kernel<T><<<grid, 256, 0, (cudaStream_t)stream>>>(
