@@ -408,6 +408,9 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         float s[16], dp[16], acc[16];
         tc::tmem_ld16(tl + C_S + cg * 16, s);
         tc::tmem_ld16(tl + C_DP + cg * 16, dp);
+        // the previous sub-chunk's bias-gradient store completed while this
+        // thread waited for S/dP (waiting right after the store was a stall)
+        if (BIAS) tc::wait_st();
         if (BIAS) tc::tmem_ld16(tl + C_DB + c0, acc);
         tc::wait_ld();
         if (last_in_batch && has_next) {
@@ -467,7 +470,6 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           pend_b = b;
           pend_c = kc;
         }
-        if (BIAS) tc::wait_st();
       }
       m2 = m2n, Dv = Dvn;
     }
@@ -485,6 +487,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
   }
   // ---- bias-gradient partial of this batch group ----
   if (BIAS && warp < NCW) {
+    tc::wait_st();
     constexpr int PER = LP / 4;
 #pragma unroll 1
     for (int c = 0; c < PER; c += 16) {

@@ -322,6 +322,9 @@ bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, co
   }
   return done;
 }
+bool pair_bias_fwd_mma(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
+                       float* mean, float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap,
+                       cudaStream_t s);  // pair_bias_mma.cu
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
@@ -342,6 +345,8 @@ int evo_pair_bias_fwd_rect(const void* z, int dtype, const float* ln_g, const fl
   EVO_REQUIRE(NI >= 0 && NJ >= 0, EVO_ERR_ARG, "pair_bias: negative extent");
   if (NI * NJ == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (pair_bias_fwd_mma(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, NI, NJ, C, H, swap_xy, s))
+    return EVO_OK;
   if (pair_bias_fwd_tpt(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, NI, NJ, C, H, swap_xy, s))
     return EVO_OK;
   if (pair_bias_fwd_vec(z, dtype, ln_g, ln_b, w_bias, nb, mean, rstd, NI, NJ, C, H, swap_xy, s))
