@@ -153,9 +153,9 @@ class DapEngine(BlockEngine):
         del dt_
         self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats)
 
-    def forward_backward(self, feats, n_cycles: int = 1, recompute: bool = False):
+    def forward_backward(self, feats, n_cycles: int = 1, recompute: bool = False, grad_ready=None):
         self.comm.phase = "fwd"
-        out = super().forward_backward(feats, n_cycles, recompute=recompute)
+        out = super().forward_backward(feats, n_cycles, recompute=recompute, grad_ready=grad_ready)
         self.comm.phase = "bwd"
         return out
 

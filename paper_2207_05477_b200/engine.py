@@ -639,6 +639,22 @@ class BlockEngine:
     def grad_region(self):
         return self.st.regions["grads"]
 
+    def block_grad_view(self, i):
+        """(view, lo, hi): block i's contiguous slice of the pooled grad region
+        (its parameters are consecutive in the flatten order), in elements."""
+        spans = getattr(self, "_block_spans", None)
+        if spans is None:
+            spans = {}
+            for sl in self.st.slots:
+                if sl.name.startswith("block"):
+                    b = int(sl.name.split(".")[0][5:])
+                    lo, hi = sl.offset // 4, (sl.offset + sl.padded_bytes) // 4
+                    cur = spans.get(b)
+                    spans[b] = (lo, hi) if cur is None else (min(cur[0], lo), max(cur[1], hi))
+            self._block_spans = spans
+        lo, hi = spans[i]
+        return self.grad_region()[lo:hi], lo, hi
+
     def empty_like(self, t):
         return torch.empty_like(t)
 
@@ -733,7 +749,7 @@ class BlockEngine:
         _, sp = self.pair_branch_fwd(i, pair_mid, feats)
         return sm, so, sp
 
-    def blocks_bwd(self, d_msa, d_pair, saved, feats, inputs=None):
+    def blocks_bwd(self, d_msa, d_pair, saved, feats, inputs=None, grad_ready=None):
         """All blocks backward, in place on (d_msa, d_pair); frees ``saved``.
 
         With ``inputs`` (recompute) ``saved`` is unused: block i's saved tensors are recomputed from ``inputs[i]`` right before its
@@ -744,7 +760,11 @@ class BlockEngine:
         copy of d(pair_mid) -- also moves to the side stream, where it overlaps
         the main stream's pair-branch backward of block i-1.  The per-block
         deferred reductions then alternate between two arenas and are finalised
-        on the side stream once both streams' kernels of the block are done."""
+        on the side stream once both streams' kernels of the block are done.
+
+        ``grad_ready(i, stream)`` is called once block i's parameter gradients
+        are final on ``stream`` (None: the current stream) -- the hook of the
+        bucketed data-parallel gradient all-reduce (parallel._GradBuckets)."""
         n = self.cfg.n_blocks
         if inputs is not None:
             saved = [None] * n
@@ -754,6 +774,8 @@ class BlockEngine:
                     saved[i] = self.block_refwd(i, *inputs[i], feats)
                 with self.deferred():
                     self.block_bwd(i, d_msa, d_pair, saved[i], feats)
+                if grad_ready is not None:
+                    grad_ready(i, None)
                 saved[i] = None
             return
         main, side = torch.cuda.current_stream(), self._side_stream()
@@ -784,6 +806,8 @@ class BlockEngine:
                 del dxl
                 side.wait_stream(main)                          # every partial of block i written
                 ops.defer_end(side)
+                if grad_ready is not None:
+                    grad_ready(i, side)
             keep.append(d_act)
             saved[i] = None
         main.wait_stream(side)
@@ -793,7 +817,8 @@ class BlockEngine:
         msa, pair, _ = self.embed_fwd(feats, prev)
         return self.blocks_fwd(msa, pair, feats)
 
-    def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1, recompute: bool = False):
+    def forward_backward(self, feats: DeviceFeatures, n_cycles: int = 1, recompute: bool = False,
+                         grad_ready=None):
         """``_serial_grads`` (src/harness.py:327-352): n-1 untaped recycling
         passes, one differentiated pass; grads land in the pooled region.
         ``recompute`` keeps only each block's inputs through the forward and
@@ -812,7 +837,7 @@ class BlockEngine:
             saved, inputs = [], None
             msa, pair = self.blocks_fwd(msa, pair, feats, saved)
         loss, d_msa, d_pair = self.loss(msa, pair)
-        self.blocks_bwd(d_msa, d_pair, saved, feats, inputs)
+        self.blocks_bwd(d_msa, d_pair, saved, feats, inputs, grad_ready=grad_ready)
         if inputs is not None:
             inputs.clear()                       # blocks_bwd joined the side stream
         with self.deferred():

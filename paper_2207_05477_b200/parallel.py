@@ -14,11 +14,16 @@ CPU tests) instead of thread-simulated ranks:
 * per block and step: forward broadcasts opm (root 0), msa' (root 0),
   pair' (root 1); backward one all-reduce of d(pair_in) -- exactly the
   reference's 3 Broadcast + 1 AllReduce (tests/test_acceptance.py:156-166);
+* forward broadcasts are asynchronous on NCCL: each rank's stream waits only
+  where it reads a received tensor, so rank 0 computes opm(i+1) while rank 1
+  still runs the pair stack of block i;
 * gradient exchange: the closing broadcast of d(msa) (module "msa_grad"),
-  then ONE all-reduce of the whole pooled grad region over the world (each
+  then the all-reduce of the pooled grad region over the world (each
   parameter's gradient is non-zero on exactly one rank of a BP pair, so the
   sum equals the reference's per-branch broadcasts), scaled by 1/dp -- the
-  DP average of src/harness.py:607-616 folded into the same collective.
+  DP average of src/harness.py:607-616 folded into the same collective.  It
+  is bucketed per block and issued as each block's backward finishes
+  (``_GradBuckets``), one logical trace record.
 
 The step is written against a small engine protocol (``BlockEngine`` on the
 GPU; the tests drive it with an adapter around the CPU oracle), and a
@@ -121,26 +126,49 @@ class Comm:
                                        primitive, t.numel() * t.element_size(), module))
         self._seq += 1
 
-    def broadcast(self, t: torch.Tensor, root: int, module: str) -> torch.Tensor:
-        """In place: ``t`` is the payload on the root, the receive buffer elsewhere."""
+    def broadcast(self, t: torch.Tensor, root: int, module: str, async_op: bool = False):
+        """In place: ``t`` is the payload on the root, the receive buffer elsewhere.
+
+        ``async_op`` (device tensors on NCCL): the collective is ordered after
+        the work already queued on the current stream but the stream does not
+        wait for it; returns a handle whose ``wait()`` makes the current stream
+        wait (None when the collective already completed, e.g. on gloo)."""
+        handle = None
         if self._host(t):
             h = t.cpu()
             dist.broadcast(h, src=self.ranks[root], group=self.group)
             t.copy_(h)
+        elif async_op and self._nccl(t):
+            handle = dist.broadcast(t, src=self.ranks[root], group=self.group, async_op=True)
         else:
             dist.broadcast(t, src=self.ranks[root], group=self.group)
         self._rec("broadcast", t, module)
-        return t
+        return handle if async_op else t
 
     def allreduce_sum(self, t: torch.Tensor, module: str) -> torch.Tensor:
-        if self._host(t):
-            h = t.cpu()
-            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
-            t.copy_(h)
-        else:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        self.allreduce_sum_raw(t)
         self._rec("allreduce", t, module)
         return t
+
+    def allreduce_sum_raw(self, t: torch.Tensor, stream=None, async_op: bool = False):
+        """Sum over the group without a trace record (one bucket of a logical
+        collective that the caller records once).  With ``stream`` the
+        collective is ordered after that stream's queued work; with
+        ``async_op`` on NCCL the handle is returned (see ``broadcast``)."""
+        ctx = torch.cuda.stream(stream) if stream is not None else _NullCtx()
+        with ctx:
+            if self._host(t):
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(h)
+            elif async_op and self._nccl(t):
+                return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return None
+
+    def _nccl(self, t):
+        return t.is_cuda and dist.get_backend(self.group) == "nccl"
 
     # -- DAP primitives (src/harness.py:262-293): dim-0 chunk i <-> group rank i ----
     # NCCL runs them on device buffers; a gloo group (the CPU tests, and the
@@ -255,31 +283,55 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
         prev = engine.forward_only(feats, prev)
     msa, pair, rec = engine.embed_fwd(feats, prev)
     saved = []
-    for i in range(n_blocks):
-        if me == 0:
-            opm, so = engine.opm_fwd(msa, f"block{i}.opm", feats, pair_res=None)
-            bp.broadcast(opm, 0, "opm")
+    # Forward, per block i: broadcasts opm(i) (root 0), msa(i) (root 0),
+    # pair(i) (root 1) in that order on both ranks.  On NCCL they are issued
+    # asynchronously and each rank's stream waits only where it reads a
+    # received tensor, so rank 0 computes opm(i+1) (it needs only msa(i))
+    # while rank 1's pair stack of block i still runs, and rank 1 posts the
+    # msa(i) receive before its pair stack instead of stalling on it.
+    if me == 0:
+        h_pair = None
+        opm, so = (engine.opm_fwd(msa, "block0.opm", feats, pair_res=None) if n_blocks else (None, None))
+        if n_blocks:
+            bp.broadcast(opm, 0, "opm", async_op=True)
+        for i in range(n_blocks):
+            _wait(h_pair)                                # pair(i-1) from rank 1
             msa_out, sm = engine.msa_branch_fwd(i, msa, pair, feats)
-            bp.broadcast(msa_out, 0, "msa_stack")
+            bp.broadcast(msa_out, 0, "msa_stack", async_op=True)
             pair_out = engine.empty_like(pair)
-            bp.broadcast(pair_out, 1, "pair_stack")
+            h_pair = bp.broadcast(pair_out, 1, "pair_stack", async_op=True)
             saved.append((msa, pair) if recompute else (so, sm))
-        else:
+            if i + 1 < n_blocks:
+                opm, so = engine.opm_fwd(msa_out, f"block{i + 1}.opm", feats, pair_res=None)
+                bp.broadcast(opm, 0, "opm", async_op=True)
+            msa, pair = msa_out, pair_out
+        _wait(h_pair)
+    else:
+        h_msa = h_opm = None
+        opm = None
+        if n_blocks:
             opm = engine.empty_like(pair)
-            bp.broadcast(opm, 0, "opm")
+            h_opm = bp.broadcast(opm, 0, "opm", async_op=True)
+        for i in range(n_blocks):
+            msa_out = engine.empty_like(msa)
+            h_msa = bp.broadcast(msa_out, 0, "msa_stack", async_op=True)
+            _wait(h_opm)
             pair_mid = engine.add(pair, opm)
             pair_out, sp = engine.pair_branch_fwd(i, pair_mid, feats)
-            msa_out = engine.empty_like(msa)
-            bp.broadcast(msa_out, 0, "msa_stack")
-            bp.broadcast(pair_out, 1, "pair_stack")
+            bp.broadcast(pair_out, 1, "pair_stack", async_op=True)
             saved.append(pair_mid if recompute else sp)
-        del opm
-        msa, pair = msa_out, pair_out
+            if i + 1 < n_blocks:
+                opm = engine.empty_like(pair)
+                h_opm = bp.broadcast(opm, 0, "opm", async_op=True)
+            msa, pair = msa_out, pair_out
+        _wait(h_msa)
+    opm = None
     loss, d_msa, d_pair = engine.loss(msa, pair)
 
     for c in (bp, world):
         c.phase = "bwd"
     deferred = getattr(engine, "deferred", None)
+    buckets = _GradBuckets(engine, world)
     for i in reversed(range(n_blocks)):
         if recompute and me == 0:
             msa_in, pair_in = saved[i]
@@ -293,13 +345,14 @@ def bp_step(engine, feats, bp: Comm, world: Comm, grid: GridConfig, n_blocks: in
             _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair)
             if me == 0:
                 d_pair = saved[i]  # the all-reduced d(pair_in), see _bp_block_bwd
+        buckets.block_done(i)      # block i's gradients are final on this rank
         saved[i] = None
     # embeddings: each worker closes out its own branch (src/harness.py:518-522)
     if me == 0:
         engine.embed_bwd(d_msa, engine.zeros_like(d_pair), feats, rec, which="msa")
     else:
         engine.embed_bwd(engine.zeros_like(d_msa), d_pair, feats, rec, which="pair")
-    return _bp_close(engine, bp, world, grid, me, d_msa, loss)
+    return _bp_close(engine, bp, world, grid, me, d_msa, loss, buckets)
 
 
 class _NullCtx:
@@ -308,6 +361,55 @@ class _NullCtx:
 
     def __exit__(self, *exc):
         return False
+
+
+def _wait(handle):
+    if handle is not None:
+        handle.wait()
+
+
+class _GradBuckets:
+    """The world gradient all-reduce, bucketed per Evoformer block.
+
+    The reference sums the flattened gradients of every parameter in one
+    collective after the backward (src/harness.py:607-616).  Here block i's
+    slice of the pooled grad region is all-reduced as soon as block i's
+    backward has produced it -- asynchronously on NCCL, ordered after the
+    stream that finished it -- so it overlaps the backward of blocks i-1 .. 0;
+    the rest of the region (embeddings, recycling) goes at the close.  The
+    trace keeps the reference's single logical "grad_sync" record (bytes of
+    the whole region).  Engines without ``block_grad_view`` (the CPU oracle
+    adapter) fall back to the one-shot collective."""
+
+    def __init__(self, engine, world):
+        self.view = getattr(engine, "block_grad_view", None)
+        self.world = world
+        self.handles = []
+        self.done = []  # (lo, hi) element ranges already issued
+
+    def block_done(self, i, stream=None):
+        if self.view is None:
+            return
+        v, lo, hi = self.view(i)
+        self.handles.append(self.world.allreduce_sum_raw(v, stream=stream, async_op=True))
+        self.done.append((lo, hi))
+
+    def close(self, g):
+        """All-reduce what is left of ``g``, wait for every bucket, record once."""
+        if self.view is None:
+            self.world.allreduce_sum(g, "grad_sync")
+            return
+        cur = 0
+        for lo, hi in sorted(self.done):
+            if lo > cur:
+                self.handles.append(self.world.allreduce_sum_raw(g[cur:lo], async_op=True))
+            cur = max(cur, hi)
+        if cur < g.numel():
+            self.handles.append(self.world.allreduce_sum_raw(g[cur:], async_op=True))
+        for h in self.handles:
+            _wait(h)
+        self.handles.clear()
+        self.world._rec("allreduce", g, "grad_sync")
 
 
 def _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair):
@@ -329,13 +431,13 @@ def _bp_block_bwd(engine, feats, bp, me, i, saved, d_msa, d_pair):
         bp.allreduce_sum(d_pair, "pair_stack")
 
 
-def _bp_close(engine, bp, world, grid, me, d_msa, loss):
+def _bp_close(engine, bp, world, grid, me, d_msa, loss, buckets=None):
     for c in (bp, world):
         c.phase = "grad-sync"
     closing = d_msa if me == 0 else engine.empty_like(d_msa)
     bp.broadcast(closing, 0, "msa_grad")
     g = engine.grad_region()
-    world.allreduce_sum(g, "grad_sync")
+    (buckets or _GradBuckets(None, world)).close(g)
     if grid.dp > 1:
         g.mul_(np.float32(1.0 / grid.dp).item())
     lt = loss.reshape(1).clone()
@@ -352,9 +454,13 @@ def dp_step(engine, feats, world: Comm, grid: GridConfig, n_cycles: int = 1, ste
     pooled grad region (src/harness.py:607-616)."""
     world.step = step
     world.phase = "grad-sync"
-    loss, _ = engine.forward_backward(feats, n_cycles, recompute=recompute)
+    buckets = _GradBuckets(engine, world)
+    if buckets.view is not None:
+        loss, _ = engine.forward_backward(feats, n_cycles, recompute=recompute, grad_ready=buckets.block_done)
+    else:
+        loss, _ = engine.forward_backward(feats, n_cycles, recompute=recompute)
     g = engine.grad_region()
-    world.allreduce_sum(g, "grad_sync")
+    buckets.close(g)
     g.mul_(np.float32(1.0 / grid.dp).item())
     lt = loss.reshape(1).clone()
     world.allreduce_sum(lt, "loss")

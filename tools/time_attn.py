@@ -51,6 +51,12 @@ def main():
         tf = timeit(lambda: ops.attn_fwd(qkvg, mask, msb, msl, bias, bg, B, L, H, D, sb, sl))
         tb = timeit(lambda: ops.attn_bwd(qkvg, mask, msb, msl, bias, ctx, gate, dg, lse, dbg, B, L, H, D,
                                          sb, sl, want_dbias=bias is not None))
+        if bias is not None and os.environ.get("ATTN_ABLATE"):
+            tnb = timeit(lambda: ops.attn_bwd(qkvg, mask, msb, msl, bias, ctx, gate, dg, lse, dbg, B, L, H, D,
+                                              sb, sl, want_dbias=False))
+            tnn = timeit(lambda: ops.attn_bwd(qkvg, mask, msb, msl, None, ctx, gate, dg, lse, dbg, B, L, H, D,
+                                              sb, sl, want_dbias=False))
+            print(f"   ablation: bwd without d(bias) {tnb:8.1f} us, without bias at all {tnn:8.1f} us")
         exps = B * H * L * L
         print(f"{which}: B={B} L={L} H={H} D={D}  fwd {tf:8.1f} us  bwd(all kernels) {tb:8.1f} us  "
               f"ex2 bound {exps / (148 * 16 * 1.965e3):.1f} us")
