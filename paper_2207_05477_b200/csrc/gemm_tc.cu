@@ -934,7 +934,19 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
   // split-K problems (few output tiles, long K): 128-wide tiles give twice
   // the tiles per split and halve each CTA's B stream (measured faster on
   // every weight-gradient shape of the block)
-  if (BN == 256 && batch == 1 && ((M + BM - 1) / BM) * ((N + 255) / 256) < num_sms() && (K + BK - 1) / BK >= 16)
+  // -- unless CTA pairs take them (cta_group::2, 256 x 256 per pair, each CTA
+  // streaming only half of B: half the L2->SM bytes per output of 128 x 128
+  // tiles, which is what bounds these GEMMs)
+  static const bool cg2_split = [] {  // A/B: EVO_GEMM_CG2_SPLIT=0
+    const char* e = getenv("EVO_GEMM_CG2_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  // (measured: 256x1024 and 1024x256 weight gradients 5% faster; with fewer
+  // than 8 pair-halves per split, e.g. 256x256, slower -- tools/splitk_sweep.py)
+  const bool pair_split = cg2_split && !opm && !cmask && batch == 1 && (M + BM - 1) / BM >= 2 &&
+                          ((M + BM - 1) / BM) * ((N + 255) / 256) >= 8 && !cg2_disabled();
+  if (BN == 256 && batch == 1 && ((M + BM - 1) / BM) * ((N + 255) / 256) < num_sms() && (K + BK - 1) / BK >= 16 &&
+      !pair_split)
     BN = 128;
   if (const int f = forced_bn(); f && f < BN) BN = f;
   Params p{};
@@ -989,7 +1001,8 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
     const char* e = getenv("EVO_GEMM_CG2_MINKB");
     return e ? atoi(e) : 8;
   }();
-  const bool cg2 = !bres && BN == 256 && !p.partial && p.kblocks >= cg2_minkb && p.n_mt >= 2 && !cg2_disabled();
+  const bool cg2 = !bres && BN == 256 && (!p.partial || pair_split) && p.kblocks >= cg2_minkb && p.n_mt >= 2 &&
+                   !cg2_disabled();
   if (cg2) p.tiles = (int)((int64_t)batch * ((p.n_mt + 1) / 2) * p.n_nt * splits);
 
   CUtensorMap ma, mb, md, mc;
