@@ -937,9 +937,11 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
   // -- unless CTA pairs take them (cta_group::2, 256 x 256 per pair, each CTA
   // streaming only half of B: half the L2->SM bytes per output of 128 x 128
   // tiles, which is what bounds these GEMMs)
-  static const bool cg2_split = [] {  // A/B: EVO_GEMM_CG2_SPLIT=0
+  // Off by default: 5% faster in isolation, but in the two-stream step the
+  // CTA pairs (two co-scheduled SMs) measured 0.5 ms slower (EVO_GEMM_CG2_SPLIT=1 enables)
+  static const bool cg2_split = [] {
     const char* e = getenv("EVO_GEMM_CG2_SPLIT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   // (measured: 256x1024 and 1024x256 weight gradients 5% faster; with fewer
   // than 8 pair-halves per split, e.g. 256x256, slower -- tools/splitk_sweep.py)
