@@ -97,10 +97,15 @@ int evo_gemm_bias(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, i
 
 /* D[M, N] = (h > 0) ? op(A) op(B) : 0 -- the transition's ReLU backward in the
  * epilogue of the d(hidden) projection (src/model.py:344-348 differentiated);
- * h is the saved ReLU output, [M, N] contiguous like D.  bf16 on the tensor
+ * h is the saved ReLU output, [M, N] contiguous like D.  With colsum != NULL
+ * the epilogue also forms the column sums of the stored D (the hidden bias
+ * gradient, b1), written (or added, accumulate = 1) to colsum[N] in a fixed
+ * order; ws >= evo_gemm_relu_mask_workspace(M, N) bytes.  bf16 on the tensor
  * cores; EVO_ERR_UNSUPPORTED otherwise (the caller masks separately). */
+int64_t evo_gemm_relu_mask_workspace(int64_t M, int64_t N);
 int evo_gemm_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
-                       int64_t ldb, int trans_b, const void* h, void* D, int dtype, void* stream);
+                       int64_t ldb, int trans_b, const void* h, void* D, int dtype, float* colsum, int accumulate,
+                       void* ws, void* stream);
 
 /* ---- LayerNorm (src/tensor.py:173-208) -----------------------------------
  * y = (x - mean) * rstd * gamma + beta over the last dim C; saves mean/rstd. */

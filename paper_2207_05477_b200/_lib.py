@@ -34,7 +34,8 @@ SIGNATURES = {
     "evo_gemm": (_i, [_i64, _i64, _i64, _p, _i64, _i, _i64, _p, _i64, _i, _i64, _p, _i64, _i64,
                       _i, _f, _f, _i, _i, _p]),
     "evo_gemm_tc_launches": (_i64, []),
-    "evo_gemm_relu_mask": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _p, _i, _p]),
+    "evo_gemm_relu_mask": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _p, _i, _p, _i, _p, _p]),
+    "evo_gemm_relu_mask_workspace": (_i64, [_i64, _i64]),
     "evo_gemm_bias": (_i, [_i64, _i64, _i64, _p, _i64, _i, _p, _i64, _i, _p, _i, _p, _p, _i, _p, _i64, _i,
                            _i, _p]),
     "evo_layernorm_fwd": (_i, [_p, _i, _p, _p, _p, _i, _p, _p, _i64, _i64, _f, _p]),

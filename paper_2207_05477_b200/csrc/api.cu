@@ -93,7 +93,9 @@ static void gemm_route(int64_t M, int64_t N, int64_t K, const void* A, int64_t l
             relu, ab_dtype, d_dtype, s);
 }
 bool gemm_tc_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, const void* B,
-                       int64_t ldb, int tb, const void* h, void* D, int d_dtype, cudaStream_t s);  // gemm_tc.cu
+                       int64_t ldb, int tb, const void* h, void* D, int d_dtype, cudaStream_t s, float* colsum,
+                       int accumulate, void* ws);  // gemm_tc.cu
+int64_t gemm_tc_relu_mask_ws(int64_t M, int64_t N);
 bool gemm_tc_try(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                  const void* B, int64_t ldb, int tb, int64_t sb, void* C, int64_t ldc, int64_t sc,
                  int batch, float alpha, float beta, int ab, int cd, cudaStream_t s);
@@ -275,13 +277,17 @@ int evo_gemm(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int tr
   EVO_API_END
 }
 
+int64_t evo_gemm_relu_mask_workspace(int64_t M, int64_t N) { return gemm_tc_relu_mask_ws(M, N); }
+
 int evo_gemm_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int trans_a, const void* B,
-                       int64_t ldb, int trans_b, const void* h, void* D, int dtype, void* stream) {
+                       int64_t ldb, int trans_b, const void* h, void* D, int dtype, float* colsum, int accumulate,
+                       void* ws, void* stream) {
   EVO_API_BEGIN
   EVO_REQUIRE(M >= 0 && N >= 0 && K >= 0, EVO_ERR_ARG, "gemm_relu_mask: bad extents");
   if (M == 0 || N == 0) return EVO_OK;
+  EVO_REQUIRE(colsum == nullptr || ws != nullptr, EVO_ERR_ARG, "gemm_relu_mask: column sums need a workspace");
   EVO_REQUIRE(dtype == EVO_BF16 && gemm_tc_relu_mask(M, N, K, A, lda, trans_a, B, ldb, trans_b, h, D, dtype,
-                                                    (cudaStream_t)stream),
+                                                    (cudaStream_t)stream, colsum, accumulate, ws),
               EVO_ERR_UNSUPPORTED, "gemm_relu_mask: bf16, TMA-addressable operands only");
   EVO_API_END
 }

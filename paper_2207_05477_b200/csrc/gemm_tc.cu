@@ -106,6 +106,10 @@ struct Params {
   int pmode, R;
   const float* rec;
   int cmask;  // the C tile masks instead of adding: D = (C > 0) ? acc : 0 (ReLU backward)
+  // per-warp column sums of the stored (bf16) D tile: row (m-tile * 4 + TMEM
+  // lane quarter) of a [n_mt * 4, N] partial block (the bias gradient of the
+  // next layer, finalised in fixed order by finalize_partials)
+  float* csum;
 };
 
 // --- TMA / bulk-async helpers -------------------------------------------------
@@ -561,6 +565,23 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
           tma_store3(&tmD, sbuf, n0 + cc, row0, zout);
           bulk_commit();
         }
+        if constexpr (!OUT_F32) {
+          if (p.csum) {
+            // columns 2*lane, 2*lane+1 of this chunk summed over the warp's
+            // 32 staged rows (the rounded values D holds; rows past M are 0)
+            float2 cs = make_float2(0.f, 0.f);
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+              const uint32_t wv = *reinterpret_cast<const uint32_t*>(
+                  sbuf + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + ((lane & 3) << 2));
+              cs = __fadd2_rn(cs, tc::bf16x2_f2(wv));
+            }
+            const int col = n0 + cc + 2 * lane;
+            float* dst = p.csum + (int64_t)((c.m0 / BM) * 4 + quarter) * p.N + col;
+            if (col < p.N) dst[0] = cs.x;
+            if (col + 1 < p.N) dst[1] = cs.y;
+          }
+        }
         if constexpr (F::STG_BUFS == 2) buf ^= 1;
       }
       tc::fence_before();
@@ -891,7 +912,7 @@ bool opm_map(CUtensorMap* m, void* base, const OpmOut& o) {
 static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                          const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
                          float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
-                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask = 0);
+                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask = 0, float* csum = nullptr);
 
 bool gemm_tc(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa, const void* B,
              int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch, float alpha,
@@ -915,17 +936,25 @@ bool gemm_tc_opm(int mode, int64_t M, int64_t N, int64_t K, const void* A, int64
 
 // D = (h > 0) ? op(A) op(B) : 0 -- the ReLU backward in the epilogue of the
 // d(hidden) GEMM (h: the saved ReLU output, [M, N] like D)
+int64_t gemm_tc_relu_mask_ws(int64_t M, int64_t N) { return ((M + BM - 1) / BM) * 4 * N * 4; }
+
 bool gemm_tc_relu_mask(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, const void* B,
-                       int64_t ldb, int tb, const void* h, void* D, int d_dtype, cudaStream_t s) {
-  return gemm_tc_impl(M, N, K, A, lda, ta, 0, B, ldb, tb, 0, D, N, 0, 1, 1.f, 0.f, h, N, nullptr, 0, d_dtype, s,
-                      nullptr, 1);
+                       int64_t ldb, int tb, const void* h, void* D, int d_dtype, cudaStream_t s, float* colsum,
+                       int accumulate, void* ws) {
+  float* part = colsum ? partial_buffer(ws, (size_t)gemm_tc_relu_mask_ws(M, N)) : nullptr;
+  if (!gemm_tc_impl(M, N, K, A, lda, ta, 0, B, ldb, tb, 0, D, N, 0, 1, 1.f, 0.f, h, N, nullptr, 0, d_dtype, s,
+                    nullptr, 1, part))
+    return false;
+  if (colsum) finalize_partials(part, (int)(((M + BM - 1) / BM) * 4), N, colsum, accumulate, s);
+  return true;
 }
 
 static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int ta, int64_t sa,
                          const void* B, int64_t ldb, int tb, int64_t sb, void* D, int64_t ldd, int64_t sd, int batch,
                          float alpha, float beta, const void* Cin, int64_t ldc, const float* bias, int relu,
-                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask) {
+                         int d_dtype, cudaStream_t s, const OpmOut* opm, int cmask, float* csum) {
   if (tc_gemm_disabled()) return false;
+  if (csum && (d_dtype != EVO_BF16 || batch != 1)) return false;
   if (M <= 0 || N <= 0 || K <= 0 || batch < 1) return false;
   if (M > (1ll << 31) - BM || N > (1ll << 31) - 256 || K > (1ll << 31) - BK) return false;
   const bool f32 = d_dtype == EVO_F32;
@@ -967,12 +996,13 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
   p.relu = relu;
   p.has_res = has_res ? 1 : 0;
   p.cmask = cmask;
+  p.csum = csum;
   const int nsm = num_sms();
   const int64_t base = (int64_t)batch * p.n_mt * p.n_nt;
   if (base > (1ll << 30)) return false;
   // split K when the output tiles cannot fill the SMs and K is long
   int splits = 1;
-  if (!opm && !cmask && batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
+  if (!opm && !cmask && !csum && batch == 1 && base < nsm && p.kblocks >= 16 && N % 4 == 0) {
     // >= 8 k-blocks (K >= 512) per split; at most 64 partial planes; the
     // split tiles must fit one wave of the persistent grid (a second, mostly
     // idle wave doubles the kernel time)

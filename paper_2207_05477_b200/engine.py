@@ -319,9 +319,8 @@ class BlockEngine:
         ops.colsum_cast(d, self.G(f"{prefix}.b2"), y=d_act)
         ops.gemm(h, d_act, self.Gm(f"{prefix}.w2", F), ta=True)
         dh = torch.empty((T, F), dtype=dt, device=d.device)
-        if dt == torch.bfloat16:  # ReLU mask in the GEMM epilogue, then a read-only column sum
-            ops.gemm_relu_mask(d_act, self.W(f"{prefix}.w2", F), h, dh, tb=True)
-            ops.colsum_cast(dh, self.G(f"{prefix}.b1"))
+        if dt == torch.bfloat16:  # ReLU mask and the b1 column sums in the GEMM epilogue
+            ops.gemm_relu_mask(d_act, self.W(f"{prefix}.w2", F), h, dh, tb=True, colsum=self.G(f"{prefix}.b1"))
         else:
             ops.gemm(d_act, self.W(f"{prefix}.w2", F), dh, tb=True)
             ops.relu_bwd_colsum_(dh, h, self.G(f"{prefix}.b1"))

@@ -98,17 +98,20 @@ def gemm_bias(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias: torch.T
     return out
 
 
-def gemm_relu_mask(a, b, h, out, ta=False, tb=False):
+def gemm_relu_mask(a, b, h, out, ta=False, tb=False, colsum=None, accumulate=False):
     """out = (h > 0) * (op(a) @ op(b)): the ReLU backward fused into the
-    d(hidden) GEMM's epilogue (bf16 only)."""
+    d(hidden) GEMM's epilogue (bf16 only); with ``colsum`` (fp32 [N]) the
+    epilogue also writes the column sums of ``out`` (the hidden bias
+    gradient)."""
     M, K = (a.shape[1], a.shape[0]) if ta else (a.shape[0], a.shape[1])
     Kb, N = (b.shape[1], b.shape[0]) if tb else (b.shape[0], b.shape[1])
     if K != Kb or tuple(out.shape) != (M, N) or tuple(h.shape) != (M, N):
         raise ValueError("gemm_relu_mask shape mismatch")
     if not (h.is_contiguous() and out.is_contiguous()):
         raise ValueError("gemm_relu_mask: h and out must be contiguous")
+    ws = _ws(_lib.load().evo_gemm_relu_mask_workspace(M, N), out.device) if colsum is not None else None
     call("evo_gemm_relu_mask", M, N, K, ptr(a), a.stride(0), int(ta), ptr(b), b.stride(0), int(tb), ptr(h),
-         ptr(out), dcode(out), stream())
+         ptr(out), dcode(out), ptr(colsum), int(accumulate), ptr(ws), stream())
     return out
 
 

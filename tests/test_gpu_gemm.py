@@ -184,8 +184,15 @@ def test_gemm_relu_mask_epilogue(M, N, K):
     b = torch.randn(N, K, device="cuda").bfloat16()
     h = torch.relu(torch.randn(M, N, device="cuda")).bfloat16()
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ops.gemm_relu_mask(a, b, h, out, tb=True)
+    cs = torch.full((N,), 7.0, device="cuda")
+    ops.gemm_relu_mask(a, b, h, out, tb=True, colsum=cs)
     ref = (a.float() @ b.float().t()) * (h.float() > 0)
     assert torch.all(out[h == 0] == 0)
     err = (out.float() - ref).abs().max() / ref.abs().max()
     assert err <= 1e-2, float(err)
+    # the epilogue's column sums are those of the stored bf16 values
+    want = out.double().sum(0).float()
+    assert float((cs - want).abs().max() / want.abs().max()) <= 1e-5
+    acc = cs.clone()
+    ops.gemm_relu_mask(a, b, h, out, tb=True, colsum=acc, accumulate=True)
+    assert float((acc - 2 * cs).abs().max() / cs.abs().max()) <= 1e-6
