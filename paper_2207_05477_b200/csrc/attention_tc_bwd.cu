@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
     const bf16* __restrict__ ctx, const bf16* __restrict__ gate, const bf16* __restrict__ dgated,
     bf16* __restrict__ dqkvg, bf16* __restrict__ dctx, float* __restrict__ Dvec, int64_t T, int H,
     int64_t ld, const float* __restrict__ mask, int64_t msb, int64_t msl, float* __restrict__ mbias,
-    int64_t B, int64_t L, int64_t sb, int64_t sl, const float* __restrict__ lse) {
+    int64_t B, int64_t L, int64_t sb, int64_t sl, const float* __restrict__ lse, float* __restrict__ gpart) {
   // key-mask bias of every (batch, key), [b][l] contiguous, in the log2
   // domain of the softmax: (m - 1) * 1e9 * log2(e)  (src/attention.py:151)
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * L;
@@ -533,6 +533,10 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
   const int64_t HD8 = (int64_t)H * D / 8;
   const int64_t n = T * HD8;
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  // gate-bias gradient: this thread's 8 columns (c8 is fixed per thread when
+  // HD8 divides the block size -- checked by the host) summed over its tokens,
+  // as the stored bf16 d(gate) values
+  float gs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += step) {
     const int64_t e = base + threadIdx.x;
     const bool act = e < n;
@@ -561,6 +565,9 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
         dsum += __bfloat162float(dq.x) * cv[u] + __bfloat162float(dq.y) * cv[u + 1];
         pc[u / 2] = *reinterpret_cast<const uint32_t*>(&dq);
         pg[u / 2] = tc::pack_bf16(g0, g1);
+        const float2 gr = tc::bf16x2_f2(pg[u / 2]);
+        gs[u] += gr.x;
+        gs[u + 1] += gr.y;
       }
       *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
       *reinterpret_cast<uint4*>(dqkvg + t * ld + 3 * HD8 * 8 + c8 * 8) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
@@ -568,6 +575,20 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
     if (act && (c8 % G) == 0) Dvec[t * H + c8 / G] = dsum;
+  }
+  if (gpart) {
+    // block partial of the gate-bias gradient: threads tid, tid + HD8, ...
+    // share column chunk tid % HD8; summed in thread order
+    __shared__ float red[256 * 8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) red[threadIdx.x * 8 + u] = gs[u];
+    __syncthreads();
+    for (int c = threadIdx.x; c < HD8 * 8; c += blockDim.x) {
+      const int c8 = c / 8, u = c % 8;
+      float acc = 0.f;
+      for (int t = c8; t < (int)blockDim.x; t += (int)HD8) acc += red[t * 8 + u];
+      gpart[(int64_t)blockIdx.x * HD8 * 8 + c] = acc;
+    }
   }
 }
 
@@ -747,21 +768,26 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   float* cols = (float*)(w + p.off_cols);
   float* mbias = (float*)(w + p.off_mb);
   const int64_t T = g.B * g.L, HD = g.H * g.D;
+  const int64_t nthr = T * HD / 8;
+  const unsigned pgrid = (unsigned)imin64((nthr + 255) / 256, (int64_t)num_sms() * 8);
+  // the gate-bias column sums ride on the prep kernel when each thread keeps
+  // one column chunk (HD / 8 divides the 256-thread block)
+  const bool gfuse = dbg != nullptr && (256 % (HD / 8)) == 0 && pgrid <= (unsigned)(8 * num_sms());
+  float* gpart = gfuse ? partial_buffer(cols, (size_t)pgrid * HD * 4) : nullptr;
   {
-    const int64_t nthr = T * HD / 8;
-    const unsigned pgrid = (unsigned)imin64((nthr + 255) / 256, (int64_t)num_sms() * 8);
     if (g.D == 16)
       attn_bwd_prep_tc_kernel<16><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L, g.sb, g.sl, lse);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart);
     else
       attn_bwd_prep_tc_kernel<32><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L, g.sb, g.sl, lse);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart);
     EVO_LAUNCH_CHECK();
   }
+  if (gfuse) finalize_partials(gpart, (int)pgrid, HD, dbg, accumulate, s);
   const bool bias = nb != nullptr && dnb != nullptr;
   if (g.D == 16)
     launch_bwd_d<16>(bias, p.LP, qkvg, dctx, mbias, nb, lse, Dvec, dqkvg, kvpart, part, g, p, s, qpart);
@@ -780,14 +806,18 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
     attn_dnb_reduce_kernel<<<cdiv(n, 256), 256, 0, s>>>(part, dnb, n, p.NG, accumulate);
     EVO_LAUNCH_CHECK();
   }
-  if (!colsum_vec((bf16*)dqkvg + 3 * HD, EVO_BF16, g.ld, nullptr, nullptr, EVO_BF16, dbg, accumulate,
-                  cols, T, HD, 0, s)) {
+  int slice = 0;
+  if (!gfuse && !colsum_vec((bf16*)dqkvg + 3 * HD, EVO_BF16, g.ld, nullptr, nullptr, EVO_BF16, dbg, accumulate,
+                            cols, T, HD, 0, s)) {
     const unsigned pg = partial_grid(T);
     colsum_slice_kernel<bf16><<<pg, 256, 0, s>>>((const bf16*)dqkvg, g.ld, 3 * HD, cols, T, HD);
     EVO_LAUNCH_CHECK();
     finalize_partials(cols, pg, HD, dbg, accumulate, s);
+    slice = 1;
   }
-  count_launch(3 + (p.NQT > 1) + bias);
+  // prep, the combine pass, the bias-gradient reduction, the column-slice
+  // sum (the main kernel, colsum_vec and finalize_partials count themselves)
+  count_launch(1 + (p.NKW > 1 || p.NQT > 1) + bias + slice);
   return true;
 }
 
