@@ -143,7 +143,7 @@ class DapEngine(BlockEngine):
         pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
         return pair, ([], s1, s2, s3)
 
-    def pair_branch_bwd(self, i, d_pair, saved, feats):
+    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False):
         p = f"block{i}"
         _, s1, s2, s3 = saved
         self.trans_bwd(d_pair, s3, f"{p}.pair_trans")

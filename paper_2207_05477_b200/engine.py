@@ -310,13 +310,16 @@ class BlockEngine:
                       bias16=self.st.weight(f"{prefix}.b2"))
         return out, dict(x=x, xl=xl, mu=mu, rs=rs, h=h)
 
-    def trans_bwd(self, d, sv, prefix, nxt=None):
+    def trans_bwd(self, d, sv, prefix, nxt=None, d_act=None):
+        """``d_act``: bf16 d(out) with the b2 gradient already taken (emitted by
+        the LayerNorm backward that last wrote ``d``)."""
         dt = self.dt
         T, C = d.shape
         h = sv["h"]
         F = h.shape[1]
-        d_act = torch.empty((T, C), dtype=dt, device=d.device)
-        ops.colsum_cast(d, self.G(f"{prefix}.b2"), y=d_act)
+        if d_act is None:
+            d_act = torch.empty((T, C), dtype=dt, device=d.device)
+            ops.colsum_cast(d, self.G(f"{prefix}.b2"), y=d_act)
         ops.gemm(h, d_act, self.Gm(f"{prefix}.w2", F), ta=True)
         dh = torch.empty((T, F), dtype=dt, device=d.device)
         if dt == torch.bfloat16:  # ReLU mask and the b1 column sums in the GEMM epilogue
@@ -403,9 +406,18 @@ class BlockEngine:
         ops.gemm(d_ab, self.wcat[prefix], dxl, tb=True)
         return dxl
 
-    def opm_ln_bwd(self, dxl, sv, prefix, d_msa):
-        ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d_msa, d_msa,
-                          self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+    def opm_ln_bwd(self, dxl, sv, prefix, d_msa, nxt=None):
+        """d_msa += LN backward of the OPM input.  With ``nxt`` (the b2 slot of
+        the MSA transition that runs next in the backward) it also returns
+        that module's bf16 operand, bias gradient taken (bf16 only)."""
+        if nxt is None or self.dt != torch.bfloat16:
+            ops.layernorm_bwd(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d_msa, d_msa,
+                              self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"))
+            return None
+        d_act = torch.empty(d_msa.shape, dtype=self.dt, device=d_msa.device)
+        ops.layernorm_bwd_ex(sv["x"], dxl, sv["mu"], sv["rs"], self.P(f"{prefix}.ln_g"), d_msa, d_msa,
+                             self.G(f"{prefix}.ln_g"), self.G(f"{prefix}.ln_b"), d_act, nxt)
+        return d_act
 
     # -- TriangleMultiplication (extension; AF2 Alg 11 outgoing / Alg 12 incoming) ---
 
@@ -494,12 +506,13 @@ class BlockEngine:
         msa, s3 = self.trans_fwd(msa, f"{p}.msa_trans")
         return msa, (s1, s2, s3)
 
-    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats, late=None):
+    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats, late=None, d_act=None):
         """d_msa: d(msa_out) -> d(msa_in) in place; the pair-bias path adds
-        d(pair_in) into d_pair_acc (appended to ``late`` instead when given)."""
+        d(pair_in) into d_pair_acc (appended to ``late`` instead when given).
+        ``d_act``: bf16 d_msa with the MSA transition's b2 gradient taken."""
         p = f"block{i}"
         s1, s2, s3 = saved
-        a = self.trans_bwd(d_msa, s3, f"{p}.msa_trans", nxt=self.G(f"{p}.col_attn.attn.bo"))
+        a = self.trans_bwd(d_msa, s3, f"{p}.msa_trans", nxt=self.G(f"{p}.col_attn.attn.bo"), d_act=d_act)
         a = self.attn_bwd(d_msa, s2, f"{p}.col_attn", self.var["col_attn"], feats, d_act=a,
                           nxt=self.G(f"{p}.row_attn.attn.bo"))
         self.attn_bwd(d_msa, s1, f"{p}.row_attn", self.var["row_attn"], feats, dpair=d_pair_acc, d_act=a,
@@ -518,17 +531,22 @@ class BlockEngine:
         pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
         return pair, (tm, s1, s2, s3)
 
-    def pair_branch_bwd(self, i, d_pair, saved, feats):
-        """d(pair_out) -> d(pair_mid) in place."""
+    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False):
+        """d(pair_out) -> d(pair_mid) in place.  With ``opm_nxt`` (the caller
+        runs this block's OPM backward on the same d(pair_mid)) the last
+        LayerNorm backward also emits the OPM's bf16 operand and its b_out
+        gradient, returned for ``opm_bwd_core(d_act=...)``; else None."""
         p = f"block{i}"
         tm, s1, s2, s3 = saved
         a = self.trans_bwd(d_pair, s3, f"{p}.pair_trans", nxt=self.G(f"{p}.tri_end.attn.bo"))
         a = self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats, d_act=a,
                           nxt=self.G(f"{p}.tri_start.attn.bo"))
-        self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats, d_act=a)
+        nxt = self.G(f"{p}.opm.b_out") if opm_nxt and not tm else None
+        a = self.attn_bwd(d_pair, s1, f"{p}.tri_start", self.var["tri_start"], feats, d_act=a, nxt=nxt)
         if tm:
             self.trimul_bwd(d_pair, tm[1], f"{p}.tri_mul_in", feats)
             self.trimul_bwd(d_pair, tm[0], f"{p}.tri_mul_out", feats)
+        return a
 
     # -- whole block (src/model.py:431-445) -------------------------------------------
 
@@ -563,8 +581,8 @@ class BlockEngine:
         """In place: (d msa_out, d pair_out) -> (d msa_in, d pair_in)."""
         sm, so, sp = saved
         if not self.branch_streams:
-            self.pair_branch_bwd(i, d_pair, sp, feats)            # d_pair = d(pair_mid)
-            dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats)
+            a = self.pair_branch_bwd(i, d_pair, sp, feats, opm_nxt=True)  # d_pair = d(pair_mid)
+            dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats, d_act=a)
             self.msa_branch_bwd(i, d_msa, d_pair, sm, feats)      # d_pair += bias path
             self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)      # d_msa += OPM path
             return
@@ -573,8 +591,8 @@ class BlockEngine:
         side.wait_stream(main)
         with torch.cuda.stream(side):
             self.msa_branch_bwd(i, d_msa, d_pair, sm, feats, late=late)
-        self.pair_branch_bwd(i, d_pair, sp, feats)                # d_pair = d(pair_mid)
-        dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats)
+        a = self.pair_branch_bwd(i, d_pair, sp, feats, opm_nxt=True)  # d_pair = d(pair_mid)
+        dxl = self.opm_bwd_core(d_pair, so, f"block{i}.opm", feats, d_act=a)
         main.wait_stream(side)
         for fn in late:                                           # d_pair += bias path
             fn()
@@ -780,6 +798,7 @@ class BlockEngine:
         main, side = torch.cuda.current_stream(), self._side_stream()
         keep = []  # main-stream tensors read by the side stream: alive until the final join
         side.wait_stream(main)
+        msa_act = None  # block i-1's MSA transition operand, emitted by block i's OPM LN backward
         for i in reversed(range(n)):
             if inputs is not None:
                 saved[i] = self.block_refwd(i, *inputs[i], feats)
@@ -787,12 +806,14 @@ class BlockEngine:
             ops.defer_begin(self.arenas[i % 2])
             late = []
             with torch.cuda.stream(side):
-                self.msa_branch_bwd(i, d_msa, d_pair, sm, feats, late=late)
+                self.msa_branch_bwd(i, d_msa, d_pair, sm, feats, late=late, d_act=msa_act)
+                msa_act = None
                 ev_msa = torch.cuda.Event()
                 ev_msa.record(side)
-            self.pair_branch_bwd(i, d_pair, sp, feats)          # d_pair = d(pair_mid)
-            d_act = torch.empty(d_pair.shape, dtype=self.dt, device=d_pair.device)
-            ops.colsum_cast(d_pair, self.G(f"block{i}.opm.b_out"), y=d_act)
+            d_act = self.pair_branch_bwd(i, d_pair, sp, feats, opm_nxt=True)  # d_pair = d(pair_mid)
+            if d_act is None:
+                d_act = torch.empty(d_pair.shape, dtype=self.dt, device=d_pair.device)
+                ops.colsum_cast(d_pair, self.G(f"block{i}.opm.b_out"), y=d_act)
             ev_pair = torch.cuda.Event()
             ev_pair.record(main)
             main.wait_event(ev_msa)
@@ -801,7 +822,8 @@ class BlockEngine:
             with torch.cuda.stream(side):
                 side.wait_event(ev_pair)
                 dxl = self.opm_bwd_core(None, so, f"block{i}.opm", feats, d_act=d_act)
-                self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa)  # d_msa += OPM path
+                msa_act = self.opm_ln_bwd(dxl, so, f"block{i}.opm", d_msa,  # d_msa += OPM path
+                                          nxt=self.G(f"block{i - 1}.msa_trans.b2") if i > 0 else None)
                 del dxl
                 side.wait_stream(main)                          # every partial of block i written
                 ops.defer_end(side)
