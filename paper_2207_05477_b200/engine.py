@@ -104,6 +104,10 @@ class BlockEngine:
                                and os.environ.get("EVO_BRANCH_STREAMS", "1") != "0")
         self._s2 = None
         self.opm_dnum_fused = os.environ.get("EVO_OPM_DNUM_TC", "1") != "0"
+        # d(LN output) from the dX GEMMs in the activation dtype: the bf16 policy
+        # stores it in bf16 like every other GEMM operand / output of the
+        # backward (EVO_DXL_BF16=0 keeps fp32); the LayerNorm backward upcasts
+        self._dy_dt = act_dtype if os.environ.get("EVO_DXL_BF16", "1") != "0" else torch.float32
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
         # two arenas for the block-pipelined backward (blocks_bwd), alternating by block
@@ -278,7 +282,7 @@ class BlockEngine:
         ops.gemm(xl, dqkvg, dwcat, ta=True)                           # d[Wq|Wk|Wv|Wg] in one GEMM
         ops.PackPlan([dwcat], [self.Gm(f"{prefix}.attn.{f}", C) for f in ("wq", "wk", "wv", "wg")],
                      [C], [HD], True, ops.F32, ops.F32).run()
-        dxl = torch.empty((T, C), dtype=F32, device=d.device)
+        dxl = torch.empty((T, C), dtype=self._dy_dt, device=d.device)
         ops.gemm(dqkvg, self.wcat[prefix], dxl, tb=True)
         del dqkvg, dwcat
         if v.bias:
@@ -329,7 +333,7 @@ class BlockEngine:
             ops.relu_bwd_colsum_(dh, h, self.G(f"{prefix}.b1"))
         del d_act
         ops.gemm(sv["xl"], dh, self.Gm(f"{prefix}.w1", C), ta=True)
-        dxl = torch.empty((T, C), dtype=F32, device=d.device)
+        dxl = torch.empty((T, C), dtype=self._dy_dt, device=d.device)
         ops.gemm(dh, self.W(f"{prefix}.w1", C), dxl, tb=True)
         del dh
         return self._ln_bwd_chain(sv["x"], dxl, sv["mu"], sv["rs"], prefix, d, nxt)
@@ -402,7 +406,7 @@ class BlockEngine:
         ops.gemm(xl, d_ab, dwlr, ta=True)                             # d[w_left | w_right] in one GEMM
         ops.PackPlan([dwlr], [self.Gm(f"{prefix}.w_left", Cm), self.Gm(f"{prefix}.w_right", Cm)],
                      [Cm], [k], True, ops.F32, ops.F32, ns=2).run()
-        dxl = torch.empty((SR, Cm), dtype=F32, device=dev)
+        dxl = torch.empty((SR, Cm), dtype=self._dy_dt, device=dev)
         ops.gemm(d_ab, self.wcat[prefix], dxl, tb=True)
         return dxl
 
