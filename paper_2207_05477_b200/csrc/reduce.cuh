@@ -59,11 +59,18 @@ static __device__ __forceinline__ void finalize_cols(const float* __restrict__ p
                                                      int accumulate, int64_t cblk, float (*sm)[33]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = cblk * 32 + lane;
-  float s = 0.f;
+  // eight independent accumulators (eight loads in flight per lane; the
+  // partial blocks reach thousands of rows), combined in a fixed order
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c < C) {
-#pragma unroll 4
-    for (int g = w; g < G; g += 8) s += partials[(int64_t)g * ld + c];
+    int g = w;
+    for (; g + 56 < G; g += 64) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] += partials[(int64_t)(g + 8 * j) * ld + c];
+    }
+    for (int j = 0; g < G; g += 8, ++j) a[j] += partials[(int64_t)g * ld + c];
   }
+  const float s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   sm[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < C) {

@@ -461,7 +461,7 @@ class BlockEngine:
         ops.colsum_cast(dyb, G(f"{prefix}.b_o"))
         ops.colsum_cast(dgp, G(f"{prefix}.b_g"))
         ops.gemm(sv["ol"], dyb, self.Gm(f"{prefix}.w_o", ch), ta=True)
-        dol = torch.empty((RR, ch), dtype=F32, device=d.device)
+        dol = torch.empty((RR, ch), dtype=self._dy_dt, device=d.device)
         ops.gemm(dyb, self.W(f"{prefix}.w_o", ch), dol, tb=True)
         del dyb
         do = torch.empty((RR, ch), dtype=F32, device=d.device)
