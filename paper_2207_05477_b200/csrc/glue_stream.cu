@@ -198,11 +198,11 @@ __global__ void __launch_bounds__(ST + 32) ln_bwd_stream_kernel(
 // One warp per token (4 channels per lane, C = 128), TPW tokens per warp and
 // stage; z, dz, the LN statistics and (without swap) the H dnb planes of a
 // stage arrive by bulk copy.  Partial row per block: [dw C*H | dgamma C | dbeta C].
-constexpr int PB_CW = 4;  // compute warps per pair-bias block (3 blocks per SM at 132 registers)
+constexpr int PB_CW = 4;  // compute warps per pair-bias block
 
-template <int NST>
+template <int NST, int TPW_ = 4>
 struct PbbStream {
-  static constexpr int C = 128, HM = 8, TPW = 4;
+  static constexpr int C = 128, HM = 8, TPW = TPW_;
   static constexpr int RS = PB_CW * TPW;  // tokens per stage
   static constexpr int ZB = RS * C * 2, DZB = RS * C * 4, SB = RS * 4, NBB = HM * RS * 4;
   static constexpr int STAGE = ((ZB + DZB + 2 * SB + NBB) + 127) / 128 * 128;
@@ -211,13 +211,13 @@ struct PbbStream {
   static constexpr int BYTES = (NST * STAGE > RED ? NST * STAGE : RED) + 2 * NST * 8;
 };
 
-template <int NST>
-__global__ void __launch_bounds__(PB_CW * 32 + 32, 3) pair_bias_bwd_stream_kernel(
+template <int NST, int TPW_, int MINB>
+__global__ void __launch_bounds__(PB_CW * 32 + 32, MINB) pair_bias_bwd_stream_kernel(
     const __nv_bfloat16* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
     const float* __restrict__ dnb, int swap_xy, float* dz, float* __restrict__ partials, int64_t NI,
     int64_t NJ, int H) {
-  using M = PbbStream<NST>;
+  using M = PbbStream<NST, TPW_>;
   constexpr int C = M::C;
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (M::BYTES - 2 * NST * 8));
@@ -532,18 +532,36 @@ bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float*
   const int64_t NT = NI * NJ;
   if (off || C != 128 || H > 8 || dt != EVO_BF16 || (NT % 4) != 0 || NT < 4096) return false;
   if (((uintptr_t)z | (uintptr_t)dz | (uintptr_t)mean | (uintptr_t)rstd | (uintptr_t)dnb) & 15) return false;
+  // tokens per warp and stage x resident blocks per SM; sweep knob
+  // EVO_PBB_CFG = "<tpw><minb>" (tools/time_glue.py: 43 45.9 us, 23 47.3,
+  // 24 55.9 (spills), 82 38.4-39.7, 162 43.3, 161 50.6, 81 46.6 -- more
+  // tokens in flight per warp beat more resident warps)
+  static const int cfg = [] {
+    const char* e = getenv("EVO_PBB_CFG");
+    return e ? atoi(e) : 82;
+  }();
+  auto launch = [&](auto kern, int bytes, int minb) {
+    static bool attr_done[16] = {};
+    const int key = (cfg % 16) & 15;
+    if (!attr_done[key]) {
+      EVO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      attr_done[key] = true;
+    }
+    const int64_t want = minb * (int64_t)num_sms();
+    const unsigned grid = (unsigned)(want < ws_blocks ? want : ws_blocks);
+    kern<<<grid, PB_CW * 32 + 32, bytes, s>>>((const __nv_bfloat16*)z, mean, rstd, g, bln, w, dnb, swap, dz,
+                                               (float*)ws, NI, NJ, (int)H);
+    return grid;
+  };
+  unsigned grid;
   constexpr int NST = 4;
-  using M = PbbStream<NST>;
-  const int64_t want = 3 * (int64_t)num_sms();
-  const unsigned grid = (unsigned)(want < ws_blocks ? want : ws_blocks);
-  auto k = pair_bias_bwd_stream_kernel<NST>;
-  static bool attr = false;
-  if (!attr) {
-    EVO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, M::BYTES));
-    attr = true;
-  }
-  k<<<grid, PB_CW * 32 + 32, M::BYTES, s>>>((const __nv_bfloat16*)z, mean, rstd, g, bln, w, dnb, swap, dz, (float*)ws,
-                                    NI, NJ, (int)H);
+  if (cfg == 24) grid = launch(pair_bias_bwd_stream_kernel<NST, 2, 4>, PbbStream<NST, 2>::BYTES, 4);
+  else if (cfg == 23) grid = launch(pair_bias_bwd_stream_kernel<NST, 2, 3>, PbbStream<NST, 2>::BYTES, 3);
+  else if (cfg == 82) grid = launch(pair_bias_bwd_stream_kernel<NST, 8, 2>, PbbStream<NST, 8>::BYTES, 2);
+  else if (cfg == 162) grid = launch(pair_bias_bwd_stream_kernel<2, 16, 2>, PbbStream<2, 16>::BYTES, 2);
+  else if (cfg == 161) grid = launch(pair_bias_bwd_stream_kernel<3, 16, 1>, PbbStream<3, 16>::BYTES, 1);
+  else if (cfg == 81) grid = launch(pair_bias_bwd_stream_kernel<6, 8, 1>, PbbStream<6, 8>::BYTES, 1);
+  else grid = launch(pair_bias_bwd_stream_kernel<NST, 4, 3>, PbbStream<NST, 4>::BYTES, 3);
   EVO_LAUNCH_CHECK();
   count_launch(1);
   const int64_t W = C * H + 2 * C;
