@@ -537,44 +537,65 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
   // HD8 divides the block size -- checked by the host) summed over its tokens,
   // as the stored bf16 d(gate) values
   float gs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += step) {
-    const int64_t e = base + threadIdx.x;
-    const bool act = e < n;
-    const int64_t t = act ? e / HD8 : 0;
-    const int c8 = act ? (int)(e % HD8) : 0;
-    float dsum = 0.f;
-    if (act) {
-      // dO is pre-scaled by this row's 1/rowsum (the backward kernel then
-      // works with the unnormalised P' = exp2(x - m):  dS = P' (dP' - D'),
-      // dV = P'^T dO' -- one multiply per score fewer; fully-masked rows stay
-      // uniform since P' = 1 there and 1/l = 1/L)
-      const int64_t bq = sl == 1 ? t / sb : t % sl, lq = sl == 1 ? t % sb : t / sl;
-      const float rl = lse[2 * ((bq * H + c8 / G) * L + lq) + 1];
-      const int64_t c = t * (HD8 * 8) + c8 * 8;
-      float dg[8], gv[8], cv[8];
-      bf16x8_to_f(*reinterpret_cast<const uint4*>(dgated + c), dg);
-      bf16x8_to_f(*reinterpret_cast<const uint4*>(gate + c), gv);
-      bf16x8_to_f(*reinterpret_cast<const uint4*>(ctx + c), cv);
-      uint32_t pc[4], pg[4];
+  // two items per thread and iteration, all loads issued before the math
+  // (memory-level parallelism; one item per iteration ran at ~2/3 of HBM)
+  constexpr int PU = 2;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += step * PU) {
+    uint4 rdg[PU], rgv[PU], rcv[PU];
+    float rl[PU];
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        const float d0 = dg[u] * gv[u] * rl, d1 = dg[u + 1] * gv[u + 1] * rl;
-        const float g0 = dg[u] * cv[u] * gv[u] * (1.0f - gv[u]);
-        const float g1 = dg[u + 1] * cv[u + 1] * gv[u + 1] * (1.0f - gv[u + 1]);
-        const __nv_bfloat162 dq = __floats2bfloat162_rn(d0, d1);
-        dsum += __bfloat162float(dq.x) * cv[u] + __bfloat162float(dq.y) * cv[u + 1];
-        pc[u / 2] = *reinterpret_cast<const uint32_t*>(&dq);
-        pg[u / 2] = tc::pack_bf16(g0, g1);
-        const float2 gr = tc::bf16x2_f2(pg[u / 2]);
-        gs[u] += gr.x;
-        gs[u + 1] += gr.y;
+    for (int q = 0; q < PU; ++q) {
+      const int64_t e = base + q * step + threadIdx.x;
+      rl[q] = 0.f;
+      if (e < n) {
+        // dO is pre-scaled by this row's 1/rowsum (the backward kernel then
+        // works with the unnormalised P' = exp2(x - m):  dS = P' (dP' - D'),
+        // dV = P'^T dO' -- one multiply per score fewer; fully-masked rows stay
+        // uniform since P' = 1 there and 1/l = 1/L)
+        const int64_t t = e / HD8;
+        const int c8 = (int)(e % HD8);
+        const int64_t bq = sl == 1 ? t / sb : t % sl, lq = sl == 1 ? t % sb : t / sl;
+        rl[q] = lse[2 * ((bq * H + c8 / G) * L + lq) + 1];
+        const int64_t c = t * (HD8 * 8) + c8 * 8;
+        rdg[q] = *reinterpret_cast<const uint4*>(dgated + c);
+        rgv[q] = *reinterpret_cast<const uint4*>(gate + c);
+        rcv[q] = *reinterpret_cast<const uint4*>(ctx + c);
       }
-      *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
-      *reinterpret_cast<uint4*>(dqkvg + t * ld + 3 * HD8 * 8 + c8 * 8) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
     }
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-    if (act && (c8 % G) == 0) Dvec[t * H + c8 / G] = dsum;
+    for (int q = 0; q < PU; ++q) {
+      const int64_t e = base + q * step + threadIdx.x;
+      const bool act = e < n;
+      const int64_t t = act ? e / HD8 : 0;
+      const int c8 = act ? (int)(e % HD8) : 0;
+      float dsum = 0.f;
+      if (act) {
+        const int64_t c = t * (HD8 * 8) + c8 * 8;
+        float dg[8], gv[8], cv[8];
+        bf16x8_to_f(rdg[q], dg);
+        bf16x8_to_f(rgv[q], gv);
+        bf16x8_to_f(rcv[q], cv);
+        uint32_t pc[4], pg[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const float d0 = dg[u] * gv[u] * rl[q], d1 = dg[u + 1] * gv[u + 1] * rl[q];
+          const float g0 = dg[u] * cv[u] * gv[u] * (1.0f - gv[u]);
+          const float g1 = dg[u + 1] * cv[u + 1] * gv[u + 1] * (1.0f - gv[u + 1]);
+          const __nv_bfloat162 dq = __floats2bfloat162_rn(d0, d1);
+          dsum += __bfloat162float(dq.x) * cv[u] + __bfloat162float(dq.y) * cv[u + 1];
+          pc[u / 2] = *reinterpret_cast<const uint32_t*>(&dq);
+          pg[u / 2] = tc::pack_bf16(g0, g1);
+          const float2 gr = tc::bf16x2_f2(pg[u / 2]);
+          gs[u] += gr.x;
+          gs[u + 1] += gr.y;
+        }
+        *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
+        *reinterpret_cast<uint4*>(dqkvg + t * ld + 3 * HD8 * 8 + c8 * 8) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      if (act && (c8 % G) == 0) Dvec[t * H + c8 / G] = dsum;
+    }
   }
   if (gpart) {
     // block partial of the gate-bias gradient: threads tid, tid + HD8, ...
