@@ -976,8 +976,17 @@ static bool gemm_tc_impl(int64_t M, int64_t N, int64_t K, const void* A, int64_t
   // than 8 pair-halves per split, e.g. 256x256, slower -- tools/splitk_sweep.py)
   const bool pair_split = cg2_split && !opm && !cmask && batch == 1 && (M + BM - 1) / BM >= 2 &&
                           ((M + BM - 1) / BM) * ((N + 255) / 256) >= 8 && !cg2_disabled();
-  if (BN == 256 && batch == 1 && ((M + BM - 1) / BM) * ((N + 255) / 256) < num_sms() && (K + BK - 1) / BK >= 16 &&
-      !pair_split)
+  // (EVO_GEMM_SPLIT_BN=0: 256-wide tiles with >= 2 M-tiles and >= 8 256-wide
+  // tiles -- 256x1024 / 1024x256 dW 24.5 -> 22.7 / 24.6 -> 23.2 us in
+  // isolation, but the bench step measured 101.8 vs 101.6 ms, so off; =256:
+  // always 256-wide)
+  static const int split_bn = [] {
+    const char* e = getenv("EVO_GEMM_SPLIT_BN");
+    return e ? atoi(e) : 128;
+  }();
+  const int64_t mt = (M + BM - 1) / BM, nt256 = (N + 255) / 256;
+  const bool wide_split = split_bn == 256 || (split_bn == 0 && mt >= 2 && mt * nt256 >= 8);
+  if (BN == 256 && batch == 1 && mt * nt256 < num_sms() && (K + BK - 1) / BK >= 16 && !pair_split && !wide_split)
     BN = 128;
   if (const int f = forced_bn(); f && f < BN) BN = f;
   Params p{};
