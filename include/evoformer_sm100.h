@@ -195,6 +195,15 @@ int evo_attn_bwd(const void* qkvg, int64_t ld_qkvg, const float* mask, int64_t m
  * z: [R*R, C] pair tokens.  P[x,y,h] = LN(z[x,y]).w_bias[:,h]; written to
  * nb (storage dtype) as nb[h,x,y] (swap_xy=0: MSA row / triangle start) or
  * nb[h,y,x] (swap_xy=1: triangle end, whose rows are the pair's columns). */
+/* The triangle attentions' input LayerNorm (ln_g, ln_b) and their pair-bias
+ * projection (bias_ln_g, bias_ln_b, w_bias; src/model.py:312-317, 381-398)
+ * read the same pair rows: one pass writes xl (bf16, z's layout), nb (as
+ * evo_pair_bias_fwd_rect) and the shared row statistics.  bf16, c_z = 128,
+ * H <= 8, >= 4096 tokens; EVO_ERR_UNSUPPORTED otherwise (the caller runs the
+ * two ops separately). */
+int evo_ln_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b, const float* bias_ln_g,
+                         const float* bias_ln_b, const float* w_bias, void* xl, void* nb, float* mean, float* rstd,
+                         int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap_xy, void* stream);
 int evo_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b,
                       const float* w_bias, void* nb, float* mean, float* rstd,
                       int64_t R, int64_t C, int64_t H, int swap_xy, void* stream);

@@ -325,6 +325,9 @@ bool pair_bias_fwd_tpt(const void* z, int dt, const float* g, const float* b, co
 bool pair_bias_fwd_mma(const void* z, int dt, const float* g, const float* b, const float* w, void* nb,
                        float* mean, float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap,
                        cudaStream_t s);  // pair_bias_mma.cu
+bool ln_pair_bias_fwd_mma(const void* z, int dt, const float* lg, const float* lb, const float* g, const float* b,
+                          const float* w, void* xl, void* nb, float* mean, float* rstd, int64_t NI, int64_t NJ,
+                          int64_t C, int64_t H, int swap, cudaStream_t s);  // pair_bias_mma.cu
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
@@ -358,6 +361,18 @@ int evo_pair_bias_fwd_rect(const void* z, int dtype, const float* ln_g, const fl
   }));
   EVO_LAUNCH_CHECK();
   count_launch(1);
+  EVO_API_END
+}
+
+int evo_ln_pair_bias_fwd(const void* z, int dtype, const float* ln_g, const float* ln_b, const float* bias_ln_g,
+                         const float* bias_ln_b, const float* w_bias, void* xl, void* nb, float* mean, float* rstd,
+                         int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap_xy, void* stream) {
+  EVO_API_BEGIN
+  EVO_REQUIRE(NI >= 0 && NJ >= 0 && H >= 1, EVO_ERR_ARG, "ln_pair_bias: bad extents");
+  if (NI * NJ == 0) return EVO_OK;
+  EVO_REQUIRE(ln_pair_bias_fwd_mma(z, dtype, ln_g, ln_b, bias_ln_g, bias_ln_b, w_bias, xl, nb, mean, rstd, NI, NJ, C,
+                                   H, swap_xy, (cudaStream_t)stream),
+              EVO_ERR_UNSUPPORTED, "ln_pair_bias: bf16, c_z = 128, H <= 8, >= 4096 tokens only");
   EVO_API_END
 }
 

@@ -33,7 +33,11 @@ namespace {
 constexpr int PBM_C = 128, PBM_TOK = 64, PBM_WARPS = 4;
 constexpr int PBM_HALF = PBM_TOK * 64 * 2;  // one 64-channel box: 8 KB
 constexpr int PBM_TILE = 2 * PBM_HALF;      // 16 KB per stage
-constexpr int PBM_SMEM = 2 * PBM_TILE + 1024 + 256;
+// tiles, then barriers / G, BW / per-warp partials / LN affine (1408 B), plus
+// the 1024-B alignment slack
+constexpr int PBM_SMEM = 2 * PBM_TILE + 1024 + 1536;
+// with the LayerNorm output: two more tiles stage xl for its TMA stores
+constexpr int PBM_SMEM_LN = 4 * PBM_TILE + 1024 + 1536;
 
 __device__ __forceinline__ void pbm_tma_load3(const CUtensorMap* m, uint32_t dst, uint32_t bar, int c0, int c1,
                                               int c2) {
@@ -71,15 +75,30 @@ __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t&
   lo = (uint32_t)__bfloat16_as_ushort(lx) | ((uint32_t)__bfloat16_as_ushort(ly) << 16);
 }
 
+__device__ __forceinline__ void pbm_tma_store3(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(src)
+               : "memory");
+}
+
+// LN = true: also the LayerNorm of the same rows with its own affine
+// (lg, lb) -> xl (bf16, TMA-stored through two swizzled staging tiles): the
+// triangle attentions' input LayerNorm and their pair-bias LayerNorm read the
+// same pair activations, so one pass serves both (src/model.py:381-398).
+template <bool LN>
 __global__ void __launch_bounds__(PBM_WARPS * 32) pair_bias_fwd_mma_kernel(
-    const __grid_constant__ CUtensorMap tmz, const float* __restrict__ g, const float* __restrict__ b,
-    const float* __restrict__ w, __nv_bfloat16* __restrict__ nb, float* __restrict__ mean,
-    float* __restrict__ rstd, int64_t NI, int64_t NJ, int H, int swap, int64_t nstage, int64_t per_line) {
+    const __grid_constant__ CUtensorMap tmz, const __grid_constant__ CUtensorMap tmx, const float* __restrict__ g,
+    const float* __restrict__ b, const float* __restrict__ w, const float* __restrict__ lg,
+    const float* __restrict__ lb, __nv_bfloat16* __restrict__ nb, float* __restrict__ mean, float* __restrict__ rstd,
+    int64_t NI, int64_t NJ, int H, int swap, int64_t nstage, int64_t per_line) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * PBM_TILE);
-  float* sG = reinterpret_cast<float*>(smem + 2 * PBM_TILE + 64);  // [8] G, [8] BW
-  float* spart = sG + 16;                                            // [4 warps][16]
+  constexpr int NT = LN ? 4 : 2;  // z double buffer (+ xl double buffer)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NT * PBM_TILE);
+  float* sG = reinterpret_cast<float*>(smem + NT * PBM_TILE + 64);  // [8] G, [8] BW
+  float* spart = sG + 16;                                             // [4 warps][16]
+  float* sLG = spart + 64;                                            // [128] lg, [128] lb (LN)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
   const uint32_t s_base = tc::smem_u32(smem);
@@ -99,8 +118,13 @@ __global__ void __launch_bounds__(PBM_WARPS * 32) pair_bias_fwd_mma_kernel(
     pbm_tma_load3(&tmz, s_base + buf * PBM_TILE + PBM_HALF, bar, 64, c1, c2);
   };
 
+  if (LN) {
+    sLG[tid] = lg[tid];
+    sLG[PBM_C + tid] = lb[tid];
+  }
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmz)) : "memory");
+    if (LN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmx)) : "memory");
     tc::mbar_init(&full[0], 1);
     tc::mbar_init(&full[1], 1);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -167,36 +191,82 @@ __global__ void __launch_bounds__(PBM_WARPS * 32) pair_bias_fwd_mma_kernel(
     tc::mbar_wait(&full[buf], (uint32_t)((k >> 1) & 1));
     const uint32_t tile = s_base + buf * PBM_TILE;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float2 s0 = make_float2(0.f, 0.f), s1 = s0, q0 = s0, q1 = s0;
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0;
+    uint32_t af[8][4];  // this lane's z values of the stage (kept for the second pass)
 #pragma unroll
     for (int kc = 0; kc < 8; ++kc) {
       const int cb = (2 * kc + lhi) & 7;
       const uint32_t addr = tile + (kc >> 2) * PBM_HALF + row_off + (uint32_t)((cb ^ rsw) << 4);
-      uint32_t a[4];
-      ldsm_x4(addr, a);
-      mma16816(acc, a, bh0[kc], bh1[kc]);
-      mma16816(acc, a, bl0[kc], bl1[kc]);
-      const float2 f0 = bf2f(a[0]), f1 = bf2f(a[1]), f2 = bf2f(a[2]), f3 = bf2f(a[3]);
+      ldsm_x4(addr, af[kc]);
+      mma16816(acc, af[kc], bh0[kc], bh1[kc]);
+      mma16816(acc, af[kc], bl0[kc], bl1[kc]);
+      const float2 f0 = bf2f(af[kc][0]), f1 = bf2f(af[kc][1]), f2 = bf2f(af[kc][2]), f3 = bf2f(af[kc][3]);
       s0 = __fadd2_rn(s0, __fadd2_rn(f0, f2));
       s1 = __fadd2_rn(s1, __fadd2_rn(f1, f3));
-      q0 = __ffma2_rn(f0, f0, __ffma2_rn(f2, f2, q0));
-      q1 = __ffma2_rn(f1, f1, __ffma2_rn(f3, f3, q1));
     }
     // every warp has read this buffer: refill it with the stage two ahead
     __syncthreads();
     if (tid == 0 && st + 2 * (int64_t)gridDim.x < nstage) issue(st + 2 * (int64_t)gridDim.x, buf);
-    float sa = s0.x + s0.y, sb = s1.x + s1.y, qa = q0.x + q0.y, qb = q1.x + q1.y;
+    float sa = s0.x + s0.y, sb = s1.x + s1.y;
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
       sa += __shfl_xor_sync(0xffffffffu, sa, o);
       sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    const float mua = sa / (float)PBM_C, mub = sb / (float)PBM_C;
+    // second pass: sum of squared deviations (the LayerNorm's own two-pass form)
+    float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+    {
+      const float2 ma = make_float2(-mua, -mua), mb = make_float2(-mub, -mub);
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+        const float2 d0 = __fadd2_rn(bf2f(af[kc][0]), ma), d2 = __fadd2_rn(bf2f(af[kc][2]), ma);
+        const float2 d1 = __fadd2_rn(bf2f(af[kc][1]), mb), d3 = __fadd2_rn(bf2f(af[kc][3]), mb);
+        q0 = __ffma2_rn(d0, d0, __ffma2_rn(d2, d2, q0));
+        q1 = __ffma2_rn(d1, d1, __ffma2_rn(d3, d3, q1));
+      }
+    }
+    float qa = q0.x + q0.y, qb = q1.x + q1.y;
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
       qa += __shfl_xor_sync(0xffffffffu, qa, o);
       qb += __shfl_xor_sync(0xffffffffu, qb, o);
     }
-    const float mua = sa / (float)PBM_C, mub = sb / (float)PBM_C;
-    const float inva = rsqrtf(fmaxf(qa / (float)PBM_C - mua * mua, 0.f) + 1e-5f);
-    const float invb = rsqrtf(fmaxf(qb / (float)PBM_C - mub * mub, 0.f) + 1e-5f);
+    const float inva = rsqrtf(qa / (float)PBM_C + 1e-5f);
+    const float invb = rsqrtf(qb / (float)PBM_C + 1e-5f);
     const int64_t line = st / per_line, off = (st % per_line) * PBM_TOK;
+    if constexpr (LN) {
+      // xl = (z - mean) * rstd * lg + lb for this lane's (token, channel pair)
+      // fragments, into the swizzled staging tile of this stage's parity
+      const uint32_t xt = s_base + (2 + buf) * PBM_TILE;
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // tile xt's last store read
+      __syncthreads();
+      const int r0 = warp * 16 + gq;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = r0 + (q & 1) * 8, hi = q >> 1;       // a0: (g, lo) a1: (g+8, lo) a2: (g, hi) a3: (g+8, hi)
+          const int c = 16 * kc + 8 * hi + 2 * tq;
+          const float mu = (q & 1) ? mub : mua, iv = (q & 1) ? invb : inva;
+          const float2 zf = bf2f(af[kc][q]);
+          const float y0 = fmaf((zf.x - mu) * iv, sLG[c], sLG[PBM_C + c]);
+          const float y1 = fmaf((zf.y - mu) * iv, sLG[c + 1], sLG[PBM_C + c + 1]);
+          const int cb = (2 * kc + hi) & 7;
+          const uint32_t a = xt + (kc >> 2) * PBM_HALF + r * 128 + ((cb ^ (r & 7)) << 4) + 4 * tq;
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(tc::pack_bf16(y0, y1)) : "memory");
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        int c1, c2;
+        coords(st, c1, c2);
+        pbm_tma_store3(&tmx, xt, 0, c1, c2);
+        pbm_tma_store3(&tmx, xt + PBM_HALF, 64, c1, c2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
     const int64_t lim = swap ? NI : NJ;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -214,6 +284,7 @@ __global__ void __launch_bounds__(PBM_WARPS * 32) pair_bias_fwd_mma_kernel(
       }
     }
   }
+  if (LN && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 bool pbm_disabled() {
@@ -226,41 +297,73 @@ bool pbm_disabled() {
 
 }  // namespace
 
-bool pair_bias_fwd_mma(const void* z, int dt, const float* g, const float* b, const float* w, void* nb, float* mean,
-                       float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap, cudaStream_t s) {
-  if (pbm_disabled() || dt != EVO_BF16 || C != PBM_C || H > 8 || H < 1 || (((uintptr_t)z) & 15)) return false;
-  if (NI * NJ < 4096 || NI > (1 << 30) || NJ > (1 << 30)) return false;
+static bool pbm_map(CUtensorMap* m, const void* base, int64_t NI, int64_t NJ, int swap) {
   auto enc = tmap_encoder();
-  if (!enc) return false;
-  CUtensorMap m;
-  cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)NJ, (cuuint64_t)NI};
-  cuuint64_t strides[2] = {(cuuint64_t)(C * 2), (cuuint64_t)(NJ * C * 2)};
+  if (!enc || (((uintptr_t)base) & 15)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)PBM_C, (cuuint64_t)NJ, (cuuint64_t)NI};
+  cuuint64_t strides[2] = {(cuuint64_t)(PBM_C * 2), (cuuint64_t)(NJ * PBM_C * 2)};
   cuuint32_t box[3] = {64, swap ? 1u : (cuuint32_t)PBM_TOK, swap ? (cuuint32_t)PBM_TOK : 1u};
   cuuint32_t estr[3] = {1, 1, 1};
-  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(z), dims, strides, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool pbm_launch(const void* z, const float* g, const float* b, const float* w, const float* lg,
+                       const float* lb, void* xl, void* nb, float* mean, float* rstd, int64_t NI, int64_t NJ,
+                       int64_t H, int swap, cudaStream_t s) {
+  CUtensorMap mz, mx;
+  if (!pbm_map(&mz, z, NI, NJ, swap)) return false;
+  if (xl) {
+    if (!pbm_map(&mx, xl, NI, NJ, swap)) return false;
+  } else {
+    mx = mz;
+  }
   const int64_t lines = swap ? NJ : NI, along = swap ? NI : NJ;
   const int64_t per_line = (along + PBM_TOK - 1) / PBM_TOK;
   const int64_t nstage = lines * per_line;
-  static bool attr = false;
-  if (!attr) {
-    EVO_CUDA(cudaFuncSetAttribute(pair_bias_fwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PBM_SMEM));
-    attr = true;
+  static bool attr[2] = {false, false};
+  if (!attr[xl ? 1 : 0]) {
+    if (xl)
+      EVO_CUDA(cudaFuncSetAttribute(pair_bias_fwd_mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    PBM_SMEM_LN));
+    else
+      EVO_CUDA(cudaFuncSetAttribute(pair_bias_fwd_mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    PBM_SMEM));
+    attr[xl ? 1 : 0] = true;
   }
   static const int bps = [] {
     const char* e = getenv("EVO_PB_MMA_BPS");  // resident blocks per SM (sweeps)
     const int v = e ? atoi(e) : 0;
-    return v > 0 && v <= 8 ? v : 4;
+    return v > 0 && v <= 8 ? v : 0;
   }();
-  const int64_t want = (int64_t)num_sms() * bps;
+  const int64_t want = (int64_t)num_sms() * (bps ? bps : (xl ? 3 : 4));
   const unsigned grid = (unsigned)(nstage < want ? nstage : want);
-  pair_bias_fwd_mma_kernel<<<grid, PBM_WARPS * 32, PBM_SMEM, s>>>(m, g, b, w, (__nv_bfloat16*)nb, mean, rstd, NI,
-                                                                  NJ, (int)H, swap, nstage, per_line);
+  if (xl)
+    pair_bias_fwd_mma_kernel<true><<<grid, PBM_WARPS * 32, PBM_SMEM_LN, s>>>(
+        mz, mx, g, b, w, lg, lb, (__nv_bfloat16*)nb, mean, rstd, NI, NJ, (int)H, swap, nstage, per_line);
+  else
+    pair_bias_fwd_mma_kernel<false><<<grid, PBM_WARPS * 32, PBM_SMEM, s>>>(
+        mz, mx, g, b, w, nullptr, nullptr, (__nv_bfloat16*)nb, mean, rstd, NI, NJ, (int)H, swap, nstage, per_line);
   EVO_LAUNCH_CHECK();
   count_launch(1);
   return true;
+}
+
+bool pair_bias_fwd_mma(const void* z, int dt, const float* g, const float* b, const float* w, void* nb, float* mean,
+                       float* rstd, int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap, cudaStream_t s) {
+  if (pbm_disabled() || dt != EVO_BF16 || C != PBM_C || H > 8 || H < 1) return false;
+  if (NI * NJ < 4096 || NI > (1 << 30) || NJ > (1 << 30)) return false;
+  return pbm_launch(z, g, b, w, nullptr, nullptr, nullptr, nb, mean, rstd, NI, NJ, H, swap, s);
+}
+
+// LayerNorm (lg, lb) of the same rows in the same pass (xl: bf16, z's layout)
+bool ln_pair_bias_fwd_mma(const void* z, int dt, const float* lg, const float* lb, const float* g, const float* b,
+                          const float* w, void* xl, void* nb, float* mean, float* rstd, int64_t NI, int64_t NJ,
+                          int64_t C, int64_t H, int swap, cudaStream_t s) {
+  if (pbm_disabled() || dt != EVO_BF16 || C != PBM_C || H > 8 || H < 1 || !xl) return false;
+  if (NI * NJ < 4096 || NI > (1 << 30) || NJ > (1 << 30)) return false;
+  return pbm_launch(z, g, b, w, lg, lb, xl, nb, mean, rstd, NI, NJ, H, swap, s);
 }
 
 }  // namespace evo

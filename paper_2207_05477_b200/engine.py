@@ -108,6 +108,8 @@ class BlockEngine:
         # stores it in bf16 like every other GEMM operand / output of the
         # backward (EVO_DXL_BF16=0 keeps fp32); the LayerNorm backward upcasts
         self._dy_dt = act_dtype if os.environ.get("EVO_DXL_BF16", "1") != "0" else torch.float32
+        # triangle attention: input LayerNorm + pair bias in one pass (EVO_LN_PB=0: two ops)
+        self.ln_pb_fused = act_dtype == torch.bfloat16 and os.environ.get("EVO_LN_PB", "1") != "0"
         # partial rows of the deferred bias / LN-affine reductions of one block backward
         self.arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device=store.device)
         # two arenas for the block-pipelined backward (blocks_bwd), alternating by block
@@ -231,9 +233,22 @@ class BlockEngine:
         H = cfg.heads
         D = C // H
         HD = H * D
-        xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
+        fused = None
+        if v.bias and pair is None and self.ln_pb_fused:
+            # triangle attention: its LayerNorm and its pair-bias LayerNorm read the
+            # same rows -- one pass (csrc/pair_bias_mma.cu), shared statistics
+            fused = ops.ln_pair_bias_fwd(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"),
+                                         self.P(f"{prefix}.bias_ln_g"), self.P(f"{prefix}.bias_ln_b"),
+                                         self.P(f"{prefix}.w_bias"), cfg.n_res, H, v.swap_xy,
+                                         ni=v.ni or None, nj=v.nj or None)
         nb = pmu = prs = None
-        if v.bias:
+        if fused is not None:
+            xl, nb, mu, rs = fused
+            pmu, prs = mu, rs
+            nb = self._gather_bias(nb, v)
+        else:
+            xl, mu, rs = ops.layernorm(x, self.P(f"{prefix}.ln_g"), self.P(f"{prefix}.ln_b"), dt)
+        if v.bias and fused is None:
             z = pair if pair is not None else x
             nb, pmu, prs = ops.pair_bias_fwd(z, self.P(f"{prefix}.bias_ln_g"),
                                              self.P(f"{prefix}.bias_ln_b"),

@@ -348,6 +348,27 @@ def pair_bias_fwd(z, g, b, w, R, H, swap_xy, ni=None, nj=None):
     return nb, mean, rstd
 
 
+def ln_pair_bias_fwd(z, lg, lb, g, b, w, R, H, swap_xy, ni=None, nj=None):
+    """One pass over the pair rows z for the triangle attentions: their input
+    LayerNorm (lg, lb) -> xl (bf16) and the pair bias nb as pair_bias_fwd, with
+    the shared row statistics.  Returns (xl, nb, mean, rstd), or None when the
+    fused kernel does not cover the shape (bf16, c_z = 128, H <= 8, >= 4096
+    rows) -- the caller then runs layernorm + pair_bias_fwd."""
+    C = z.shape[1]
+    ni = R if ni is None else ni
+    nj = R if nj is None else nj
+    if z.dtype != torch.bfloat16 or C != 128 or H > 8 or ni * nj < 4096 or not z.is_contiguous():
+        return None
+    dev = z.device
+    xl = torch.empty_like(z)
+    nb = torch.empty((H, nj, ni) if swap_xy else (H, ni, nj), dtype=z.dtype, device=dev)
+    mean = torch.empty(ni * nj, dtype=torch.float32, device=dev)
+    rstd = torch.empty(ni * nj, dtype=torch.float32, device=dev)
+    call("evo_ln_pair_bias_fwd", ptr(z), dcode(z), ptr(lg), ptr(lb), ptr(g), ptr(b), ptr(w), ptr(xl), ptr(nb),
+         ptr(mean), ptr(rstd), ni, nj, C, H, int(swap_xy), stream())
+    return xl, nb, mean, rstd
+
+
 def pair_bias_bwd(z, mean, rstd, g, b, w, dnb, swap_xy, dz, dg, db, dw, R, H,
                   accumulate=False, ni=None, nj=None):
     C = z.shape[1]

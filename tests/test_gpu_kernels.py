@@ -503,3 +503,34 @@ def test_opm_rec_once_per_pass_matches_inline():
     assert torch.equal(rec0, rec) and torch.equal(out0, out1)
     rec_s = ops.opm_rec(mask, S, R, i0=16, ni=32)
     assert torch.equal(rec_s, rec.view(R, R)[16:48].reshape(-1))
+
+
+@pytest.mark.parametrize("NI,NJ,swap", [(256, 256, 0), (256, 256, 1), (128, 256, 0), (256, 128, 1),
+                                        (100, 82, 0), (82, 100, 1)])
+def test_ln_pair_bias_fused_vs_torch(NI, NJ, swap):
+    """Triangle attention's input LayerNorm and its pair bias in one pass
+    (csrc/pair_bias_mma.cu, LN = true) against fp32 torch: xl and nb within
+    bf16 rounding, the shared row statistics to fp32 accuracy; the unfused
+    ops agree with it."""
+    from paper_2207_05477_b200 import ops
+    C, H = 128, 8
+    torch.manual_seed(NI * 3 + NJ + swap)
+    z = (torch.randn(NI * NJ, C, device="cuda") * 1.5 + 0.3).bfloat16()
+    lg, lb = torch.randn(C, device="cuda"), torch.randn(C, device="cuda") * 0.1
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda") * 0.1
+    w = torch.randn(C, H, device="cuda") * 0.2
+    out = ops.ln_pair_bias_fwd(z, lg, lb, g, b, w, 0, H, swap, ni=NI, nj=NJ)
+    assert out is not None
+    xl, nb, mu, rs = out
+    zf = z.float()
+    assert rel(xl.float(), torch.nn.functional.layer_norm(zf, (C,), lg, lb, 1e-5)) <= 1e-2
+    P = torch.nn.functional.layer_norm(zf, (C,), g, b, 1e-5) @ w
+    ref = P.view(NI, NJ, H).permute(2, 0, 1)
+    if swap:
+        ref = ref.transpose(1, 2)
+    assert rel(nb.float(), ref) <= 1e-2
+    assert rel(mu, zf.mean(1)) <= 1e-5
+    assert rel(rs, torch.rsqrt(zf.var(1, unbiased=False) + 1e-5)) <= 1e-5
+    nb2, mu2, rs2 = ops.pair_bias_fwd(z, g, b, w, 0, H, swap, ni=NI, nj=NJ)
+    xl2, _, _ = ops.layernorm(z, lg, lb, torch.bfloat16)
+    assert rel(nb.float(), nb2.float()) <= 1e-2 and rel(xl.float(), xl2.float()) <= 1e-2
