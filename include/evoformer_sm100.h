@@ -221,6 +221,15 @@ int evo_pair_bias_bwd(const void* z, int dtype, const float* mean, const float* 
 int evo_pair_bias_fwd_rect(const void* z, int dtype, const float* ln_g, const float* ln_b,
                            const float* w_bias, void* nb, float* mean, float* rstd,
                            int64_t NI, int64_t NJ, int64_t C, int64_t H, int swap_xy, void* stream);
+/* evo_pair_bias_bwd_rect that also emits the updated dz as bf16 (dz16, may be
+ * NULL) and its column sums (dzsum[C], written; may be NULL) in the same pass:
+ * the next module's GEMM operand and output-bias gradient when this bias
+ * gradient is the last write to dz.  bf16 z, c_z = 128, H <= 8, >= 4096
+ * tokens (a multiple of 4); EVO_ERR_UNSUPPORTED (nothing written) otherwise. */
+int evo_pair_bias_bwd_ex(const void* z, int dtype, const float* mean, const float* rstd, const float* ln_g,
+                         const float* ln_b, const float* w_bias, const float* dnb, int swap_xy, float* dz,
+                         float* dln_g, float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t NI, int64_t NJ,
+                         int64_t C, int64_t H, void* dz16, float* dzsum, void* stream);
 int evo_pair_bias_bwd_rect(const void* z, int dtype, const float* mean, const float* rstd,
                            const float* ln_g, const float* ln_b, const float* w_bias, const float* dnb,
                            int swap_xy, float* dz, float* dln_g, float* dln_b,

@@ -70,6 +70,8 @@ SIGNATURES = {
     "evo_ln_pair_bias_fwd": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _p]),
     "evo_pair_bias_bwd_rect": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _i, _p,
                                     _i64, _i64, _i64, _i64, _p]),
+    "evo_pair_bias_bwd_ex": (_i, [_p, _i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _i, _p,
+                                  _i64, _i64, _i64, _i64, _p, _p, _p]),
     "evo_opm_norm_fwd_rows": (_i, [_p, _i, _p, _p, _p, _i, _i64, _i64, _i64, _i64, _i64, _p]),
     "evo_opm_norm_bwd_rows": (_i, [_p, _i, _p, _p, _i, _i64, _i64, _i64, _p]),
     "evo_swap01": (_i, [_p, _p, _i64, _i64, _i64, _p]),

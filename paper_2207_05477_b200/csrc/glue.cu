@@ -896,21 +896,25 @@ bool pair_bias_fwd_vec(const void* z, int dt, const float* g, const float* b, co
 bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                           const float* bln, const float* w, const float* dnb, int swap, float* dz, float* dg,
                           float* db, float* dw, int accumulate, void* ws, int64_t NI, int64_t NJ, int64_t C,
-                          int64_t H, int64_t ws_blocks, cudaStream_t s);
+                          int64_t H, int64_t ws_blocks, cudaStream_t s, __nv_bfloat16* dz16, float* dzsum);
 
 int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H) {
-  return (int64_t)num_sms() * PB_PARTIAL_PER_SM * (C * H + 2 * C) * 4;
+  return (int64_t)num_sms() * PB_PARTIAL_PER_SM * (C * H + 3 * C) * 4;
 }
 
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
                        float* dg, float* db, float* dw, int accumulate, void* ws, int64_t NI,
-                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s) {
+                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s, __nv_bfloat16* dz16, float* dzsum,
+                       bool* fused_out) {
+  if (fused_out) *fused_out = false;
   if (!pow2_width(C) || C > 256 || H > 8 || !al16(z) || !al16(dz)) return false;
   ws = partial_buffer(ws, pair_bias_bwd_vec_ws(C, H));
   if (pair_bias_bwd_stream(z, dt, mean, rstd, g, bln, w, dnb, swap, dz, dg, db, dw, accumulate, ws, NI, NJ, C, H,
-                           (int64_t)num_sms() * PB_PARTIAL_PER_SM, s))
+                           (int64_t)num_sms() * PB_PARTIAL_PER_SM, s, dz16, dzsum)) {
+    if (fused_out) *fused_out = true;
     return true;
+  }
   unsigned grid = 0;
   POW2_C_DISPATCH(C, CC, {
     if constexpr (CC <= 256) {

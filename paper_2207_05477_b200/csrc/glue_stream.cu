@@ -206,7 +206,7 @@ struct PbbStream {
   static constexpr int RS = PB_CW * TPW;  // tokens per stage
   static constexpr int ZB = RS * C * 2, DZB = RS * C * 4, SB = RS * 4, NBB = HM * RS * 4;
   static constexpr int STAGE = ((ZB + DZB + 2 * SB + NBB) + 127) / 128 * 128;
-  static constexpr int W = C * HM + 2 * C;
+  static constexpr int W = C * HM + 3 * C;  // [dw | dgamma | dbeta | colsum(dz) (optional)]
   static constexpr int RED = PB_CW * W * 4;
   static constexpr int BYTES = (NST * STAGE > RED ? NST * STAGE : RED) + 2 * NST * 8;
 };
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, MINB) pair_bias_bwd_stream_ke
     const __nv_bfloat16* __restrict__ z, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ g, const float* __restrict__ bln, const float* __restrict__ w,
     const float* __restrict__ dnb, int swap_xy, float* dz, float* __restrict__ partials, int64_t NI,
-    int64_t NJ, int H) {
+    int64_t NJ, int H, __nv_bfloat16* __restrict__ dz16, int want_dzsum) {
   using M = PbbStream<NST, TPW_>;
   constexpr int C = M::C;
   extern __shared__ __align__(128) uint8_t sm[];
@@ -279,6 +279,8 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, MINB) pair_bias_bwd_stream_ke
   for (int e = 0; e < 4; ++e)
 #pragma unroll
     for (int q = 0; q < M::HM / 2; ++q) dw2[e][q] = make_float2(0.f, 0.f);
+  // column sums of the updated dz (the next module's output-bias gradient)
+  float2 dzs2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   for (int it = 0; it < n; ++it) {
     const int s = it % NST;
     const int64_t t0 = (s0 + it) * M::RS;
@@ -344,6 +346,13 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, MINB) pair_bias_bwd_stream_ke
       const float2 o0 = __ffma2_rn(inv2, __ffma2_rn(xh2[0], nm2, __fadd2_rn(dxh2[0], nm1)), make_float2(dzr.x, dzr.y));
       const float2 o1 = __ffma2_rn(inv2, __ffma2_rn(xh2[1], nm2, __fadd2_rn(dxh2[1], nm1)), make_float2(dzr.z, dzr.w));
       *reinterpret_cast<float4*>(dz + (t0 + tt) * C + c0) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      if (dz16)  // the next module's bf16 operand
+        *reinterpret_cast<uint2*>(dz16 + (t0 + tt) * C + c0) =
+            make_uint2(tc::pack_bf16(o0.x, o0.y), tc::pack_bf16(o1.x, o1.y));
+      if (want_dzsum) {
+        dzs2[0] = __fadd2_rn(dzs2[0], o0);
+        dzs2[1] = __fadd2_rn(dzs2[1], o1);
+      }
       }
     }
     tc::mbar_arrive_warp(&emp[s]);
@@ -358,9 +367,10 @@ __global__ void __launch_bounds__(PB_CW * 32 + 32, MINB) pair_bias_bwd_stream_ke
       if (hh < H) mine[(c0 + e) * H + hh] = (hh & 1) ? dw2[e][hh / 2].y : dw2[e][hh / 2].x;
     mine[C * H + c0 + e] = (e & 1) ? dgs2[e / 2].y : dgs2[e / 2].x;
     mine[C * H + C + c0 + e] = (e & 1) ? dbs2[e / 2].y : dbs2[e / 2].x;
+    mine[C * H + 2 * C + c0 + e] = (e & 1) ? dzs2[e / 2].y : dzs2[e / 2].x;
   }
   asm volatile("bar.sync 1, %0;" ::"r"(PB_CW * 32) : "memory");
-  const int Wd = C * H + 2 * C;
+  const int Wd = C * H + (want_dzsum ? 3 : 2) * C;
   for (int c = tid; c < Wd; c += PB_CW * 32) {
     float acc = 0.f;
     for (int q = 0; q < PB_CW; ++q) acc += red[q * M::W + c];
@@ -521,17 +531,23 @@ bool ln_bwd_stream(const void* x, int xdt, const void* dy, int dydt, const float
 
 namespace evo {
 
-bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float* rstd, const float* g,
-                          const float* bln, const float* w, const float* dnb, int swap, float* dz, float* dg,
-                          float* db, float* dw, int accumulate, void* ws, int64_t NI, int64_t NJ, int64_t C,
-                          int64_t H, int64_t ws_blocks, cudaStream_t s) {
+bool pair_bias_bwd_stream_ok(const void* z, int dt, const void* dz, const void* dz16, const float* mean,
+                             const float* rstd, const float* dnb, int64_t NI, int64_t NJ, int64_t C, int64_t H) {
   static const bool off = [] {
     const char* e = getenv("EVO_GLUE_STREAM");
     return e && e[0] == '0';
   }();
   const int64_t NT = NI * NJ;
   if (off || C != 128 || H > 8 || dt != EVO_BF16 || (NT % 4) != 0 || NT < 4096) return false;
-  if (((uintptr_t)z | (uintptr_t)dz | (uintptr_t)mean | (uintptr_t)rstd | (uintptr_t)dnb) & 15) return false;
+  return ((((uintptr_t)z | (uintptr_t)dz | (uintptr_t)mean | (uintptr_t)rstd | (uintptr_t)dnb) & 15) == 0 &&
+          (((uintptr_t)dz16) & 7) == 0);
+}
+
+bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float* rstd, const float* g,
+                          const float* bln, const float* w, const float* dnb, int swap, float* dz, float* dg,
+                          float* db, float* dw, int accumulate, void* ws, int64_t NI, int64_t NJ, int64_t C,
+                          int64_t H, int64_t ws_blocks, cudaStream_t s, __nv_bfloat16* dz16, float* dzsum) {
+  if (!pair_bias_bwd_stream_ok(z, dt, dz, dz16, mean, rstd, dnb, NI, NJ, C, H)) return false;
   // tokens per warp and stage x resident blocks per SM; sweep knob
   // EVO_PBB_CFG = "<tpw><minb>" (tools/time_glue.py: 43 45.9 us, 23 47.3,
   // 24 55.9 (spills), 82 38.4-39.7, 162 43.3, 161 50.6, 81 46.6 -- more
@@ -550,7 +566,7 @@ bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float*
     const int64_t want = minb * (int64_t)num_sms();
     const unsigned grid = (unsigned)(want < ws_blocks ? want : ws_blocks);
     kern<<<grid, PB_CW * 32 + 32, bytes, s>>>((const __nv_bfloat16*)z, mean, rstd, g, bln, w, dnb, swap, dz,
-                                               (float*)ws, NI, NJ, (int)H);
+                                               (float*)ws, NI, NJ, (int)H, dz16, dzsum != nullptr);
     return grid;
   };
   unsigned grid;
@@ -564,10 +580,11 @@ bool pair_bias_bwd_stream(const void* z, int dt, const float* mean, const float*
   else grid = launch(pair_bias_bwd_stream_kernel<NST, 4, 3>, PbbStream<NST, 4>::BYTES, 3);
   EVO_LAUNCH_CHECK();
   count_launch(1);
-  const int64_t W = C * H + 2 * C;
+  const int64_t W = C * H + (dzsum ? 3 : 2) * C;
   finalize_partials((const float*)ws, grid, C * H, dw, accumulate, s, W);
   finalize_partials((const float*)ws + C * H, grid, C, dg, accumulate, s, W);
   finalize_partials((const float*)ws + C * H + C, grid, C, db, accumulate, s, W);
+  if (dzsum) finalize_partials((const float*)ws + C * H + 2 * C, grid, C, dzsum, 0, s, W);
   return true;
 }
 

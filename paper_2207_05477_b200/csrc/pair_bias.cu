@@ -332,7 +332,8 @@ int64_t pair_bias_bwd_vec_ws(int64_t C, int64_t H);
 bool pair_bias_bwd_vec(const void* z, int dt, const float* mean, const float* rstd, const float* g,
                        const float* bln, const float* w, const float* dnb, int swap, float* dz,
                        float* dg, float* db, float* dw, int accumulate, void* ws, int64_t NI,
-                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s);
+                       int64_t NJ, int64_t C, int64_t H, cudaStream_t s, __nv_bfloat16* dz16, float* dzsum,
+                       bool* fused_out);
 
 }  // namespace evo
 
@@ -399,7 +400,7 @@ int evo_pair_bias_bwd_rect(const void* z, int dtype, const float* mean, const fl
   if (NI * NJ == 0) return EVO_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (pair_bias_bwd_vec(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b,
-                        dw_bias, accumulate, ws, NI, NJ, C, H, s))
+                        dw_bias, accumulate, ws, NI, NJ, C, H, s, nullptr, nullptr, nullptr))
     return EVO_OK;
   const int64_t want = (NI * NJ + PB_WARPS - 1) / PB_WARPS;
   unsigned grid = (unsigned)(want < EVO_PARTIAL_BLOCKS ? want : EVO_PARTIAL_BLOCKS);
@@ -418,6 +419,37 @@ int evo_pair_bias_bwd_rect(const void* z, int dtype, const float* mean, const fl
   finalize_partials(part, grid, C * H, dw_bias, accumulate, s, W);
   finalize_partials(part + C * H, grid, C, dln_g, accumulate, s, W);
   finalize_partials(part + C * H + C, grid, C, dln_b, accumulate, s, W);
+  EVO_API_END
+}
+
+}  // extern "C"
+namespace evo {
+bool pair_bias_bwd_stream_ok(const void* z, int dt, const void* dz, const void* dz16, const float* mean,
+                             const float* rstd, const float* dnb, int64_t NI, int64_t NJ, int64_t C,
+                             int64_t H);  // glue_stream.cu
+}
+extern "C" {
+
+int evo_pair_bias_bwd_ex(const void* z, int dtype, const float* mean, const float* rstd, const float* ln_g,
+                         const float* ln_b, const float* w_bias, const float* dnb, int swap_xy, float* dz,
+                         float* dln_g, float* dln_b, float* dw_bias, int accumulate, void* ws, int64_t NI, int64_t NJ,
+                         int64_t C, int64_t H, void* dz16, float* dzsum, void* stream) {
+  if (!dz16 && !dzsum)
+    return evo_pair_bias_bwd_rect(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b, dw_bias,
+                                  accumulate, ws, NI, NJ, C, H, stream);
+  EVO_API_BEGIN
+  EVO_REQUIRE(H >= 1 && H <= 8 && ws != nullptr && NI > 0 && NJ > 0, EVO_ERR_ARG, "pair_bias_bwd_ex: bad arguments");
+  // decided before any work, so an unsupported call leaves dz untouched
+  EVO_REQUIRE(pair_bias_bwd_stream_ok(z, dtype, dz, dz16, mean, rstd, dnb, NI, NJ, C, H), EVO_ERR_UNSUPPORTED,
+              "pair_bias_bwd_ex: the fused bf16 copy / column sums need the streamed path "
+              "(bf16, c_z = 128, H <= 8, >= 4096 tokens, a multiple of 4)");
+  bool fused = false;
+  EVO_REQUIRE(pair_bias_bwd_vec(z, dtype, mean, rstd, ln_g, ln_b, w_bias, dnb, swap_xy, dz, dln_g, dln_b, dw_bias,
+                                accumulate, ws, NI, NJ, C, H, (cudaStream_t)stream, (__nv_bfloat16*)dz16, dzsum,
+                                &fused) &&
+                  fused,
+              EVO_ERR_UNSUPPORTED, "pair_bias_bwd_ex: the fused bf16 copy / column sums need the streamed path "
+                                   "(bf16, c_z = 128, H <= 8, >= 4096 tokens, a multiple of 4)");
   EVO_API_END
 }
 

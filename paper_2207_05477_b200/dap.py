@@ -123,10 +123,10 @@ class DapEngine(BlockEngine):
         msa, s3 = self.trans_fwd(msa, f"{p}.msa_trans")
         return msa, (s1, s2, s3)
 
-    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats, late=None):
+    def msa_branch_bwd(self, i, d_msa, d_pair_acc, saved, feats, late=None, d_act=None):
         p = f"block{i}"
         s1, s2, s3 = saved
-        self.trans_bwd(d_msa, s3, f"{p}.msa_trans")
+        self.trans_bwd(d_msa, s3, f"{p}.msa_trans", d_act=d_act)
         dt_ = self._to_cols(d_msa, self.s_loc, "msa_col_attn")
         self.attn_bwd(dt_, s2, f"{p}.col_attn", self.var["col_attn"], feats)
         self._to_rows(dt_, self.s_loc, "msa_col_attn", out=d_msa)
@@ -143,10 +143,10 @@ class DapEngine(BlockEngine):
         pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
         return pair, ([], s1, s2, s3)
 
-    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False):
+    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False, d_act=None):
         p = f"block{i}"
         _, s1, s2, s3 = saved
-        self.trans_bwd(d_pair, s3, f"{p}.pair_trans")
+        self.trans_bwd(d_pair, s3, f"{p}.pair_trans", d_act=d_act)
         dt_ = self._to_cols(d_pair, self.r_loc, "tri_end")
         self.attn_bwd(dt_, s2, f"{p}.tri_end", self.var["tri_end"], feats)
         self._to_rows(dt_, self.r_loc, "tri_end", out=d_pair)

@@ -303,12 +303,14 @@ class BlockEngine:
         if v.bias:
             target = dpair if dpair is not None else d
 
-            def pair_bias_bwd():
+            def pair_bias_bwd(dz16=None, dzsum=None):
+                # dz16 / dzsum: when the caller knows this is the last write to the
+                # pair gradient, the next module's bf16 operand and b2 gradient
                 ops.pair_bias_bwd(sv["pair"], sv["pmu"], sv["prs"], self.P(f"{prefix}.bias_ln_g"),
                                   self.P(f"{prefix}.bias_ln_b"), self.P(f"{prefix}.w_bias"), dnb,
                                   v.swap_xy, target, self.G(f"{prefix}.bias_ln_g"),
                                   self.G(f"{prefix}.bias_ln_b"), self.G(f"{prefix}.w_bias"),
-                                  cfg.n_res, H, ni=v.ni or None, nj=v.nj or None)
+                                  cfg.n_res, H, ni=v.ni or None, nj=v.nj or None, dz16=dz16, dzsum=dzsum)
             if dpair is not None and late is not None:
                 late.append(pair_bias_bwd)  # into the pair gradient: run by the caller after its join
             else:
@@ -550,14 +552,15 @@ class BlockEngine:
         pair, s3 = self.trans_fwd(pair, f"{p}.pair_trans")
         return pair, (tm, s1, s2, s3)
 
-    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False):
+    def pair_branch_bwd(self, i, d_pair, saved, feats, opm_nxt=False, d_act=None):
         """d(pair_out) -> d(pair_mid) in place.  With ``opm_nxt`` (the caller
         runs this block's OPM backward on the same d(pair_mid)) the last
         LayerNorm backward also emits the OPM's bf16 operand and its b_out
-        gradient, returned for ``opm_bwd_core(d_act=...)``; else None."""
+        gradient, returned for ``opm_bwd_core(d_act=...)``; else None.
+        ``d_act``: bf16 d_pair with the pair transition's b2 gradient taken."""
         p = f"block{i}"
         tm, s1, s2, s3 = saved
-        a = self.trans_bwd(d_pair, s3, f"{p}.pair_trans", nxt=self.G(f"{p}.tri_end.attn.bo"))
+        a = self.trans_bwd(d_pair, s3, f"{p}.pair_trans", nxt=self.G(f"{p}.tri_end.attn.bo"), d_act=d_act)
         a = self.attn_bwd(d_pair, s2, f"{p}.tri_end", self.var["tri_end"], feats, d_act=a,
                           nxt=self.G(f"{p}.tri_start.attn.bo"))
         nxt = self.G(f"{p}.opm.b_out") if opm_nxt and not tm else None
@@ -820,6 +823,7 @@ class BlockEngine:
         keep = []  # main-stream tensors read by the side stream: alive until the final join
         side.wait_stream(main)
         msa_act = None  # block i-1's MSA transition operand, emitted by block i's OPM LN backward
+        pair_act = None  # block i-1's pair transition operand, emitted by block i's row-attention pair bias
         for i in reversed(range(n)):
             if inputs is not None:
                 saved[i] = self.block_refwd(i, *inputs[i], feats)
@@ -831,15 +835,22 @@ class BlockEngine:
                 msa_act = None
                 ev_msa = torch.cuda.Event()
                 ev_msa.record(side)
-            d_act = self.pair_branch_bwd(i, d_pair, sp, feats, opm_nxt=True)  # d_pair = d(pair_mid)
+            d_act = self.pair_branch_bwd(i, d_pair, sp, feats, opm_nxt=True, d_act=pair_act)  # d(pair_mid)
+            pair_act = None
             if d_act is None:
                 d_act = torch.empty(d_pair.shape, dtype=self.dt, device=d_pair.device)
                 ops.colsum_cast(d_pair, self.G(f"block{i}.opm.b_out"), y=d_act)
             ev_pair = torch.cuda.Event()
             ev_pair.record(main)
             main.wait_event(ev_msa)
-            for fn in late:                                     # d_pair += bias path
-                fn()
+            for k, fn in enumerate(late):                       # d_pair += bias path
+                if k == len(late) - 1 and i > 0 and self.dt == torch.bfloat16:
+                    # the last write to d(pair_in): it also emits block i-1's pair
+                    # transition operand and b2 gradient
+                    pair_act = torch.empty(d_pair.shape, dtype=self.dt, device=d_pair.device)
+                    fn(dz16=pair_act, dzsum=self.G(f"block{i - 1}.pair_trans.b2"))
+                else:
+                    fn()
             with torch.cuda.stream(side):
                 side.wait_event(ev_pair)
                 dxl = self.opm_bwd_core(None, so, f"block{i}.opm", feats, d_act=d_act)

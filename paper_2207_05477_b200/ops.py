@@ -370,14 +370,25 @@ def ln_pair_bias_fwd(z, lg, lb, g, b, w, R, H, swap_xy, ni=None, nj=None):
 
 
 def pair_bias_bwd(z, mean, rstd, g, b, w, dnb, swap_xy, dz, dg, db, dw, R, H,
-                  accumulate=False, ni=None, nj=None):
+                  accumulate=False, ni=None, nj=None, dz16=None, dzsum=None):
+    """With ``dz16`` / ``dzsum`` the pass also emits the updated dz as bf16
+    and its column sums (the next module's operand and output-bias gradient);
+    shapes the fused path does not cover get a separate colsum/cast pass."""
     C = z.shape[1]
     ni = R if ni is None else ni
     nj = R if nj is None else nj
     ws = _ws(_lib.load().evo_pair_bias_bwd_workspace(C, H), z.device)
+    fused_ok = (z.dtype == torch.bfloat16 and C == 128 and H <= 8 and (ni * nj) % 4 == 0 and ni * nj >= 4096)
+    if (dz16 is not None or dzsum is not None) and fused_ok:
+        call("evo_pair_bias_bwd_ex", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
+             ptr(dnb), int(swap_xy), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
+             ptr(ws), ni, nj, C, H, ptr(dz16), ptr(dzsum), stream())
+        return
     call("evo_pair_bias_bwd_rect", ptr(z), dcode(z), ptr(mean), ptr(rstd), ptr(g), ptr(b), ptr(w),
          ptr(dnb), int(swap_xy), ptr(dz), ptr(dg), ptr(db), ptr(dw), int(accumulate),
          ptr(ws), ni, nj, C, H, stream())
+    if dz16 is not None or dzsum is not None:
+        colsum_cast(dz, dzsum, y=dz16)
 
 
 # ---------------------------------------------------------------------------

@@ -534,3 +534,31 @@ def test_ln_pair_bias_fused_vs_torch(NI, NJ, swap):
     nb2, mu2, rs2 = ops.pair_bias_fwd(z, g, b, w, 0, H, swap, ni=NI, nj=NJ)
     xl2, _, _ = ops.layernorm(z, lg, lb, torch.bfloat16)
     assert rel(nb.float(), nb2.float()) <= 1e-2 and rel(xl.float(), xl2.float()) <= 1e-2
+
+
+@pytest.mark.parametrize("swap", [0, 1])
+def test_pair_bias_bwd_emits_next_operand(swap):
+    """pair_bias_bwd with dz16 / dzsum (the last write to the pair gradient):
+    the same dz, dgamma, dbeta, dw as without, plus bf16(dz) and its column
+    sums in the same pass (csrc/glue_stream.cu)."""
+    from paper_2207_05477_b200 import ops
+    R, C, H = 256, 128, 8
+    torch.manual_seed(17 + swap)
+    z = torch.randn(R * R, C, device="cuda").bfloat16()
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda") * 0.1
+    w = torch.randn(C, H, device="cuda") * 0.2
+    _, mu, rs = ops.pair_bias_fwd(z, g, b, w, R, H, swap)
+    dnb = torch.randn(H, R, R, device="cuda")
+    dz0 = torch.randn(R * R, C, device="cuda")
+    outs = []
+    for fused in (False, True):
+        dz = dz0.clone()
+        dg, db, dw = torch.empty(C, device="cuda"), torch.empty(C, device="cuda"), torch.empty(C, H, device="cuda")
+        d16 = torch.empty(R * R, C, device="cuda", dtype=torch.bfloat16) if fused else None
+        dsum = torch.full((C,), 3.0, device="cuda") if fused else None
+        ops.pair_bias_bwd(z, mu, rs, g, b, w, dnb, swap, dz, dg, db, dw, R, H, dz16=d16, dzsum=dsum)
+        outs.append((dz, dg, db, dw, d16, dsum))
+    (dz, dg, db, dw, _, _), (dzf, dgf, dbf, dwf, d16, dsum) = outs
+    assert torch.equal(dz, dzf) and torch.equal(dg, dgf) and torch.equal(db, dbf) and torch.equal(dw, dwf)
+    assert torch.equal(d16, dzf.bfloat16())
+    assert rel(dsum, dzf.double().sum(0).float()) <= 1e-5
