@@ -601,7 +601,14 @@ bool ln_fwd_stream(const void* x, int xdt, const float* g, const float* b, void*
   if (off || (C != 128 && C != 256) || xdt != EVO_BF16 || rows < 4096) return false;
   if (((uintptr_t)x | (uintptr_t)y) & 15) return false;
   constexpr int NST = 4;
-  const unsigned grid = (unsigned)(2 * num_sms());
+  // resident blocks per SM (EVO_LNF_BPS sweep, tools/time_glue.py: 1 -> 7.7 us,
+  // 2 -> 7.1 us, 3 -> 9.1 us at the pair shape)
+  static const int bps = [] {
+    const char* e = getenv("EVO_LNF_BPS");
+    const int v = e ? atoi(e) : 0;
+    return v >= 1 && v <= 3 ? v : 2;
+  }();
+  const unsigned grid = (unsigned)(bps * num_sms());
   bool done = false;
   auto go = [&](auto cc, auto ty) {
     constexpr int CC = decltype(cc)::value;
