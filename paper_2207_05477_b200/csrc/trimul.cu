@@ -9,6 +9,7 @@
 //   transpose  [rows, cols] <-> [cols, rows] (smem tiled, coalesced both ways)
 //   gated residual  out = z + sigmoid(gp + bg) * (y + by) and its backward
 #include "common.cuh"
+#include "tc_common.cuh"
 #include "reduce.cuh"
 #include "vec.cuh"
 
@@ -99,6 +100,52 @@ __global__ void __launch_bounds__(256) transpose_kernel(const TI* __restrict__ x
   __syncthreads();
   for (int r = ty; r < TT; r += 8)
     if (c0 + r < cols && r0 + tx < rows) y[(c0 + r) * rows + r0 + tx] = from_f<TO>(t[tx][r]);
+}
+
+// 64 x 64 tiles, 16-byte accesses on both sides: each thread loads two 8-wide
+// row chunks, the tile goes through shared memory (fp32, padded), and each
+// thread stores two 8-wide chunks of the transposed tile
+template <typename TI>
+__device__ __forceinline__ void ld8f(const TI* p, float (&f)[8]);
+template <>
+__device__ __forceinline__ void ld8f<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 t = tc::bf16x2_f2(w[k]);
+    f[2 * k] = t.x;
+    f[2 * k + 1] = t.y;
+  }
+}
+template <>
+__device__ __forceinline__ void ld8f<float>(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+
+template <typename TI>
+__global__ void __launch_bounds__(256) transpose_vec_kernel(const TI* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                            int64_t rows, int64_t cols) {
+  __shared__ float t[64][65];
+  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = threadIdx.x + q * 256, r = idx >> 3, c8 = (idx & 7) * 8;
+    float f[8];
+    ld8f<TI>(x + (r0 + r) * cols + c0 + c8, f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) t[r][c8 + e] = f[e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = threadIdx.x + q * 256, oc = idx >> 3, r8 = (idx & 7) * 8;  // output row = input column
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = tc::pack_bf16(t[r8 + 2 * k][oc], t[r8 + 2 * k + 1][oc]);
+    *reinterpret_cast<uint4*>(y + (c0 + oc) * rows + r0 + r8) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 // out = res + sigmoid(gp + bg) * (y + by); g saved
@@ -337,6 +384,18 @@ int evo_trimul_gate_bwd(const void* proj, int64_t ld, const float* b_ap, const f
 int evo_transpose2d(const void* x, int x_dtype, void* y, int y_dtype, int64_t rows, int64_t cols,
                     void* stream) {
   EVO_API_BEGIN
+  if (y_dtype == EVO_BF16 && rows % 64 == 0 && cols % 64 == 0 && rows / 64 <= 65535 && al16(x) && al16(y)) {
+    dim3 g64((unsigned)(cols / 64), (unsigned)(rows / 64));
+    if (x_dtype == EVO_BF16)
+      transpose_vec_kernel<__nv_bfloat16><<<g64, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x,
+                                                                                 (__nv_bfloat16*)y, rows, cols);
+    else
+      transpose_vec_kernel<float><<<g64, 256, 0, (cudaStream_t)stream>>>((const float*)x, (__nv_bfloat16*)y, rows,
+                                                                         cols);
+    EVO_LAUNCH_CHECK();
+    count_launch(1);
+    return EVO_OK;
+  }
   dim3 grid(cdiv(cols, TT), cdiv(rows, TT));
   EVO_DISPATCH_T(x_dtype, TI, EVO_DISPATCH_T(y_dtype, TO, {
     transpose_kernel<TI, TO><<<grid, 256, 0, (cudaStream_t)stream>>>((const TI*)x, (TO*)y, rows, cols);

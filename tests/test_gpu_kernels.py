@@ -562,3 +562,16 @@ def test_pair_bias_bwd_emits_next_operand(swap):
     assert torch.equal(dz, dzf) and torch.equal(dg, dgf) and torch.equal(db, dbf) and torch.equal(dw, dwf)
     assert torch.equal(d16, dzf.bfloat16())
     assert rel(dsum, dzf.double().sum(0).float()) <= 1e-5
+
+
+@pytest.mark.parametrize("rows,cols,src", [(128, 4096, "bf16"), (4096, 128, "f32"), (96, 200, "bf16")])
+def test_transpose2d_vs_torch(rows, cols, src):
+    """evo_transpose2d (TriMul's channel-major <-> token-major re-layouts): the
+    16-byte tiled kernel (multiples of 64) and the scalar one, exact."""
+    from paper_2207_05477_b200 import ops
+    torch.manual_seed(rows + cols)
+    x = torch.randn(rows, cols, device="cuda")
+    if src == "bf16":
+        x = x.bfloat16()
+    y = ops.transpose2d(x, torch.bfloat16)
+    assert torch.equal(y, x.t().contiguous().bfloat16())
