@@ -114,6 +114,14 @@ __device__ __forceinline__ void tmem_zero(uint32_t taddr) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// 8 bf16 added into global memory at L2 (round-to-nearest).  Used only where
+// exactly two addends meet a zeroed destination, so the result does not depend
+// on their arrival order (0 + a + b == 0 + b + a: fp addition commutes)
+__device__ __forceinline__ void red_add_bf16x8(void* p, const uint4& v) {
+  asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
 
 template <int D, int LP>
 __device__ __forceinline__ void bwd_stage(uint8_t* st, const bf16* qkvg, const bf16* dctx,
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     const bf16* __restrict__ qkvg, const bf16* __restrict__ dctx, const float* __restrict__ mbias,
     const bf16* __restrict__ nb, const float* __restrict__ lse, const float* __restrict__ Dvec,
     bf16* __restrict__ dqkvg, bf16* __restrict__ kvpart, float* __restrict__ dnb_part,
-    AttnGeom g, float scale, int NG, bf16* __restrict__ qpart, int NKW) {
+    AttnGeom g, float scale, int NG, bf16* __restrict__ qpart, int NKW, int kv_red) {
   using SM = BwdSmem<D, LP>;
   constexpr int DC = D / 8;
   constexpr int NKC = LP / 128;
@@ -340,11 +348,18 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
 #pragma unroll
         for (int e = 0; e < DH; e += 2) pk[e / 2] = tc::pack_bf16(vv[e] * sc, vv[e + 1] * sc);
         const int64_t t = g.tok(b, key);
-        bf16* dst = (qt == 0) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
-                              : kvpart + (qt - 1) * Ttok * 2 * HD + t * 2 * HD + region * HD + h * D + chalf * DH;
+        bf16* dst = (qt == 0 || kv_red) ? dqkvg + t * g.ld + (1 + region) * HD + h * D + chalf * DH
+                                        : kvpart + (qt - 1) * Ttok * 2 * HD + t * 2 * HD + region * HD + h * D + chalf * DH;
+        if (kv_red) {
+          // two query tiles: both add into the zeroed dK/dV slices (no combine pass)
 #pragma unroll
-        for (int k = 0; k < DH / 8; ++k)
-          reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+          for (int k = 0; k < DH / 8; ++k)
+            red_add_bf16x8(dst + 8 * k, make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < DH / 8; ++k)
+            reinterpret_cast<uint4*>(dst)[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+        }
       }
     };
     auto drain_dq = [&](int64_t b) {
@@ -521,7 +536,8 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
     const bf16* __restrict__ ctx, const bf16* __restrict__ gate, const bf16* __restrict__ dgated,
     bf16* __restrict__ dqkvg, bf16* __restrict__ dctx, float* __restrict__ Dvec, int64_t T, int H,
     int64_t ld, const float* __restrict__ mask, int64_t msb, int64_t msl, float* __restrict__ mbias,
-    int64_t B, int64_t L, int64_t sb, int64_t sl, const float* __restrict__ lse, float* __restrict__ gpart) {
+    int64_t B, int64_t L, int64_t sb, int64_t sl, const float* __restrict__ lse, float* __restrict__ gpart,
+    int zero_kv) {
   // key-mask bias of every (batch, key), [b][l] contiguous, in the log2
   // domain of the softmax: (m - 1) * 1e9 * log2(e)  (src/attention.py:151)
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * L;
@@ -591,6 +607,10 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_tc_kernel(
         }
         *reinterpret_cast<uint4*>(dctx + c) = make_uint4(pc[0], pc[1], pc[2], pc[3]);
         *reinterpret_cast<uint4*>(dqkvg + t * ld + 3 * HD8 * 8 + c8 * 8) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+        if (zero_kv) {  // the dK / dV slices the backward's two query tiles add into
+          st_zero16(dqkvg + t * ld + HD8 * 8 + c8 * 8);
+          st_zero16(dqkvg + t * ld + 2 * HD8 * 8 + c8 * 8);
+        }
       }
 #pragma unroll
       for (int o = G / 2; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
@@ -694,7 +714,7 @@ bool tc_disabled() {
 }
 
 struct BwdPlan {
-  int NQT, NG, LP, NKW;
+  int NQT, NG, LP, NKW, kv_red;
   int64_t off_dctx, off_dvec, off_mb, off_kv, off_q, off_part, off_cols, total;
 };
 
@@ -712,6 +732,15 @@ BwdPlan bwd_plan(const AttnGeom& g) {
   if (ng < 1) ng = 1;
   if (ng > g.B) ng = (int)g.B;
   p.NG = ng;
+  // two query tiles over one key window: dK/dV by reduction stores into slices
+  // the prep kernel zeroed (order-independent with two addends) instead of a
+  // partial plane and a combine pass (EVO_ATTN_KV_RED=0 restores the latter)
+  static int kvr = -1;
+  if (kvr < 0) {
+    const char* e = getenv("EVO_ATTN_KV_RED");
+    kvr = (e && e[0] == '0') ? 0 : 1;
+  }
+  p.kv_red = (kvr == 1 && p.NQT == 2 && p.NKW == 1) ? 1 : 0;
   const int64_t T = g.B * g.L;  // tokens covered by the problem set
   const int64_t HD = g.H * g.D;
   auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
@@ -747,7 +776,7 @@ void launch_bwd(const void* qkvg, const bf16* dctx, const float* mask, const voi
   dim3 grid((unsigned)p.NG, (unsigned)g.H, (unsigned)(p.NQT * p.NKW));
   const float scale = (float)(1.0 / sqrt((double)D));
   k<<<grid, 544, SM::total, s>>>((const bf16*)qkvg, dctx, mask, (const bf16*)nb, lse, Dvec,
-                                 (bf16*)dqkvg, kvpart, part, g, scale, p.NG, qpart, p.NKW);
+                                 (bf16*)dqkvg, kvpart, part, g, scale, p.NG, qpart, p.NKW, p.kv_red);
   EVO_LAUNCH_CHECK();
   count_launch(1);
 }
@@ -800,12 +829,12 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
       attn_bwd_prep_tc_kernel<16><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart, p.kv_red);
     else
       attn_bwd_prep_tc_kernel<32><<<pgrid, 256, 0, s>>>((const bf16*)ctx, (const bf16*)gate,
                                                          (const bf16*)dgated, (bf16*)dqkvg, dctx,
                                                          Dvec, T, (int)g.H, g.ld, mask, g.msb, g.msl,
-                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart);
+                                                         mbias, g.B, g.L, g.sb, g.sl, lse, gpart, p.kv_red);
     EVO_LAUNCH_CHECK();
   }
   if (gfuse) finalize_partials(gpart, (int)pgrid, HD, dbg, accumulate, s);
@@ -818,7 +847,7 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
     attn_part_combine_kernel<<<cdiv(T * 3 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, qpart, p.NKW - 1, kvpart,
                                                                         p.NQT - 1, T, g.ld, HD);
     EVO_LAUNCH_CHECK();
-  } else if (p.NQT > 1) {
+  } else if (p.NQT > 1 && !p.kv_red) {
     attn_kv_combine_kernel<<<cdiv(T * 2 * HD / 8, 256), 256, 0, s>>>((bf16*)dqkvg, kvpart, T, g.ld, HD);
     EVO_LAUNCH_CHECK();
   }
@@ -838,7 +867,7 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
   }
   // prep, the combine pass, the bias-gradient reduction, the column-slice
   // sum (the main kernel, colsum_vec and finalize_partials count themselves)
-  count_launch(1 + (p.NKW > 1 || p.NQT > 1) + bias + slice);
+  count_launch(1 + (p.NKW > 1 || (p.NQT > 1 && !p.kv_red)) + bias + slice);
   return true;
 }
 
