@@ -22,6 +22,16 @@
 
 namespace evo {
 
+#ifdef EVO_BWD_TRACE
+// phase timestamps of CTA (0, 0, 0): softmax warps 0 / 15 and the MMA warp
+// (tools/bwd_trace.py; a -DEVO_BWD_TRACE build from tools/build_trace.py --
+// its extra registers spill, so read phases relative to each other)
+__device__ long long g_bwd_trace[8192];
+#define BT(base, slot) do { if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0) g_bwd_trace[(base) + (slot)] = clock64(); } while (0)
+#else
+#define BT(base, slot) do {} while (0)
+#endif
+
 bool colsum_vec(void* x, int xdt, int64_t ldx, const void* h, void* y, int ydt, float* out,
                 int accumulate, void* ws, int64_t rows, int64_t C, int mode, cudaStream_t s);
 
@@ -281,19 +291,24 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     for (int64_t j = 0; j < nsub; ++j) {
       const int sj = (int)(j % NSUB);
       const uint32_t st = s0 + (uint32_t)((j / NSUB) & 1) * SM::STAGE;
+      const int tb = 2048 + 8 * (int)(j & 127);
+      BT(tb, 0);
       tc::mbar_wait(&bar2[0], phSf);
       phSf ^= 1;
       tc::fence_after();
+      BT(tb, 1);
       if (j + 1 < nsub) {
         const int sj2 = (int)((j + 1) % NSUB);
         const uint32_t st2 = s0 + (uint32_t)(((j + 1) / NSUB) & 1) * SM::STAGE;
         issue_sdp<D>(st2, sj2 * 64, tbase, C_S, C_DP, &bar[0], SM::q, SM::o, SM::k, SM::v);
       }
+      BT(tb, 2);
       if (sj & 1) {
         const int kc = sj >> 1;
         tc::mbar_wait(&bar2[1], phP);
         phP ^= 1;
         tc::fence_after();
+        BT(tb, 3);
         // dQ += dS Kc ; dK = dS^T Q ; dV = P^T dO   (chunk of 128 keys)
         const uint64_t b_k = tc::sdesc(st + SM::k + (kc * 16) * DC * 128, DC * 128, 128);
         const uint64_t b_q = tc::sdesc(st + SM::q, DC * 128, 128);
@@ -308,6 +323,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
                             k > 0 ? 1u : 0u);
         }
         tc::mma_commit_w(&bar[1]);
+        BT(tb, 4);
       }
     }
   } else if (b_lo < b_hi) {
@@ -417,9 +433,12 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           mbv[e] = t4.x, mbv[e + 1] = t4.y, mbv[e + 2] = t4.z, mbv[e + 3] = t4.w;
         }
         // ---- S/dP(j) out of TMEM, then hand the columns back ----
+        const int tb = (warp == 0 ? 0 : (warp == NCW - 1 ? 4096 : 6144)) + 16 * (int)(((b - b_lo) * NSUB + sj) & 127);
+        BT(tb, 0);
         tc::mbar_wait(&bar[0], phS);
         phS ^= 1;
         tc::fence_after();
+        BT(tb, 1);
         float s[16], dp[16], acc[16];
         tc::tmem_ld16(tl + C_S + cg * 16, s);
         tc::tmem_ld16(tl + C_DP + cg * 16, dp);
@@ -438,6 +457,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         }
         tc::fence_before();
         tc::mbar_arrive_warp(&bar2[0]);
+        BT(tb, 2);
         // ---- P, dS, bias gradient ----
         uint32_t pp[8], pd[8];
 #pragma unroll
@@ -455,11 +475,13 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           pd[e / 2] = tc::pack_bf16(d.x, d.y);
         }
         if (BIAS) tmem_st16(tl + C_DB + c0, acc);
+        BT(tb, 3);
         // ---- previous chunk's dQ/dK/dV: wait, drain, recycle its staging ----
         if (sub == 0 && kv_pending) {
           tc::mbar_wait(&bar[1], phKV);
           phKV ^= 1;
           tc::fence_after();
+          BT(tb, 4);
           drain_kv(pend_b, pend_c);
           if (pend_c == NKC - 1) {
             drain_dq(pend_b);
@@ -468,6 +490,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
             cp_async_commit();
           }
           kv_pending = false;
+          BT(tb, 5);
         }
         // ---- P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B ----
         const int kcol = sub * 64 + cg * 16;
@@ -477,10 +500,12 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
           *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
         }
+        BT(tb, 6);
         if (sub == 1) {
           tc::fence_proxy_async();
           tc::fence_before();
           tc::mbar_arrive_warp(&bar2[1]);
+          BT(tb, 7);
           kv_pending = true;
           pend_b = b;
           pend_c = kc;
@@ -872,3 +897,9 @@ bool attn_bwd_tc_try(const void* qkvg, const float* mask, const void* nb, const 
 }
 
 }  // namespace evo
+
+#ifdef EVO_BWD_TRACE
+extern "C" int evo_bwd_trace_read(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, evo::g_bwd_trace, sizeof(long long) * n);
+}
+#endif
