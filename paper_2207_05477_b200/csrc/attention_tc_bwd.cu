@@ -13,8 +13,10 @@
 //   per 128-key chunk: dQ += dS K, dK = dS^T Q, dV = P^T dO on the tensor
 //   core (MN-major operand descriptors read the same shared tiles
 //   transposed), drained to HBM.
-// Query tile 1 (keys seen from queries 128..255) writes its dK/dV partial to
-// a workspace that a small combine kernel adds in (two addends, exact order).
+// With two query tiles (L <= 256) both add their dK/dV into slices the prep
+// kernel zeroed, by bf16x8 reduction stores: two addends onto zero give the
+// same bits in either arrival order.  More query tiles or key windows write
+// partials that a combine kernel adds in fixed order.
 #include "common.cuh"
 #include "reduce.cuh"
 #include "attn_geom.cuh"
