@@ -693,6 +693,26 @@ __global__ void __launch_bounds__(GT) pack_cols_kernel(const __grid_constant__ P
   }
 }
 
+// the same with 8 consecutive columns per thread (16-byte / 32-byte vector
+// accesses, 32-bit index math): N % 8 == 0 and 16-byte aligned bases
+template <typename TS, typename TD>
+__global__ void __launch_bounds__(GT) pack_cols8_kernel(const __grid_constant__ PackBatch pb) {
+  const PackDesc& d = pb.d[blockIdx.y];
+  const int N8 = (int)(d.N / 8), row8 = d.ns * N8, n8 = (int)d.C * row8;
+  for (int e = blockIdx.x * GT + threadIdx.x; e < n8; e += gridDim.x * GT) {
+    const int c = e / row8, r = e - c * row8;
+    const int s = r / N8, j = (r - s * N8) * 8;
+    float v[8];
+    if (!pb.unpack) {
+      ld8(reinterpret_cast<const TS*>(d.src[s]) + (int64_t)c * d.N + j, v);
+      st8(reinterpret_cast<TD*>(d.dst[0]) + (int64_t)e * 8, v);
+    } else {
+      ld8(reinterpret_cast<const TS*>(d.src[0]) + (int64_t)e * 8, v);
+      st8(reinterpret_cast<TD*>(d.dst[s]) + (int64_t)c * d.N + j, v);
+    }
+  }
+}
+
 // rec[i, j] = 1 / (sum_s m[s, i0 + i] m[s, j] + 1e-3)   (block per local row i; exact
 // integer sums).  i0 > 0: the rows of one DAP shard (src/model.py:351-378 sharded)
 __global__ void __launch_bounds__(GT) opm_rec_vec_kernel_(const float* __restrict__ mask,
@@ -755,6 +775,18 @@ void pack_cols(const void* const* src, void* const* dst, const int64_t* C, const
       pb.d[k].N = N[i];
       pb.d[k].ns = ns;
       maxe = std::max<int64_t>(maxe, C[i] * ns * N[i]);
+    }
+    bool v8 = maxe < (1ll << 31);
+    for (int k = 0; k < pb.n && v8; ++k) {
+      v8 = pb.d[k].N % 8 == 0;
+      for (int q = 0; q < ns; ++q) v8 = v8 && al16(pb.d[k].src[unpack ? 0 : q]) && al16(pb.d[k].dst[unpack ? q : 0]);
+    }
+    if (v8) {
+      dim3 grid((unsigned)std::min<int64_t>((maxe / 8 + GT - 1) / GT, 1024), (unsigned)pb.n);
+      EVO_DISPATCH_T(sdt, TS, EVO_DISPATCH_T(ddt, TD, { pack_cols8_kernel<TS, TD><<<grid, GT, 0, s>>>(pb); }));
+      EVO_LAUNCH_CHECK();
+      count_launch(1);
+      continue;
     }
     dim3 grid((unsigned)std::min<int64_t>((maxe + GT - 1) / GT, 1024), (unsigned)pb.n);
     EVO_DISPATCH_T(sdt, TS, EVO_DISPATCH_T(ddt, TD, { pack_cols_kernel<TS, TD><<<grid, GT, 0, s>>>(pb); }));
