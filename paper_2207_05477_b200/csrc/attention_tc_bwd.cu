@@ -350,8 +350,9 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     if (b_lo + 1 < b_hi) bwd_stage<D, LP>(smem + SM::STAGE, qkvg, dctx, mbias, g, b_lo + 1, h, q0, tid, k0);
     cp_async_commit();
 
-    // drain dK / dV of chunk c of batch b: lanes = keys, cg -> (dK|dV, column half)
-    auto drain_kv = [&](int64_t b, int c) {
+    // drain dK / dV of chunk c of batch b: lanes = keys, cg -> (dK|dV, column half);
+    // ``mid`` runs while the TMEM load is in flight
+    auto drain_kv = [&](int64_t b, int c, auto&& mid) {
       const int key = k0 + c * 128 + row;
       const int region = cg >> 1, chalf = cg & 1;
       constexpr int DH = D / 2;
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
       const uint32_t col = (region ? C_DV : C_DK) + chalf * DH;
       if constexpr (DH == 16) tc::tmem_ld16(tl + col, vv);
       else tc::tmem_ld8(tl + col, vv);
+      mid();
       tc::wait_ld();
       if (key < L) {
         const float sc = region ? 1.0f : scale;
@@ -478,13 +480,27 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         }
         if (BIAS) tmem_st16(tl + C_DB + c0, acc);
         BT(tb, 3);
+        // ---- P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B ----
+        // (stored once the previous chunk's dQ/dK/dV MMAs, which read the tile, are complete)
+        auto store_pds = [&]() {
+          const int kcol = sub * 64 + cg * 16;
+#pragma unroll
+          for (int qd = 0; qd < 2; ++qd) {
+            const int off = ((row >> 3) * 16 + (kcol >> 3) + qd) * 64 + (row & 7) * 8;
+            *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
+            *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
+          }
+        };
+        bool pds_stored = false;
         // ---- previous chunk's dQ/dK/dV: wait, drain, recycle its staging ----
         if (sub == 0 && kv_pending) {
           tc::mbar_wait(&bar[1], phKV);
           phKV ^= 1;
           tc::fence_after();
           BT(tb, 4);
-          drain_kv(pend_b, pend_c);
+          // this sub-chunk's P / dS go to shared memory while the dK/dV load is in flight
+          drain_kv(pend_b, pend_c, store_pds);
+          pds_stored = true;
           if (pend_c == NKC - 1) {
             drain_dq(pend_b);
             // every MMA that read batch b-1's buffer is complete: prefetch b+1 into it
@@ -494,14 +510,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           kv_pending = false;
           BT(tb, 5);
         }
-        // ---- P / dS tile [128 q x 128 k]: core (row/8, kcol/8) at ((row/8)*16 + kcol/8)*128 B ----
-        const int kcol = sub * 64 + cg * 16;
-#pragma unroll
-        for (int qd = 0; qd < 2; ++qd) {
-          const int off = ((row >> 3) * 16 + (kcol >> 3) + qd) * 64 + (row & 7) * 8;
-          *reinterpret_cast<uint4*>(sP + off) = make_uint4(pp[4 * qd], pp[4 * qd + 1], pp[4 * qd + 2], pp[4 * qd + 3]);
-          *reinterpret_cast<uint4*>(sdS + off) = make_uint4(pd[4 * qd], pd[4 * qd + 1], pd[4 * qd + 2], pd[4 * qd + 3]);
-        }
+        if (!pds_stored) store_pds();
         BT(tb, 6);
         if (sub == 1) {
           tc::fence_proxy_async();
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
     if (kv_pending) {
       tc::mbar_wait(&bar[1], phKV);
       tc::fence_after();
-      drain_kv(pend_b, pend_c);
+      drain_kv(pend_b, pend_c, [] {});
       drain_dq(pend_b);
     }
   } else if (BIAS) {  // empty batch group: zero bias-gradient partial
