@@ -382,18 +382,14 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         }
       }
     };
-    auto drain_dq = [&](int64_t b) {
-      constexpr int DQ = D / 4;
-      float vv[8];
-      if constexpr (DQ == 8) {
-        tc::tmem_ld8(tl + C_DQ + cg * DQ, vv);
-      } else {
-        float v4[4];
-        tmem_ld4(tl + C_DQ + cg * DQ, v4);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) vv[e] = v4[e];
-      }
-      tc::wait_ld();
+    // dQ of batch b: the TMEM load (dq_issue) and, after a tcgen05.wait::ld, the
+    // store (dq_store) -- split so the load can overlap other work
+    constexpr int DQ = D / 4;
+    auto dq_issue = [&](float (&vv)[DQ]) {
+      if constexpr (DQ == 8) tc::tmem_ld8(tl + C_DQ + cg * DQ, vv);
+      else tmem_ld4(tl + C_DQ + cg * DQ, vv);
+    };
+    auto dq_store = [&](int64_t b, const float (&vv)[DQ]) {
       if (valid) {
         const int64_t t = g.tok(b, i);
         bf16* dst = (kw == 0) ? dqkvg + t * g.ld + h * D + cg * DQ
@@ -406,6 +402,12 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
         else
           *reinterpret_cast<uint2*>(dst) = make_uint2(pk[0], pk[1]);
       }
+    };
+    auto drain_dq = [&](int64_t b) {
+      float vv[DQ];
+      dq_issue(vv);
+      tc::wait_ld();
+      dq_store(b, vv);
     };
 
 #pragma unroll 1
@@ -498,15 +500,30 @@ __global__ void __launch_bounds__(544, 1) attn_bwd_tc_kernel(
           phKV ^= 1;
           tc::fence_after();
           BT(tb, 4);
-          // this sub-chunk's P / dS go to shared memory while the dK/dV load is in flight
-          drain_kv(pend_b, pend_c, store_pds);
-          pds_stored = true;
+          // this sub-chunk's P / dS go to shared memory while the dK/dV load is
+          // in flight; at a batch boundary also the dQ load and the prefetch of
+          // batch b+1 into batch b-1's buffer (every MMA that read it is complete)
           if (pend_c == NKC - 1) {
-            drain_dq(pend_b);
-            // every MMA that read batch b-1's buffer is complete: prefetch b+1 into it
-            if (has_next) bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mbias, g, b + 1, h, q0, tid, k0);
-            cp_async_commit();
+            float vq[DQ];
+            // (the prefetch inside the load window measured faster for one key
+            // chunk per batch -- col 105 -> 97 us -- and slower for two -- tri
+            // 197.5 -> 200 us -- so with two it follows the dQ store)
+            auto stage_next = [&] {
+              if (has_next)
+                bwd_stage<D, LP>(smem + (buf ^ 1) * SM::STAGE, qkvg, dctx, mbias, g, b + 1, h, q0, tid, k0);
+              cp_async_commit();
+            };
+            drain_kv(pend_b, pend_c, [&] {
+              dq_issue(vq);
+              store_pds();
+              if (NKC == 1) stage_next();
+            });
+            dq_store(pend_b, vq);
+            if (NKC > 1) stage_next();
+          } else {
+            drain_kv(pend_b, pend_c, store_pds);
           }
+          pds_stored = true;
           kv_pending = false;
           BT(tb, 5);
         }
